@@ -1,0 +1,289 @@
+/*
+ * smo_oracle.c -- plain, slow, fp64 CPU oracle of the binary SMO solve.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference leg may load this library.  The product path
+ * (paper_2311_14908_b200/, libsvmb200.so) never links, imports or calls it, and it
+ * shares no code, header, table or constant with the CUDA path.
+ *
+ * What it follows (PAPER.md = "P:L<line>", SPEC.md = "S:L<line>"):
+ *   - problem: binary soft-margin kernel SVM dual QP, y in {+1,-1}     P:L132-133 (§3.1)
+ *   - kernels: linear x.y, Gaussian RBF exp(-gamma ||x-y||^2)
+ *   - SMO: two multipliers per step "under the KKT constraints"         P:L140 (§3.2)
+ *     with the maximal-violating-pair rule, f, I_up/I_low, tie-break,
+ *     stopping rule, bias, eta-degenerate rule
+ *   - "convergence checks ... for every set of iterations"              P:L144; tested
+ *     every iteration here (reading R6)
+ *
+ * Everything is fp64; X is read as float32 and widened exactly.  Rounding-order
+ * readings: squared distance and dot product accumulate in
+ * ascending feature order, one fma per term; exp is correctly rounded (computed in
+ * double-double and rounded once); kernel arguments below -708 give K = 0.
+ *
+ * Pins (tests/test_oracle_*.py): closed-form two/three-point duals, RBF two-point,
+ * eta = 0 duplicates, separable toy with known margin, brute-force active-set QP,
+ * KKT at convergence, invariants per step, mpmath-rounded exp.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <float.h>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define ORACLE_LINEAR 0
+#define ORACLE_RBF 1
+
+/* ------------------------------------------------------------------ double-double */
+typedef struct { double hi, lo; } dd_t;
+
+static dd_t fast_two_sum(double a, double b) {   /* |a| >= |b| */
+    dd_t r; r.hi = a + b; r.lo = b - (r.hi - a); return r;
+}
+static dd_t two_sum(double a, double b) {
+    dd_t r; r.hi = a + b; double bb = r.hi - a; r.lo = (a - (r.hi - bb)) + (b - bb); return r;
+}
+static dd_t two_prod(double a, double b) {
+    dd_t r; r.hi = a * b; r.lo = fma(a, b, -r.hi); return r;
+}
+static dd_t dd_add(dd_t a, dd_t b) {
+    dd_t s = two_sum(a.hi, b.hi), t = two_sum(a.lo, b.lo);
+    s.lo += t.hi; s = fast_two_sum(s.hi, s.lo);
+    s.lo += t.lo; return fast_two_sum(s.hi, s.lo);
+}
+static dd_t dd_mul(dd_t a, dd_t b) {
+    dd_t p = two_prod(a.hi, b.hi);
+    p.lo += a.hi * b.lo + a.lo * b.hi;
+    return fast_two_sum(p.hi, p.lo);
+}
+static dd_t dd_div_d(dd_t a, double b) {          /* a / b, ~2^-104 relative */
+    double q1 = a.hi / b;
+    dd_t p = two_prod(q1, b);
+    double r = ((a.hi - p.hi) - p.lo + a.lo) / b;
+    return fast_two_sum(q1, r);
+}
+
+/* ln 2 and 1/i! in double-double, computed here from their series (no tables). */
+static dd_t g_ln2;
+static dd_t g_invfact[16];
+static int g_init = 0;
+static long g_exp_ambiguous = 0;
+
+static void oracle_init(void) {
+    if (g_init) return;
+    /* ln 2 = sum_{k>=1} 1 / (k 2^k); 120 terms reach far below 2^-110. */
+    dd_t s = {0.0, 0.0};
+    for (int k = 120; k >= 1; --k) {
+        dd_t term = {ldexp(1.0, -k), 0.0};
+        s = dd_add(s, dd_div_d(term, (double)k));
+    }
+    g_ln2 = s;
+    g_invfact[0].hi = 1.0; g_invfact[0].lo = 0.0;
+    for (int i = 1; i < 16; ++i) g_invfact[i] = dd_div_d(g_invfact[i - 1], (double)i);
+    g_init = 1;
+}
+
+/*
+ * Correctly rounded exp(x) for x in [-708, 0] (the RBF argument range); the
+ * reading of "exp" in P:L179 / S:L120 is the exact exponential rounded once.
+ *   x = k ln2 + r, |r| <= ln2/2          (r in double-double)
+ *   exp(r) = (sum_{i<=12} (r/256)^i / i!)^(2^8)    (double-double, ~2^-96 rel.)
+ *   exp(x) = 2^k exp(r), then one rounding to double.
+ * A result whose double-double value lies within 2^-88 (relative) of a rounding
+ * boundary is counted in g_exp_ambiguous (tests assert it stays 0).
+ */
+double oracle_exp_cr(double x) {
+    oracle_init();
+    if (x == 0.0) return 1.0;
+    if (x < -708.0) return 0.0;
+    double k = nearbyint(x / g_ln2.hi);
+    dd_t kl = two_prod(k, g_ln2.hi);                    /* exact */
+    dd_t r = two_sum(x, -kl.hi);                        /* exact */
+    r = dd_add(r, (dd_t){-kl.lo, 0.0});
+    r = dd_add(r, (dd_t){-k * g_ln2.lo, 0.0});
+    dd_t y = {ldexp(r.hi, -8), ldexp(r.lo, -8)};
+    dd_t p = g_invfact[12];
+    for (int i = 11; i >= 0; --i) p = dd_add(dd_mul(p, y), g_invfact[i]);
+    for (int i = 0; i < 8; ++i) p = dd_mul(p, p);
+    /* p is normalised (p.hi = RN(p.hi + p.lo)); 2^k scaling is exact because
+     * x >= -708 keeps the result >= 2^-1021 (normal). */
+    if (p.lo != 0.0) {
+        double nb = p.lo > 0 ? nextafter(p.hi, INFINITY) : nextafter(p.hi, -INFINITY);
+        double half_gap = fabs(nb - p.hi) * 0.5;
+        if (fabs(fabs(p.lo) - half_gap) <= ldexp(p.hi, -88)) g_exp_ambiguous++;
+    }
+    return ldexp(p.hi, (int)k);
+}
+
+long oracle_exp_ambiguous_count(void) { return g_exp_ambiguous; }
+
+/* ------------------------------------------------------------------------ kernels */
+/* ||a - b||^2, ascending k, one fma per term (reading R13). */
+static double sqdist(const float* a, const float* b, int64_t d) {
+    double acc = 0.0;
+    for (int64_t k = 0; k < d; ++k) {
+        double t = (double)a[k] - (double)b[k];   /* exact */
+        acc = fma(t, t, acc);
+    }
+    return acc;
+}
+/* a . b, ascending k (fp32 x fp32 products are exact in fp64). */
+static double dot(const float* a, const float* b, int64_t d) {
+    double acc = 0.0;
+    for (int64_t k = 0; k < d; ++k) acc = fma((double)a[k], (double)b[k], acc);
+    return acc;
+}
+
+/* K(a, b): S:L119-127.  same != 0 marks the diagonal (RBF K_ii == 1). */
+double oracle_kernel(int kernel, double gamma, const float* a, const float* b, int64_t d, int same) {
+    if (kernel == ORACLE_LINEAR) return dot(a, b, d);
+    if (same) return 1.0;
+    double arg = -(gamma * sqdist(a, b, d));
+    return oracle_exp_cr(arg);
+}
+
+/* row i of K over all n samples: S:L128-136 (kernel_row). */
+void oracle_kernel_row(int kernel, double gamma, const float* X, int64_t n, int64_t d,
+                       int64_t i, double* out) {
+    for (int64_t j = 0; j < n; ++j)
+        out[j] = oracle_kernel(kernel, gamma, X + i * d, X + j * d, d, i == j);
+}
+
+/* --------------------------------------------------------------------- selection */
+/* i_up = argmin f over I_up, i_low = argmax f over I_low, ties -> lowest
+ * index.  Returns 0 when either set is empty. */
+int oracle_select(const double* f, const int8_t* y, const double* alpha, double C, int64_t n,
+                  int64_t* i_up, int64_t* i_low, double* b_up, double* b_low) {
+    int64_t u = -1, l = -1;
+    double fu = 0.0, fl = 0.0;
+    for (int64_t j = 0; j < n; ++j) {
+        int in_up = (y[j] == 1 && alpha[j] < C) || (y[j] == -1 && alpha[j] > 0.0);
+        int in_low = (y[j] == 1 && alpha[j] > 0.0) || (y[j] == -1 && alpha[j] < C);
+        if (in_up && (u < 0 || f[j] < fu)) { u = j; fu = f[j]; }
+        if (in_low && (l < 0 || f[j] > fl)) { l = j; fl = f[j]; }
+    }
+    *i_up = u; *i_low = l; *b_up = fu; *b_low = fl;
+    return (u >= 0 && l >= 0);
+}
+
+/* ------------------------------------------------------------------------- train */
+/*
+ * SMO, step by step (SURVEY.md §8(c) pseudo-code):
+ *   alpha = 0, f = -y
+ *   loop: select (u, l); if b_low - b_up <= 2 tol: converged
+ *         if it == max_iter: stop, not converged
+ *         eta = K_uu + K_ll - 2 K_ul
+ *         t = min(t_u, t_l, gap / max(eta, 1e-12))        (clip to the box; eta rule S:L251)
+ *         alpha_u += y_u t, alpha_l -= y_l t, snapped to the bound when clipped
+ *         f_j += c_u K(u, j) + c_l K(l, j)
+ *   b = -(b_up + b_low) / 2
+ * Optional warm start (alpha0 and f0 both non-NULL) resumes a saved state.
+ * pair_trace (nullable) receives (i_up, i_low) per update.
+ * Returns 0 on success, -3 on a single-class problem, -1 on bad arguments.
+ */
+int oracle_svm_train(const float* X, const int8_t* y, int64_t n, int64_t d, double C,
+                     int kernel, double gamma, double tol, int64_t max_iter,
+                     const double* alpha0, const double* f0,
+                     double* alpha, double* f, double* b_out, int64_t* iters_out,
+                     int* converged_out, double* b_up_out, double* b_low_out,
+                     int64_t* pair_trace, int64_t trace_cap) {
+    oracle_init();
+    if (n < 2 || d < 1 || !(C > 0.0) || !(tol > 0.0)) return -1;
+    if (kernel == ORACLE_RBF && !(gamma > 0.0)) return -1;
+    int has_pos = 0, has_neg = 0;
+    for (int64_t j = 0; j < n; ++j) {
+        if (y[j] == 1) has_pos = 1; else if (y[j] == -1) has_neg = 1; else return -2;
+    }
+    if (!has_pos || !has_neg) return -3;
+    if (max_iter <= 0) max_iter = (10 * n > 10000) ? 10 * n : 10000;
+
+    for (int64_t j = 0; j < n; ++j) {
+        alpha[j] = alpha0 ? alpha0[j] : 0.0;
+        f[j] = f0 ? f0[j] : -(double)y[j];
+    }
+    int64_t it = 0;
+    int converged = 0;
+    double b_up = 0.0, b_low = 0.0;
+    for (;;) {
+        int64_t u, l;
+        if (!oracle_select(f, y, alpha, C, n, &u, &l, &b_up, &b_low)) { converged = 1; break; }
+        if (b_low - b_up <= 2.0 * tol) { converged = 1; break; }
+        if (it == max_iter) break;
+
+        const float* xu = X + u * d;
+        const float* xl = X + l * d;
+        double Kuu = oracle_kernel(kernel, gamma, xu, xu, d, 1);
+        double Kll = oracle_kernel(kernel, gamma, xl, xl, d, 1);
+        double Kul = oracle_kernel(kernel, gamma, xu, xl, d, u == l);
+        double eta = Kuu + Kll - 2.0 * Kul;
+        double gap = b_low - b_up;
+        double yu = (double)y[u], yl = (double)y[l];
+        double tu = (y[u] == 1) ? C - alpha[u] : alpha[u];
+        double tl = (y[l] == 1) ? alpha[l] : C - alpha[l];
+        double t = gap / (eta > 1e-12 ? eta : 1e-12);
+        if (tu < t) t = tu;
+        if (tl < t) t = tl;
+        double au = (t == tu) ? (y[u] == 1 ? C : 0.0) : alpha[u] + yu * t;
+        double al = (t == tl) ? (y[l] == 1 ? 0.0 : C) : alpha[l] - yl * t;
+        double cu = yu * (au - alpha[u]);
+        double cl = yl * (al - alpha[l]);
+        alpha[u] = au;
+        alpha[l] = al;
+        if (pair_trace && it < trace_cap) { pair_trace[2 * it] = u; pair_trace[2 * it + 1] = l; }
+
+        #pragma omp parallel for schedule(static) if (n * d > 65536)
+        for (int64_t j = 0; j < n; ++j) {
+            double ku = oracle_kernel(kernel, gamma, xu, X + j * d, d, j == u);
+            double kl = oracle_kernel(kernel, gamma, xl, X + j * d, d, j == l);
+            f[j] = fma(cl, kl, fma(cu, ku, f[j]));
+        }
+        ++it;
+    }
+    *b_out = -(b_up + b_low) / 2.0;
+    *iters_out = it;
+    *converged_out = converged;
+    *b_up_out = b_up;
+    *b_low_out = b_low;
+    return 0;
+}
+
+/* dec(x) = sum_s coef_s K(x_s, x) + b, coef = alpha * y, ascending s. */
+void oracle_decision(const float* Xsv, const double* coef, int64_t nsv, int64_t d, double b,
+                     int kernel, double gamma, const float* Xt, int64_t m, double* dec) {
+    oracle_init();
+    #pragma omp parallel for schedule(static) if (m * nsv * d > 65536)
+    for (int64_t i = 0; i < m; ++i) {
+        double acc = 0.0;
+        for (int64_t s = 0; s < nsv; ++s)
+            acc += coef[s] * oracle_kernel(kernel, gamma, Xsv + s * d, Xt + i * d, d, 0);
+        dec[i] = acc + b;
+    }
+}
+
+/* W(alpha) = sum alpha - 1/2 sum_ij alpha_i alpha_j y_i y_j K_ij, O(n^2 d). */
+double oracle_dual_objective(const float* X, const int8_t* y, const double* alpha, int64_t n,
+                             int64_t d, int kernel, double gamma) {
+    oracle_init();
+    double lin = 0.0, quad = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+        lin += alpha[i];
+        if (alpha[i] == 0.0) continue;
+        for (int64_t j = 0; j < n; ++j) {
+            if (alpha[j] == 0.0) continue;
+            quad += alpha[i] * alpha[j] * (double)y[i] * (double)y[j]
+                    * oracle_kernel(kernel, gamma, X + i * d, X + j * d, d, i == j);
+        }
+    }
+    return lin - 0.5 * quad;
+}
+
+int oracle_num_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}

@@ -1,0 +1,191 @@
+"""Pins of the oracle's SMO against the QP it solves (§3.1-3.2):
+brute-force active-set enumeration on tiny inputs, KKT conditions at convergence,
+per-step invariants, primal-dual gap, determinism.  The Gram matrices here are built
+with numpy (independent of the oracle's kernel code).  CPU only."""
+import itertools
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+
+def np_gram(X, kind, gamma):
+    X = X.astype(np.float64)
+    if kind == O.LINEAR:
+        return X @ X.T
+    D = ((X[:, None, :] - X[None, :, :]) ** 2).sum(-1)
+    return np.exp(-gamma * D)
+
+
+def np_W(alpha, y, K):
+    v = alpha * y
+    return alpha.sum() - 0.5 * v @ K @ v
+
+
+def brute_force_qp(K, y, C):
+    """max W(a) s.t. 0 <= a <= C, sum a y = 0 by enumerating every (0 / C / free)
+    pattern and solving the KKT system of the free set with the equality multiplier."""
+    n = len(y)
+    y = y.astype(np.float64)
+    Q = (y[:, None] * y[None, :]) * K
+    best, best_a = -np.inf, None
+    for pat in itertools.product((0, 1, 2), repeat=n):
+        pat = np.array(pat)
+        F = np.where(pat == 2)[0]
+        a = np.where(pat == 1, C, 0.0).astype(np.float64)
+        if len(F):
+            B = np.where(pat != 2)[0]
+            m = len(F)
+            A = np.zeros((m + 1, m + 1))
+            A[:m, :m] = Q[np.ix_(F, F)]
+            A[:m, m] = y[F]
+            A[m, :m] = y[F]
+            rhs = np.zeros(m + 1)
+            rhs[:m] = 1.0 - Q[np.ix_(F, B)] @ a[B]
+            rhs[m] = -(y[B] @ a[B])
+            sol, *_ = np.linalg.lstsq(A, rhs, rcond=None)
+            a[F] = sol[:m]
+        if np.any(a < -1e-12) or np.any(a > C + 1e-12) or abs(a @ y) > 1e-10:
+            continue
+        a = np.clip(a, 0, C)
+        w = np_W(a, y, K)
+        if w > best:
+            best, best_a = w, a
+    return best, best_a
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_smo_matches_brute_force_qp(seed):
+    rng = np.random.default_rng(100 + seed)
+    n = int(rng.integers(3, 7))
+    d = int(rng.integers(1, 4))
+    X = (rng.standard_normal((n, d)) * 1.5).astype(np.float32)
+    y = np.where(rng.random(n) < 0.5, 1, -1).astype(np.int8)
+    y[0], y[1] = 1, -1
+    kind = O.RBF if seed % 2 else O.LINEAR
+    gamma = 0.7 if kind == O.RBF else 0.0
+    C = float(rng.choice([0.5, 1.0, 5.0]))
+    K = np_gram(X, kind, gamma)
+    Wbf, _ = brute_force_qp(K, y, C)
+    r = O.train(X, y, C, kind, gamma, tol=1e-10, max_iter=200000)
+    assert r.converged
+    Wsmo = np_W(r.alpha, y.astype(float), K)
+    assert Wsmo == pytest.approx(Wbf, rel=1e-11, abs=1e-12)
+
+
+def test_against_scipy_qp():
+    """Independent solver cross-check (scipy SLSQP) on n = 12."""
+    scipy_opt = pytest.importorskip("scipy.optimize")
+    rng = np.random.default_rng(17)
+    X = rng.standard_normal((12, 3)).astype(np.float32)
+    y = np.where(X[:, 0] + 0.5 * rng.standard_normal(12) > 0, 1, -1).astype(np.int8)
+    y[0], y[1] = 1, -1
+    K = np_gram(X, O.RBF, 0.5)
+    yf = y.astype(float)
+    C = 2.0
+    res = scipy_opt.minimize(lambda a: -np_W(a, yf, K), np.full(12, 0.1),
+                             jac=lambda a: -(1 - yf * (K @ (a * yf))),
+                             bounds=[(0, C)] * 12,
+                             constraints=[{"type": "eq", "fun": lambda a: a @ yf, "jac": lambda a: yf}],
+                             method="SLSQP", options={"ftol": 1e-14, "maxiter": 1000})
+    r = O.train(X, y, C, O.RBF, 0.5, tol=1e-9)
+    assert np_W(r.alpha, yf, K) >= -res.fun - 1e-9
+    assert np_W(r.alpha, yf, K) == pytest.approx(-res.fun, rel=1e-7)
+
+
+def _kkt_violations(alpha, y, dec, C, tolp):
+    m = y * dec
+    v = 0
+    for a, mi in zip(alpha, m):
+        if a == 0.0:
+            v += mi < 1 - tolp
+        elif a == C:
+            v += mi > 1 + tolp
+        else:
+            v += abs(mi - 1) > tolp
+    return v
+
+
+@pytest.mark.parametrize("wl", ["W1", "W2", "W3", "W5"])
+def test_kkt_at_convergence(wl):
+    """S:L233-238 / S:L492: a converged model has 0 KKT violations at tol' = 2 tau;
+    decision values recomputed from scratch with numpy."""
+    from gen import workloads as W
+    w = W.get(wl)
+    X, y = w.train(min(w.n, 400))
+    r = O.train(X, y, w.C, w.kernel, w.gamma, w.tol)
+    assert r.converged
+    K = np_gram(X, w.kernel, w.gamma)
+    yf = y.astype(float)
+    dec = K @ (r.alpha * yf) + r.b
+    assert _kkt_violations(r.alpha, yf, dec, w.C, 2 * w.tol) == 0
+    # untrained, separable data -> every point violates
+    assert _kkt_violations(np.zeros_like(r.alpha), yf, np.zeros_like(dec), w.C, 1e-6) == len(y)
+
+
+def test_invariants_every_step():
+    """box feasibility, |sum alpha y| <= 1e-9, W non-decreasing, and f
+    equals its from-scratch value; checked after every one of the first 120 steps by
+    re-running with max_iter = k (the oracle is deterministic)."""
+    from gen import workloads as W
+    w = W.get("W5")
+    X, y = w.train(60)
+    K = np_gram(X, w.kernel, w.gamma)
+    yf = y.astype(float)
+    prev = -np.inf
+    for k in range(1, 121):
+        r = O.train(X, y, w.C, w.kernel, w.gamma, 1e-9, max_iter=k)
+        a = r.alpha
+        assert np.all(a >= 0) and np.all(a <= w.C)
+        assert abs(a @ yf) <= 1e-9
+        Wk = np_W(a, yf, K)
+        assert Wk >= prev - 1e-12
+        prev = Wk
+        np.testing.assert_allclose(r.f, K @ (a * yf) - yf, atol=1e-12)
+        if r.converged:
+            break
+
+
+def test_f_consistency_after_1000_steps():
+    """incrementally maintained f matches from-scratch within 1e-6 after 1000 steps."""
+    from gen import workloads as W
+    w = W.get("W2")
+    X, y = w.train(1500)
+    r = O.train(X, y, w.C, w.kernel, w.gamma, w.tol, max_iter=1000)
+    assert r.iterations == 1000
+    K = np_gram(X, w.kernel, w.gamma)
+    yf = y.astype(float)
+    np.testing.assert_allclose(r.f, K @ (r.alpha * yf) - yf, atol=1e-6)
+
+
+def test_primal_dual_gap_linear():
+    """Weak duality for the linear kernel: P(w, b) >= W(alpha), and the gap is small at
+    convergence."""
+    from gen import workloads as W
+    w = W.get("W1")
+    X, y = w.train()
+    r = O.train(X, y, w.C, O.LINEAR, 0.0, 1e-5)
+    yf = y.astype(float)
+    wv = ((r.alpha * yf)[:, None] * X.astype(np.float64)).sum(0)
+    P = 0.5 * wv @ wv + w.C * np.maximum(0, 1 - yf * (X.astype(np.float64) @ wv + r.b)).sum()
+    Wd = np_W(r.alpha, yf, np_gram(X, O.LINEAR, 0))
+    assert P >= Wd - 1e-9
+    assert (P - Wd) / P < 1e-3
+
+
+def test_openmp_threads_bit_identical():
+    """parallel and sequential execution give identical models."""
+    code = ("import sys, numpy as np; sys.path.insert(0, %r);"
+            "from oracle import oracle as O; from gen import workloads as W;"
+            "w = W.get('W3'); X, y = w.train(600);"
+            "r = O.train(X, y, w.C, w.kernel, w.gamma, w.tol);"
+            "sys.stdout.write(r.alpha.tobytes().hex() + ' ' + repr(r.b))") % os.path.dirname(os.path.dirname(__file__))
+    outs = []
+    for t in ("1", "4"):
+        env = dict(os.environ, OMP_NUM_THREADS=t)
+        outs.append(subprocess.check_output([sys.executable, "-c", code], env=env))
+    assert outs[0] == outs[1]
