@@ -1,0 +1,354 @@
+"""bench.py -- SVM train time-to-converge on B200 (BASELINE.json metric), one JSON line.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload W2]
+
+A step is one pass of the whole hot path over the workload: stage + SMO solve to
+convergence and batched prediction of the held-out rows
+(a11).  `value` is the time-to-converge of the solve (seconds, lower is better; mean of
+K steps, max over ranks), measured with CUDA events on the launching stream with the
+inputs already resident in HBM.  `e2e` is the same solve through the host C-ABI call
+(svm_train_ex / svm_predict) with host buffers, H2D/D2H inside the timed region.
+
+N > 1 is launched by torchrun (one process per GPU): the rows are sharded and every
+iteration exchanges per-CTA candidate records over NVLink (strong scaling: the problem
+is fixed).  --impl reference times the CPU oracle (oracle/) on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SVM train time-to-converge (s) & SMO iters/s at 1/2/4/8 B200; kernel-row HBM GB/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """Samples nvidia-smi during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        def run():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.check_output(
+                        ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                         "--format=csv,noheader,nounits"], timeout=5).decode().strip()
+                    self.rows.append([c.strip() for c in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 5 + i and r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def oracle_sample(w, X, y, budget_s: float, iters_total: int):
+    """Time the oracle as it stands on the head of this workload's trajectory, about
+    budget_s seconds of CPU work; returns (iters/s, iterations run, threads)."""
+    from oracle import oracle as O
+    t0 = time.perf_counter()
+    O.train(X, y, w.C, w.kernel, w.gamma, w.tol, max_iter=5)
+    probe = max(time.perf_counter() - t0, 1e-6) / 5
+    k = int(max(5, min(iters_total, budget_s / probe)))
+    t0 = time.perf_counter()
+    r = O.train(X, y, w.C, w.kernel, w.gamma, w.tol, max_iter=k)
+    dt = time.perf_counter() - t0
+    return r.iterations / dt, r.iterations, O.num_threads()
+
+
+def golden_iterations(name: str):
+    import numpy as np
+    p = os.path.join(ROOT, "tests", "golden", f"{name}_oracle.npz")
+    if os.path.exists(p):
+        return int(np.load(p)["iterations"])
+    return None
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from gen import workloads as W
+    w = W.get(args.workload)
+    X, y = w.train()
+    iters = golden_iterations(args.workload)
+    per_step = []
+    k_iters = 0
+    threads = 1
+    for s in range(args.warmup + args.steps):
+        ips, k, threads = oracle_sample(w, X, y, args.ref_budget, iters or 10 ** 9)
+        if s >= args.warmup:
+            per_step.append(ips)
+            k_iters = k
+    ips = statistics.mean(per_step)
+    value = (iters / ips) if iters else None
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * k_iters / ips, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{w.name}: {w.config}", "n": w.n, "d": w.d},
+        "smo_iters_per_s": ips,
+        "cpu_baseline": {"value": value, "unit": "s", "cores": threads, "kind": "oracle",
+                         "sample": f"{k_iters} SMO iterations of {w.name} per step on {threads} host "
+                                   f"threads; time-to-converge projected with the oracle's own "
+                                   f"iteration count {iters}"},
+        "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2311_14908_b200 as S
+    from gen import workloads as W
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    S.lib()
+    w = W.get(args.workload)
+    X, y = w.train()
+    Xt, _ = w.test(args.predict_rows if args.predict_rows >= 0 else None)
+    n, d = X.shape
+    m = Xt.shape[0]
+    blocks = S.shard_rows(n, world)
+    lo, hi = blocks[rank]
+    stream = torch.cuda.current_stream()
+    Xd_full = torch.from_numpy(X).to(dev)
+    yd_full = torch.from_numpy(y).to(dev)
+    Xl = Xd_full[lo:hi].contiguous()
+    yl = yd_full[lo:hi].contiguous()
+    mt = -(-m // world)
+    tl, th = min(m, rank * mt), min(m, (rank + 1) * mt)
+    Xt_d = torch.from_numpy(Xt[tl:th]).to(dev).contiguous()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > L2 (126 MB)
+    comm = None
+    if world > 1:
+        uid = S.svm_comm_unique_id() if rank == 0 else bytes(128)
+        t = torch.tensor(list(uid), dtype=torch.uint8, device=dev)
+        dist.broadcast(t, 0)
+        comm = S.svm_comm_init(rank, world, bytes(t.cpu().tolist()), local)
+
+    def train_once():
+        if world == 1:
+            return S.svm_train_dev(Xd_full, yd_full, w.C, w.kernel, w.gamma, w.tol, stream=stream)
+        return S.svm_train_shard(comm, Xl, yl, lo, n, w.C, w.kernel, w.gamma, w.tol, stream=stream)
+
+    def predict_once(r):
+        # support vectors of the whole model (alpha gathered across ranks at N > 1)
+        alpha = r["alpha"]
+        if world > 1:
+            parts = [torch.empty(b[1] - b[0], dtype=torch.float64, device=dev) for b in blocks]
+            dist.all_gather(parts, alpha.contiguous())
+            alpha = torch.cat(parts)
+        sv = alpha > 1e-8
+        coef = (alpha * yd_full.to(torch.float64))[sv].contiguous()
+        Xsv = Xd_full[sv].contiguous()
+        return S.svm_predict_dev(Xsv, coef, r["b"], w.kernel, w.gamma, Xt_d, stream=stream), int(sv.sum())
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- warm-up
+    for _ in range(args.warmup):
+        r = train_once()
+        predict_once(r)
+    barrier()
+
+    # ---- timed steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    infos = []
+    nsv = 0
+    with Clocks(local) as clk:
+        barrier()
+        for k in range(args.steps):
+            flush.fill_(float(k))                      # L2 flush between steps
+            e0, e1, e2 = ev[k]
+            e0.record(stream)
+            r = train_once()
+            e1.record(stream)
+            _, nsv = predict_once(r)
+            e2.record(stream)
+            infos.append(r["info"])
+        barrier()
+    t_train = [a.elapsed_time(b) * 1e-3 for a, b, _ in ev]
+    t_step = [a.elapsed_time(c) * 1e-3 for a, _, c in ev]
+    t_solve = [i["seconds_solve"] for i in infos]
+    iters = infos[-1]["iterations"]
+    launches = infos[-1]["launches"]
+
+    def gmax(vals):
+        v = torch.tensor([statistics.mean(vals)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(v, op=dist.ReduceOp.MAX)
+        return float(v.item())
+
+    train_s = gmax(t_train)
+    step_s = gmax(t_step)
+    solve_s = gmax(t_solve)
+
+    # ---- e2e through the host C-ABI (host buffers; H2D/D2H inside the timed region)
+    e2e = None
+    if world == 1:
+        e2e_t = []
+        for k in range(max(1, min(args.steps, 3))):
+            flush.fill_(float(k))
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            rr = S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol)
+            svh = rr["alpha"] > 1e-8
+            S.svm_predict(X[svh], (rr["alpha"] * y)[svh], rr["b"], w.kernel, w.gamma, Xt)
+            e2e_t.append(time.perf_counter() - t0)
+        nsv_h = int(svh.sum())
+        e2e = {"value": statistics.mean(e2e_t), "unit": "s",
+               "h2d_bytes_per_step": int(n * d * 4 + n + nsv_h * d * 4 + nsv_h * 8 + m * d * 4),
+               "d2h_bytes_per_step": int(2 * n * 8 + m * 8),
+               "api": "svm_train_ex + svm_predict (host pointers)"}
+    else:
+        e2e_t = []
+        Xh = torch.from_numpy(X[lo:hi]).pin_memory()
+        yh = torch.from_numpy(y[lo:hi]).pin_memory()
+        ah = torch.empty(hi - lo, dtype=torch.float64).pin_memory()
+        for k in range(max(1, min(args.steps, 3))):
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            Xl.copy_(Xh, non_blocking=True); yl.copy_(yh, non_blocking=True)
+            rr = S.svm_train_shard(comm, Xl, yl, lo, n, w.C, w.kernel, w.gamma, w.tol, stream=stream)
+            ah.copy_(rr["alpha"], non_blocking=True)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            e2e_t.append(e0.elapsed_time(e1) * 1e-3)
+        e2e = {"value": gmax(e2e_t), "unit": "s",
+               "h2d_bytes_per_step": int((hi - lo) * (d * 4 + 1)),
+               "d2h_bytes_per_step": int((hi - lo) * 8),
+               "api": "svm_train_shard (pinned host -> device copies in the timed region)"}
+
+    # ---- roofline of the dominant kernel (smo_persistent): algorithmic bytes per
+    # iteration = the X rows streamed, n_r * d * 4 (state lives in shared memory)
+    hbm, peak_kind = peaks()
+    n_r = hi - lo
+    bytes_iter = n_r * d * 4
+    achieved = bytes_iter * iters / statistics.mean(t_solve) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_{w.name}.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    line = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            ips, k_it, thr = oracle_sample(w, X, y, args.cpu_budget, iters)
+            cpu = {"value": iters / ips, "unit": "s", "cores": thr, "kind": "oracle",
+                   "sample": f"first {k_it} SMO iterations of {w.name} (n={n}) on {thr} host threads "
+                             f"({ips:.1f} iters/s); time-to-converge projected to the {iters} iterations "
+                             f"of the identical trajectory"}
+        per_launch_launches = (1 + 2 + launches + 1) if world == 1 else (1 + 2 + launches + 1)
+        line = {
+            "metric": METRIC, "value": train_s, "unit": "s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{w.name}: {w.config}", "n": n, "d": d, "kernel": "rbf" if w.kernel else "linear",
+                       "gamma": w.gamma, "C": w.C, "tol": w.tol, "predict_rows": m, "n_sv": nsv,
+                       "parallelism": f"rows sharded over {world} GPU(s)", "l2": "flushed between steps (256 MB write)"},
+            "iterations": iters,
+            "smo_iters_per_s": iters / train_s,
+            "us_per_iter": 1e6 * solve_s / max(iters, 1),
+            "solve_s": solve_s,
+            "kernel_row_gbs": achieved,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
+                         "kernel": "smo_persistent", "bytes_per_iter": bytes_iter},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": per_launch_launches * args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        S.svm_comm_destroy(comm)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="W2")
+    ap.add_argument("--predict-rows", type=int, default=-1)
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--ref-budget", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,150 @@
+/*
+ * svmb200.h -- C ABI of the B200-native SMO SVM solver (libsvmb200.so).
+ *
+ * The library trains a binary soft-margin kernel SVM by SMO on NVIDIA B200 (sm_100a)
+ * and evaluates batched decision values.  Sources of the operations:
+ *   PAPER.md  = Elgarhy, "Support Vector Machine Implementation on MPI-CUDA and
+ *               Tensorflow Framework" (arXiv 2311.14908), cited "P:L<line>"
+ *   SPEC.md   = the derived CPU specification, cited "S:L<line>"
+ *
+ *   svm_train / svm_train_ex   the SMO solve of the dual QP
+ *       max_a  sum a_i - 1/2 sum_ij a_i a_j y_i y_j K(x_i, x_j)
+ *       s.t.   0 <= a_i <= C,  sum a_i y_i = 0                      (§3.1-3.2)
+ *     two multipliers per step "under the KKT constraints", the maximal
+ *     violating pair with lowest-index ties, f_i = sum_j a_j y_j K_ij - y_i, stop when
+ *     b_low - b_up <= 2 tol, b = -(b_up + b_low)/2
+ *     Kernels: linear x.z and RBF exp(-gamma ||x - z||^2)
+ *   svm_predict                dec(x) = sum_s coef_s K(x_s, x) + b
+ *
+ * Arithmetic contract: X is float32; every kernel value,
+ * the error vector f, the multipliers and all reductions are fp64; distances and
+ * dot products accumulate in ascending feature order with one fma per term; exp is
+ * correctly rounded.  Results are therefore identical to any implementation of the
+ * same readings (the repository's CPU oracle) bit for bit, and independent of the
+ * number of GPUs / CTAs the rows are spread over.
+ *
+ * Conventions
+ *   - Return value: SVM_OK (0) or a negative svm_status; svm_last_error() gives a
+ *     thread-local message for the last failing call on the calling thread.
+ *   - Non-convergence (max_iter reached) is success with info->converged = 0.
+ *   - Host entry points take host pointers; the caller owns every buffer, the library
+ *     copies inputs in and keeps no pointer after return.  Device entry points take
+ *     device pointers on the caller's stream and allocate only scratch, freed before
+ *     return.
+ *   - Layout: X row-major [n][d] float32; y int8 in {+1,-1}; alpha, f, coef, dec fp64.
+ *   - Calls are not re-entrant on one communicator.
+ */
+#ifndef SVMB200_H
+#define SVMB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum { SVM_LINEAR = 0, SVM_RBF = 1 } svm_kernel;
+
+typedef enum {
+    SVM_OK = 0,
+    SVM_EINVAL = -1,        /* n < 2, d < 1, C <= 0 or non-finite, tol <= 0, RBF gamma <= 0, null pointer */
+    SVM_ELABEL = -2,        /* a label outside {+1, -1} */
+    SVM_ESINGLECLASS = -3,  /* all labels equal */
+    SVM_ENONFINITE = -4,    /* NaN / Inf in X */
+    SVM_ENOMEM = -5,        /* device allocation failed, or a shard too large for the SMEM-resident state */
+    SVM_ECUDA = -6,         /* CUDA runtime error (message in svm_last_error) */
+    SVM_ENCCL = -7,         /* NCCL error during communicator setup */
+    SVM_ETIMEOUT = -8       /* a device-side wait for another CTA / rank exceeded its watchdog */
+} svm_status;
+
+/* Solver controls.  Zero / negative fields take the defaults shown. */
+typedef struct {
+    double C;               /* box bound, > 0 */
+    double gamma;           /* RBF width, > 0 (ignored for linear) */
+    double tol;             /* tau; <= 0 -> 1e-3; converged when b_low - b_up <= 2 tau */
+    int64_t max_iter;       /* <= 0 -> max(10 n, 10000) */
+    int32_t check_interval; /* <= 0 -> 64: the host-visible progress word is refreshed every
+                               check_interval iterations ("convergence checks ... for every set
+                               of iterations"); results do not depend on it */
+    int32_t kernel;         /* svm_kernel */
+    double sv_epsilon;      /* <= 0 -> 1e-8: support set {alpha > sv_epsilon} */
+    int32_t virtual_ranks;  /* <= 1 -> 1.  >1 splits the rows of ONE GPU into that many ranks
+                               that run the full multi-rank exchange protocol among CTA groups
+                               (test hook for the row-sharded path; results are identical) */
+    int32_t ctas;           /* <= 0 -> one CTA per SM; else the CTA count (test hook) */
+    int64_t iters_per_launch; /* <= 0 -> unlimited: the whole solve is one persistent launch */
+} svm_params;
+
+typedef struct {
+    int64_t iterations;     /* SMO pair updates performed */
+    int32_t converged;      /* 1: b_low - b_up <= 2 tol;  0: stopped at max_iter */
+    int32_t n_sv;           /* |{alpha > sv_epsilon}| */
+    double gap;             /* final b_low - b_up */
+    double b_up, b_low;     /* final min f over I_up, max f over I_low */
+    double dual_objective;  /* W = 1/2 sum_i alpha_i (1 - y_i f_i) */
+    double seconds_solve;   /* device time of the solver launches (CUDA events) */
+    double seconds_total;   /* host wall time of the call, including H2D / D2H */
+    int64_t launches;       /* persistent-kernel launches used */
+} svm_info;
+
+/* Optional debug / test hooks; a NULL svm_debug costs nothing. */
+typedef struct {
+    const double* alpha0;     /* warm start [n] (both alpha0 and f0, or neither) */
+    const double* f0;         /* warm start [n]: the error vector matching alpha0 */
+    double* f_out;            /* [n] out: final f */
+    int64_t* pair_trace;      /* [2 * pair_trace_cap] out: (i_up, i_low) of each update */
+    int64_t pair_trace_cap;
+} svm_debug;
+
+/* Train on host data.  alpha: [n] out (dense, zeros for non-SVs); b: out. */
+int svm_train(const float* X, const int8_t* y, int64_t n, int64_t d, double C, int kernel,
+              double gamma, double tol, double* alpha, double* b);
+
+/* Train on host data with full controls; info and dbg may be NULL. */
+int svm_train_ex(const float* X, const int8_t* y, int64_t n, int64_t d, const svm_params* p,
+                 double* alpha, double* b, svm_info* info, const svm_debug* dbg);
+
+/* Train on device data already resident in HBM (X row-major [n][d] float32, y int8),
+ * on `cuda_stream` (cudaStream_t, NULL = legacy default).  alpha (device, [n]) out,
+ * b and info host out; dbg pointers are host pointers. */
+int svm_train_dev(const float* X, const int8_t* y, int64_t n, int64_t d, const svm_params* p,
+                  double* alpha, double* b, svm_info* info, const svm_debug* dbg,
+                  void* cuda_stream);
+
+/* Decision values of m test rows (host pointers): dec[i] = sum_s coef_s K(sv_s, x_i) + b
+ * with coef_s = alpha_s y_s, summed in ascending s in fp64.  n_sv = 0 gives
+ * dec = b. */
+int svm_predict(const float* X_sv, const double* coef, int64_t n_sv, int64_t d, double b,
+                int kernel, double gamma, const float* X_test, int64_t m, double* dec);
+
+/* Same on device pointers and the caller's stream. */
+int svm_predict_dev(const float* X_sv, const double* coef, int64_t n_sv, int64_t d, double b,
+                    int kernel, double gamma, const float* X_test, int64_t m, double* dec,
+                    void* cuda_stream);
+
+/* ---- multi-GPU, one process per GPU (torchrun) -----------------------------------
+ * svm_comm_unique_id fills 128 bytes on rank 0 that the caller broadcasts (e.g. with
+ * torch.distributed); every rank then calls svm_comm_init.  svm_train_shard trains on
+ * the rank's contiguous row block [row_offset, row_offset + n_local) of an n_global-row
+ * problem; every rank must call it with the same parameters.  Device pointers; alpha_local
+ * receives the rank's slice of alpha.  Each iteration exchanges one 48-byte record per CTA
+ * with every peer over NVLink (peer stores + a monotonic arrival counter); results are
+ * bit-identical for any number of ranks. */
+int svm_comm_unique_id(uint8_t id[128]);
+int svm_comm_init(void** comm, int rank, int world, const uint8_t id[128], int device);
+int svm_train_shard(void* comm, const float* X_local, const int8_t* y_local, int64_t n_local,
+                    int64_t row_offset, int64_t n_global, int64_t d, const svm_params* p,
+                    double* alpha_local, double* b, svm_info* info, void* cuda_stream);
+void svm_comm_destroy(void* comm);
+
+/* Message for the last non-OK status returned on this thread ("" if none). */
+const char* svm_last_error(void);
+
+/* Library version string, e.g. "svmb200 0.1 sm_100a". */
+const char* svm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SVMB200_H */

@@ -1,0 +1,66 @@
+"""Build libsvmb200.so in-tree with nvcc for sm_100a (no torch extension machinery).
+
+  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo --fmad=false -shared ...
+
+--fmad=false keeps every product and sum the source writes as a separate rounding;
+the kernels request fused multiply-adds explicitly with fma() where the arithmetic
+contract has one.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+ROOT = os.path.dirname(HERE)
+LIB = os.path.join(HERE, "libsvmb200.so")
+SOURCES = ["svmb200.cu", "predict.cu", "comm.cu"]
+HEADERS = ["smo_kernel.cuh", "svm_exp.cuh", "exp_table.inc", "svm_internal.h", "predict_tc.cuh"]
+
+
+def _nccl_paths():
+    try:
+        import nvidia.nccl as _n  # the torch-bundled NCCL 2.28 (headers + libnccl.so.2)
+        base = os.path.dirname(_n.__file__) if _n.__file__ else list(_n.__path__)[0]
+    except Exception:
+        base = "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl"
+    return os.path.join(base, "include"), os.path.join(base, "lib")
+
+
+def nvcc() -> str:
+    for c in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", shutil.which("nvcc")):
+        if c and os.path.exists(c):
+            return c
+    raise RuntimeError("nvcc not found")
+
+
+def _stale() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "svmb200.h")]
+    return any(os.path.exists(p) and os.path.getmtime(p) > t for p in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not _stale():
+        return LIB
+    inc, lib = _nccl_paths()
+    srcs = [os.path.join(CSRC, f) for f in SOURCES if os.path.exists(os.path.join(CSRC, f))]
+    cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
+           "--fmad=false", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
+           "-Xptxas", "-v" if verbose else "-O3",
+           "-I", inc, "-I", os.path.join(ROOT, "include"),
+           "-o", LIB + ".tmp"] + srcs + [
+           "-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + lib, "-lcudart"]
+    cmd = [c for c in cmd if c]
+    subprocess.check_call(cmd)
+    os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

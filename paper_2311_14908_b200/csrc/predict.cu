@@ -1,0 +1,85 @@
+// predict.cu -- batched decision values:
+//   dec_i = sum_s coef_s K(sv_s, x_i) + b,   coef_s = alpha_s y_s.
+//
+// Exact path (this file, k_predict_exact): fp64 SIMT, one test row per thread, support
+// vectors consumed in blocks of SB with their feature chunks staged in shared memory;
+// each (i, s) distance accumulates in ascending k with one fma per term, the kernel
+// value is the correctly rounded exp, and the SB terms are added to the running sum in
+// ascending s -- the oracle's order, so decision values match it bit for bit.
+#include <cuda_runtime.h>
+
+#include "svm_exp.cuh"
+#include "svm_internal.h"
+
+namespace svmint {
+
+namespace {
+constexpr int TI = 256;   // test rows per CTA (one per thread)
+constexpr int SB = 8;     // support vectors per block
+constexpr int KC = 32;    // features per shared-memory chunk
+}
+
+template <int KERNEL>
+__global__ void __launch_bounds__(TI) k_predict_exact(const float* __restrict__ Xsv,
+                                                      const double* __restrict__ coef, long long nsv,
+                                                      int d, double b, double gamma,
+                                                      const float* __restrict__ Xt, long long m,
+                                                      double* __restrict__ dec) {
+    __shared__ float tt[KC][TI + 1];
+    __shared__ double sv[SB][KC];
+    const int tid = threadIdx.x;
+    const long long i0 = (long long)blockIdx.x * TI;
+    const long long i = i0 + tid;
+    double acc = 0.0;
+    for (long long s0 = 0; s0 < nsv; s0 += SB) {
+        const int nb = (int)((nsv - s0) < SB ? (nsv - s0) : SB);
+        double dist[SB];
+#pragma unroll
+        for (int s = 0; s < SB; ++s) dist[s] = 0.0;
+        for (int k0 = 0; k0 < d; k0 += KC) {
+            const int kc = (d - k0) < KC ? (d - k0) : KC;
+            __syncthreads();
+            for (int e = tid; e < TI * KC; e += TI) {
+                const int row = e / KC, kk = e % KC;
+                tt[kk][row] = (i0 + row < m && kk < kc) ? Xt[(i0 + row) * d + k0 + kk] : 0.0f;
+            }
+            for (int e = tid; e < SB * KC; e += TI) {
+                const int s = e / KC, kk = e % KC;
+                sv[s][kk] = (s < nb && kk < kc) ? (double)Xsv[(s0 + s) * d + k0 + kk] : 0.0;
+            }
+            __syncthreads();
+            for (int kk = 0; kk < kc; ++kk) {
+                const double x = tt[kk][tid];
+#pragma unroll
+                for (int s = 0; s < SB; ++s) {
+                    if (KERNEL == 1) {
+                        const double e = sv[s][kk] - x;
+                        dist[s] = fma(e, e, dist[s]);
+                    } else {
+                        dist[s] = fma(sv[s][kk], x, dist[s]);
+                    }
+                }
+            }
+        }
+        for (int s = 0; s < nb; ++s) {
+            const double K = (KERNEL == 1) ? svmexp::exp_cr(-(gamma * dist[s])) : dist[s];
+            acc = acc + coef[s0 + s] * K;
+        }
+    }
+    if (i < m) dec[i] = acc + b;
+}
+
+int predict_device(const float* X_sv, const double* coef, long long n_sv, long long d, double b,
+                   int kernel, double gamma, const float* X_test, long long m, double* dec,
+                   cudaStream_t st) {
+    const long long grid = (m + TI - 1) / TI;
+    if (grid > 0x7fffffffll) return fail(SVM_EINVAL, "too many test rows");
+    if (kernel == SVM_RBF)
+        k_predict_exact<1><<<(unsigned)grid, TI, 0, st>>>(X_sv, coef, n_sv, (int)d, b, gamma, X_test, m, dec);
+    else
+        k_predict_exact<0><<<(unsigned)grid, TI, 0, st>>>(X_sv, coef, n_sv, (int)d, b, gamma, X_test, m, dec);
+    CKR(cudaGetLastError());
+    return SVM_OK;
+}
+
+}  // namespace svmint

@@ -1,0 +1,160 @@
+// svm_exp.cuh -- correctly rounded fp64 exp for the RBF kernel, sm_100a + host.
+//
+// The RBF kernel is K(x, z) = exp(-gamma ||x - z||^2) (SPEC.md
+// L120).  The CUDA path evaluates exp correctly rounded (reading R14), so
+// every kernel value is the unique double nearest the exact exponential of the
+// fp64 argument; with identical arguments the trajectory of SMO pair choices is then
+// bit-reproducible against any other correctly rounded evaluation.
+//
+// Method (table-driven, two-phase / Ziv):
+//   x = (32 k + j) ln2/32 + r,  |r| <= ln2/64,  r in double-double (3-part ln2/32)
+//   exp(x) = 2^k * T_j * exp(r),  T_j = 2^(j/32) as double-double
+//   fast phase:  exp(r) = 1 + r + r^2/2 (double-double) + tail (double Horner,
+//                degree 3..10), relative error < 2^-72
+//   if the fast result lies within 2^-68 (relative) of a rounding boundary,
+//   slow phase:  exp(r) by a degree-13 double-double Horner (~2^-100)
+// Arguments below -708 return 0 (reading R15); x = 0 returns 1.
+// Domain used by the solver: x <= 0.  Constants: exp_table.inc
+// (tools/gen_exp_table.py, decimal arithmetic).
+//
+// Compiled with --fmad=false: products and sums below are never contracted.
+#pragma once
+
+#include <stdint.h>
+#include <string.h>
+#include <math.h>
+
+#include "exp_table.inc"
+
+#if defined(__CUDACC__)
+#define SVM_HD __host__ __device__ __forceinline__
+#else
+#define SVM_HD static inline
+#endif
+
+namespace svmexp {
+
+#if defined(__CUDACC__)
+__device__ const double d_T_hi[32] = {SVM_EXP_T_HI_INIT};
+__device__ const double d_T_lo[32] = {SVM_EXP_T_LO_INIT};
+__device__ const double d_IF_hi[16] = {SVM_EXP_IF_HI_INIT};
+__device__ const double d_IF_lo[16] = {SVM_EXP_IF_LO_INIT};
+#endif
+static const double h_T_hi[32] = {SVM_EXP_T_HI_INIT};
+static const double h_T_lo[32] = {SVM_EXP_T_LO_INIT};
+static const double h_IF_hi[16] = {SVM_EXP_IF_HI_INIT};
+static const double h_IF_lo[16] = {SVM_EXP_IF_LO_INIT};
+
+#if defined(__CUDA_ARCH__)
+#define SVM_TAB(name, i) __ldg(&d_##name[i])
+#else
+#define SVM_TAB(name, i) (h_##name[i])
+#endif
+
+struct dd { double hi, lo; };
+
+SVM_HD uint64_t bits_of(double x) {
+#if defined(__CUDA_ARCH__)
+    return (uint64_t)__double_as_longlong(x);
+#else
+    uint64_t u; memcpy(&u, &x, 8); return u;
+#endif
+}
+SVM_HD double from_bits(uint64_t u) {
+#if defined(__CUDA_ARCH__)
+    return __longlong_as_double((long long)u);
+#else
+    double x; memcpy(&x, &u, 8); return x;
+#endif
+}
+
+SVM_HD dd fast_two_sum(double a, double b) {  // |a| >= |b|
+    dd r; r.hi = a + b; r.lo = b - (r.hi - a); return r;
+}
+SVM_HD dd two_sum(double a, double b) {
+    dd r; r.hi = a + b; double bb = r.hi - a; r.lo = (a - (r.hi - bb)) + (b - bb); return r;
+}
+SVM_HD dd two_prod(double a, double b) {
+    dd r; r.hi = a * b; r.lo = fma(a, b, -r.hi); return r;
+}
+SVM_HD dd dd_mul(dd a, dd b) {
+    dd p = two_prod(a.hi, b.hi);
+    p.lo = p.lo + (a.hi * b.lo + a.lo * b.hi);
+    return fast_two_sum(p.hi, p.lo);
+}
+SVM_HD dd dd_add(dd a, dd b) {
+    dd s = two_sum(a.hi, b.hi);
+    dd t = two_sum(a.lo, b.lo);
+    s.lo = s.lo + t.hi;
+    s = fast_two_sum(s.hi, s.lo);
+    s.lo = s.lo + t.lo;
+    return fast_two_sum(s.hi, s.lo);
+}
+
+// Distance (in units of 2^-68 relative) from the nearest rounding boundary test:
+// returns true when (hi + lo) is provably on the same side of every boundary as
+// hi, i.e. RN(exact) == hi, given |exact - (hi + lo)| <= hi * 2^-shift.
+SVM_HD bool rounding_safe(double hi, double lo, int shift) {
+    uint64_t b = bits_of(hi);
+    uint64_t E = (b >> 52) & 0x7ffu;                       // hi is normal, in [0.98, 2)
+    double hg = from_bits((E - 53u) << 52);                // ulp(hi) / 2
+    bool pow2 = (b & 0xfffffffffffffull) == 0;
+    double g = (lo < 0.0 && pow2) ? 0.5 * hg : hg;
+    double margin = from_bits((E - (uint64_t)shift) << 52);  // 2^(e - shift) >= hi 2^-(shift+1)
+    return fabs(fabs(lo) - g) > margin;
+}
+
+SVM_HD double exp_cr(double x) {
+    if (x == 0.0) return 1.0;
+    if (x < -708.0) return 0.0;
+    double N = rint(x * SVM_EXP_INV_L32);
+    int Ni = (int)N;
+    int j = Ni & 31;
+    int k = (Ni - j) / 32;
+    // r = x - N ln2/32 as double-double
+    double r1 = fma(-N, SVM_EXP_L32_1, x);                 // exact (Sterbenz, 38-bit L1)
+    dd p2 = two_prod(N, SVM_EXP_L32_2);
+    dd s = two_sum(r1, -p2.hi);
+    double rlo = (s.lo - p2.lo) - N * SVM_EXP_L32_3;
+    dd r = two_sum(s.hi, rlo);
+    double rh = r.hi, rl = r.lo;
+    // fast phase
+    double t = SVM_TAB(IF_hi, 10);
+    t = fma(t, rh, SVM_TAB(IF_hi, 9));
+    t = fma(t, rh, SVM_TAB(IF_hi, 8));
+    t = fma(t, rh, SVM_TAB(IF_hi, 7));
+    t = fma(t, rh, SVM_TAB(IF_hi, 6));
+    t = fma(t, rh, SVM_TAB(IF_hi, 5));
+    t = fma(t, rh, SVM_TAB(IF_hi, 4));
+    t = fma(t, rh, SVM_TAB(IF_hi, 3));
+    double rh2 = rh * rh;
+    double tail = t * (rh2 * rh);
+    dd q = two_prod(rh, rh);
+    dd a = fast_two_sum(1.0, rh);
+    dd b = two_sum(a.hi, 0.5 * q.hi);
+    double lo = (a.lo + b.lo) + (rl + (0.5 * q.lo + (rh * rl + tail)));
+    dd S = fast_two_sum(b.hi, lo);
+    double Th = SVM_TAB(T_hi, j), Tl = SVM_TAB(T_lo, j);
+    dd P = two_prod(Th, S.hi);
+    double pl = P.lo + (Th * S.lo + Tl * S.hi);
+    dd R = fast_two_sum(P.hi, pl);
+#if defined(SVM_EXP_PROBE) && !defined(__CUDA_ARCH__)
+    svm_exp_probe_fast(R.hi * from_bits((uint64_t)(k + 1023) << 52),
+                       R.lo * from_bits((uint64_t)(k + 1023) << 52),
+                       !rounding_safe(R.hi, R.lo, 67));
+#endif
+    if (!rounding_safe(R.hi, R.lo, 67)) {
+        // slow phase: exp(r) with a degree-13 double-double Horner scheme
+        dd p; p.hi = SVM_TAB(IF_hi, 13); p.lo = SVM_TAB(IF_lo, 13);
+        for (int i = 12; i >= 0; --i) {
+            dd c; c.hi = SVM_TAB(IF_hi, i); c.lo = SVM_TAB(IF_lo, i);
+            p = dd_add(dd_mul(p, r), c);
+        }
+        dd T; T.hi = Th; T.lo = Tl;
+        R = dd_mul(p, T);
+    }
+    double scale = from_bits((uint64_t)(k + 1023) << 52);  // k >= -1022: normal
+    return R.hi * scale;
+}
+
+}  // namespace svmexp

@@ -1,0 +1,73 @@
+// svm_internal.h -- shared declarations of the host driver (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "../../include/svmb200.h"
+#include "smo_kernel.cuh"
+
+namespace svmint {
+
+extern thread_local std::string g_err;
+int fail(int code, const std::string& msg);
+
+#define CKR(x)                                                                          \
+    do {                                                                                \
+        cudaError_t e_ = (x);                                                           \
+        if (e_ != cudaSuccess)                                                          \
+            return ::svmint::fail(SVM_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+struct SolveOut {
+    long long iterations = 0;
+    int state = 0;
+    double b_up = 0, b_low = 0;
+    double seconds_solve = 0;
+    long long launches = 0;
+};
+
+struct SolveArgs;
+typedef int (*PreLaunchFn)(SolveArgs&, svmk::Params&);
+
+struct SolveArgs {
+    svm_params p;
+    long long n_global = 0, d = 0;
+    const float* xr = nullptr;                 // row-major replica [n_global][d] (device)
+    int world = 1, rank_base = 0, nranks_here = 1, ctas_per_rank = 1;
+    int n_sm = 0, max_smem = 0;
+    long long n_rows_max = 0;
+    long long row_off[svmk::MAXR] = {};
+    long long n_rows[svmk::MAXR] = {};
+    const float* x_rank[svmk::MAXR] = {};      // device rows of rank r, row-major
+    const int8_t* y_rank[svmk::MAXR] = {};
+    double* alpha_out[svmk::MAXR] = {};        // device alpha of rank r's rows
+    svmk::Mailbox* mbox[svmk::MAXR] = {};      // all ranks (peer pointers) unless local alloc
+    bool mbox_local_alloc = true;
+    const double* alpha0 = nullptr;            // device, global indexing (warm start)
+    const double* f0 = nullptr;
+    double* f_out = nullptr;                   // destination of f (global indexing if f_out_global)
+    cudaMemcpyKind f_out_kind = cudaMemcpyDeviceToHost;
+    bool f_out_global = true;
+    long long* trace = nullptr;                // host
+    long long trace_cap = 0;
+    cudaStream_t stream = nullptr;
+    long long timeout_ns = 20ll * 1000 * 1000 * 1000;
+    PreLaunchFn pre_launch = nullptr;
+    void* user = nullptr;
+    SolveOut out;
+};
+
+int check_params(long long n, long long d, const svm_params* p, svm_params* q);
+int validate_device(const float* X, const int8_t* y, long long n, long long d, cudaStream_t st,
+                    int* n_pos);
+int device_limits(int* n_sm, int* max_smem);
+int solve(SolveArgs& a);
+
+// predict.cu
+int predict_device(const float* X_sv, const double* coef, long long n_sv, long long d, double b,
+                   int kernel, double gamma, const float* X_test, long long m, double* dec,
+                   cudaStream_t st);
+
+}  // namespace svmint

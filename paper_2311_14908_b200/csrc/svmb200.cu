@@ -1,0 +1,537 @@
+// svmb200.cu -- C ABI (include/svmb200.h) and host driver of the B200 SMO solver.
+//
+// Stages:
+//   a1  stage + shard + init: validate, H2D (host entry points), build the CTA-blocked
+//       feature-major copy of each rank's rows (k_build_xblk), init alpha/f/flags
+//   a2-a7  the persistent kernel (smo_kernel.cuh), one cooperative launch per
+//       `iters_per_launch` iterations (default: the whole solve)
+//   a10 finalize: b = -(b_up + b_low)/2, D2H alpha, info
+//   a11 predict: predict.cu
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/svmb200.h"
+#include "smo_kernel.cuh"
+#include "svm_internal.h"
+
+using namespace svmk;
+
+namespace svmint {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+// ------------------------------------------------------------------ prep kernels
+// Blocked feature-major copy of one rank's rows: CTA c, tile t, feature k, row r ->
+// xblk[c * cta_stride + t * d_pad * rt + k * rows_pad4(t) + r]  (zero padded).
+__global__ void k_build_xblk(const float* __restrict__ X, long long n_r, int d, int d_pad,
+                             int G, int rt, long long cta_stride, float* __restrict__ xblk) {
+    const int c = blockIdx.y;
+    const long long r0 = (n_r * c) / G, r1 = (n_r * (c + 1)) / G;
+    const long long R = r1 - r0;
+    const long long total = R * d_pad;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long k = e / R;
+        const long long j = e - k * R;
+        const long long tile = j / rt, rin = j - tile * rt;
+        const long long rows_t = (R - tile * rt) < rt ? (R - tile * rt) : rt;
+        const long long rp = (rows_t + 3) & ~3ll;
+        const float v = (k < d) ? X[(r0 + j) * d + k] : 0.0f;
+        xblk[(long long)c * cta_stride + tile * (long long)d_pad * rt + k * rp + rin] = v;
+    }
+}
+
+__global__ void k_init_state(const int8_t* __restrict__ y, long long n, double C,
+                             const double* __restrict__ alpha0, const double* __restrict__ f0,
+                             double* __restrict__ f, double* __restrict__ alpha,
+                             uint8_t* __restrict__ flags) {
+    for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+         j += (long long)gridDim.x * blockDim.x) {
+        const int yj = y[j];
+        const double a = alpha0 ? alpha0[j] : 0.0;
+        alpha[j] = a;
+        f[j] = f0 ? f0[j] : -(double)yj;                       // f = -y at alpha = 0
+        flags[j] = flags_of(yj, a, C);
+    }
+}
+
+// counts[0] non-finite X, [1] labels outside {+1,-1}, [2] positives, [3] negatives
+__global__ void k_validate(const float* __restrict__ X, long long nx, const int8_t* __restrict__ y,
+                           long long n, unsigned long long* counts) {
+    unsigned long long bad = 0, lab = 0, pos = 0, neg = 0;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < nx;
+         e += (long long)gridDim.x * blockDim.x)
+        bad += !isfinite(X[e]);
+    for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+         j += (long long)gridDim.x * blockDim.x) {
+        const int v = y[j];
+        pos += v == 1; neg += v == -1; lab += (v != 1 && v != -1);
+    }
+    if (bad) atomicAdd(&counts[0], bad);
+    if (lab) atomicAdd(&counts[1], lab);
+    if (pos) atomicAdd(&counts[2], pos);
+    if (neg) atomicAdd(&counts[3], neg);
+}
+
+int validate_device(const float* X, const int8_t* y, long long n, long long d, cudaStream_t st,
+                    int* n_pos) {
+    unsigned long long* dc = nullptr;
+    CKR(cudaMallocAsync(&dc, 4 * sizeof(unsigned long long), st));
+    CKR(cudaMemsetAsync(dc, 0, 4 * sizeof(unsigned long long), st));
+    k_validate<<<1024, 256, 0, st>>>(X, n * d, y, n, dc);
+    unsigned long long hc[4];
+    CKR(cudaMemcpyAsync(hc, dc, sizeof(hc), cudaMemcpyDeviceToHost, st));
+    CKR(cudaFreeAsync(dc, st));
+    CKR(cudaStreamSynchronize(st));
+    if (hc[0]) return fail(SVM_ENONFINITE, "X contains " + std::to_string(hc[0]) + " non-finite values");
+    if (hc[1]) return fail(SVM_ELABEL, std::to_string(hc[1]) + " labels are not +1/-1");
+    if (hc[2] == 0 || hc[3] == 0) return fail(SVM_ESINGLECLASS, "single-class problem");
+    if (n_pos) *n_pos = (int)hc[2];
+    return SVM_OK;
+}
+
+int check_params(long long n, long long d, const svm_params* p, svm_params* q) {
+    if (!p) return fail(SVM_EINVAL, "null params");
+    *q = *p;
+    if (n < 2) return fail(SVM_EINVAL, "n < 2");
+    if (d < 1) return fail(SVM_EINVAL, "d < 1");
+    if (n > 0x7fffffffll) return fail(SVM_EINVAL, "n >= 2^31");
+    if (!(q->C > 0.0) || !std::isfinite(q->C)) return fail(SVM_EINVAL, "C must be finite and > 0");
+    if (q->kernel != SVM_LINEAR && q->kernel != SVM_RBF) return fail(SVM_EINVAL, "unknown kernel");
+    if (q->kernel == SVM_RBF && (!(q->gamma > 0.0) || !std::isfinite(q->gamma)))
+        return fail(SVM_EINVAL, "RBF gamma must be finite and > 0");
+    if (q->tol <= 0.0) q->tol = 1e-3;
+    if (!std::isfinite(q->tol)) return fail(SVM_EINVAL, "tol must be finite");
+    if (q->max_iter <= 0) q->max_iter = (10 * n > 10000) ? 10 * n : 10000;
+    if (q->check_interval <= 0) q->check_interval = 64;
+    if (q->sv_epsilon <= 0.0) q->sv_epsilon = 1e-8;
+    if (q->virtual_ranks <= 1) q->virtual_ranks = 1;
+    if (q->virtual_ranks > MAXR) return fail(SVM_EINVAL, "virtual_ranks > 8");
+    return SVM_OK;
+}
+
+// ------------------------------------------------------------------ planning
+struct Plan {
+    int G = 0;        // CTAs per rank
+    int rpt = 1, rt = 256, kc = 16, d_pad = 0, n_chunks = 0, stages = 0, state_cap = 0;
+    long long cta_stride = 0;
+    size_t smem = 0;
+};
+
+int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl) {
+    pl.G = G;
+    pl.state_cap = (int)((n_r_max + G - 1) / G);
+    if (pl.state_cap < 1) pl.state_cap = 1;
+    pl.rpt = (pl.state_cap >= 2 * NT * 4) ? 4 : 1;
+    pl.rt = NT * pl.rpt;
+    pl.kc = (pl.rt >= 1024) ? 4 : 16;
+    pl.d_pad = (d + pl.kc - 1) / pl.kc * pl.kc;
+    pl.n_chunks = pl.d_pad / pl.kc;
+    const int n_tiles = (pl.state_cap + pl.rt - 1) / pl.rt;
+    pl.cta_stride = (long long)n_tiles * pl.d_pad * pl.rt;
+    size_t fixed = (sizeof(Shared) + 127) & ~size_t(127);
+    fixed += 2 * (size_t)pl.d_pad * 8 + (size_t)pl.state_cap * 17;
+    fixed = (fixed + 127) & ~size_t(127);
+    const size_t stage_bytes = (size_t)pl.kc * pl.rt * 4;
+    if ((size_t)max_smem <= fixed + 2 * stage_bytes)
+        return fail(SVM_ENOMEM, "rows per CTA (" + std::to_string(pl.state_cap) +
+                                    ") exceed the shared-memory state capacity; shard over more GPUs");
+    pl.stages = (int)((max_smem - fixed) / stage_bytes);
+    if (pl.stages > MAX_STAGES) pl.stages = MAX_STAGES;
+    pl.smem = fixed + (size_t)pl.stages * stage_bytes;
+    return SVM_OK;
+}
+
+typedef void (*KernelFn)(const Params);
+
+KernelFn pick_kernel(int kernel, int rpt) {
+    if (kernel == SVM_RBF) return rpt == 4 ? smo_persistent<1, 4> : smo_persistent<1, 1>;
+    return rpt == 4 ? smo_persistent<0, 4> : smo_persistent<0, 1>;
+}
+
+int device_limits(int* n_sm, int* max_smem) {
+    int dev;
+    CKR(cudaGetDevice(&dev));
+    CKR(cudaDeviceGetAttribute(n_sm, cudaDevAttrMultiProcessorCount, dev));
+    CKR(cudaDeviceGetAttribute(max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    return SVM_OK;
+}
+
+// ------------------------------------------------------------------ the solve
+// Runs the solver for `nranks_here` ranks served by this process/launch.  Every rank r
+// of the problem (0..world-1) owns rows [row_off[r], row_off[r] + n_rows[r]).  For a
+// single-process solve (world == nranks_here) all pointers are local.
+int solve(SolveArgs& a) {
+    const svm_params& p = a.p;
+    Plan pl;
+    int rc = make_plan(a.n_rows_max, (int)a.d, a.ctas_per_rank, a.max_smem, pl);
+    if (rc) return rc;
+    KernelFn fn = pick_kernel(p.kernel, pl.rpt);
+    CKR(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+    int per_sm = 0;
+    CKR(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, NTHREADS, pl.smem));
+    const int grid = a.ctas_per_rank * a.nranks_here;
+    if (per_sm < 1 || grid > per_sm * a.n_sm)
+        return fail(SVM_ECUDA, "persistent grid of " + std::to_string(grid) + " CTAs is not co-resident");
+
+    cudaStream_t st = a.stream;
+    const int world = a.world;
+    const int g_total = world * a.ctas_per_rank;
+    const size_t mbox_bytes = sizeof(Mailbox) + 2 * (size_t)g_total * sizeof(Partial);
+
+    // ---- per-rank device state (a1)
+    std::vector<void*> owned;
+    auto dalloc = [&](void** ptr, size_t bytes) -> int {
+        cudaError_t e = cudaMallocAsync(ptr, bytes, st);
+        if (e != cudaSuccess) return fail(SVM_ENOMEM, std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
+        owned.push_back(*ptr);
+        return SVM_OK;
+    };
+    auto release = [&]() {
+        for (void* q : owned) cudaFreeAsync(q, st);
+        owned.clear();
+    };
+    Params P;
+    memset(&P, 0, sizeof(P));
+    P.kernel = p.kernel; P.gamma = p.gamma; P.C = p.C; P.tol = p.tol;
+    P.max_iter = p.max_iter; P.iter_limit = p.iters_per_launch > 0 ? p.iters_per_launch : 0;
+    P.d = (int)a.d; P.d_pad = pl.d_pad; P.kc = pl.kc; P.n_chunks = pl.n_chunks;
+    P.stages = pl.stages; P.rt = pl.rt;
+    P.world = world; P.rank_base = a.rank_base; P.ctas_per_rank = a.ctas_per_rank;
+    P.n_global = a.n_global; P.xr = a.xr; P.cta_stride = pl.cta_stride;
+    P.check_interval = p.check_interval; P.state_cap = pl.state_cap;
+    P.timeout_ns = a.timeout_ns;
+    for (int r = 0; r < world; ++r) { P.row_off[r] = a.row_off[r]; P.n_rows[r] = (int)a.n_rows[r]; P.mbox[r] = a.mbox[r]; }
+
+    for (int r = a.rank_base; r < a.rank_base + a.nranks_here; ++r) {
+        const long long nr = a.n_rows[r];
+        float* xb; double* f; double* al; uint8_t* fl; Ctl* ctl;
+        if ((rc = dalloc((void**)&xb, (size_t)pl.cta_stride * pl.G * 4 + 16))) { release(); return rc; }
+        if ((rc = dalloc((void**)&f, (size_t)nr * 8 + 8))) { release(); return rc; }
+        if ((rc = dalloc((void**)&fl, (size_t)nr + 8))) { release(); return rc; }
+        if ((rc = dalloc((void**)&ctl, sizeof(Ctl)))) { release(); return rc; }
+        al = a.alpha_out[r];
+        CKR(cudaMemsetAsync(xb, 0, (size_t)pl.cta_stride * pl.G * 4, st));
+        CKR(cudaMemsetAsync(ctl, 0, sizeof(Ctl), st));
+        dim3 bg(256, pl.G);
+        k_build_xblk<<<bg, 256, 0, st>>>(a.x_rank[r], nr, (int)a.d, pl.d_pad, pl.G, pl.rt, pl.cta_stride, xb);
+        k_init_state<<<256, 256, 0, st>>>(a.y_rank[r], nr, p.C, a.alpha0 ? a.alpha0 + a.row_off[r] : nullptr,
+                                          a.f0 ? a.f0 + a.row_off[r] : nullptr, f, al, fl);
+        CKR(cudaGetLastError());
+        P.xblk[r] = xb; P.f[r] = f; P.alpha[r] = al; P.flags[r] = fl; P.ctl[r] = ctl;
+        if (a.mbox_local_alloc) {
+            Mailbox* mb;
+            if ((rc = dalloc((void**)&mb, mbox_bytes))) { release(); return rc; }
+            CKR(cudaMemsetAsync(mb, 0, mbox_bytes, st));
+            P.mbox[r] = mb;
+        }
+    }
+    long long* dtrace = nullptr;
+    if (a.trace && a.trace_cap > 0) {
+        if ((rc = dalloc((void**)&dtrace, (size_t)a.trace_cap * 16))) { release(); return rc; }
+        CKR(cudaMemsetAsync(dtrace, 0xff, (size_t)a.trace_cap * 16, st));
+        P.trace = dtrace; P.trace_cap = a.trace_cap;
+    }
+    unsigned long long* progress_h = nullptr;
+    if (cudaHostAlloc(&progress_h, 64, cudaHostAllocMapped) == cudaSuccess) {
+        *progress_h = 0;
+        unsigned long long* pd = nullptr;
+        if (cudaHostGetDevicePointer(&pd, progress_h, 0) == cudaSuccess) P.progress = pd;
+    } else {
+        progress_h = nullptr;
+        cudaGetLastError();
+    }
+    if (a.pre_launch) {
+        rc = a.pre_launch(a, P);
+        if (rc) { release(); return rc; }
+    }
+
+    // ---- a2-a7: persistent launches
+    cudaEvent_t e0, e1;
+    CKR(cudaEventCreate(&e0));
+    CKR(cudaEventCreate(&e1));
+    CKR(cudaEventRecord(e0, st));
+    Ctl hc;
+    memset(&hc, 0, sizeof(hc));
+    long long launches = 0;
+    for (;;) {
+        void* args[] = {(void*)&P};
+        cudaError_t e = cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(NTHREADS), args, pl.smem, st);
+        if (e != cudaSuccess) { release(); return fail(SVM_ECUDA, std::string("cooperative launch: ") + cudaGetErrorString(e)); }
+        ++launches;
+        CKR(cudaMemcpyAsync(&hc, P.ctl[a.rank_base], sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+        CKR(cudaStreamSynchronize(st));
+        if (hc.state != ST_LIMIT) break;
+    }
+    CKR(cudaEventRecord(e1, st));
+    CKR(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    a.out.seconds_solve = ms * 1e-3;
+    a.out.launches = launches;
+    a.out.iterations = hc.it;
+    a.out.state = hc.state;
+    a.out.b_up = hc.b_up;
+    a.out.b_low = hc.b_low;
+    if (a.f_out) {
+        for (int r = a.rank_base; r < a.rank_base + a.nranks_here; ++r)
+            CKR(cudaMemcpyAsync(a.f_out + (a.f_out_global ? a.row_off[r] : 0), P.f[r],
+                                (size_t)a.n_rows[r] * 8, a.f_out_kind, st));
+    }
+    if (dtrace) {
+        const long long nt = hc.it < a.trace_cap ? hc.it : a.trace_cap;
+        CKR(cudaMemcpyAsync(a.trace, dtrace, (size_t)nt * 16, cudaMemcpyDeviceToHost, st));
+    }
+    release();
+    CKR(cudaStreamSynchronize(st));
+    if (progress_h) cudaFreeHost(progress_h);
+    if (hc.state == ST_TIMEOUT) return fail(SVM_ETIMEOUT, "device wait for the candidate exchange timed out");
+    if (hc.state != ST_CONVERGED && hc.state != ST_MAXITER)
+        return fail(SVM_ECUDA, "solver ended in state " + std::to_string(hc.state));
+    return SVM_OK;
+}
+
+// Single-process solve over p.virtual_ranks ranks of the current device.  X, y, alpha
+// are device pointers; alpha0/f0 (optional) device pointers; f_out any pointer of kind
+// f_kind; trace host.
+int train_device(const float* X, const int8_t* y, long long n, long long d, const svm_params& p,
+                 double* alpha, const double* alpha0, const double* f0, double* f_out,
+                 cudaMemcpyKind f_kind, long long* trace, long long trace_cap, cudaStream_t st,
+                 SolveOut& out) {
+    int n_sm = 0, max_smem = 0;
+    int rc = device_limits(&n_sm, &max_smem);
+    if (rc) return rc;
+    const int vr = p.virtual_ranks;
+    int ctas = p.ctas > 0 ? p.ctas : n_sm;
+    if (ctas > n_sm) ctas = n_sm;
+    const int cpr = ctas / vr;
+    if (cpr < 1) return fail(SVM_EINVAL, "more virtual ranks than CTAs");
+    SolveArgs a;
+    a.p = p;
+    a.n_global = n; a.d = d; a.xr = X;
+    a.world = vr; a.rank_base = 0; a.nranks_here = vr; a.ctas_per_rank = cpr;
+    a.n_sm = n_sm; a.max_smem = max_smem;
+    const long long per = (n + vr - 1) / vr;           // rank r owns [r per, min(n, (r+1) per))
+    for (int r = 0; r < vr; ++r) {
+        const long long lo = r * per < n ? r * per : n;
+        const long long hi = (r + 1) * per < n ? (r + 1) * per : n;
+        a.row_off[r] = lo; a.n_rows[r] = hi - lo;
+        if (a.n_rows[r] > a.n_rows_max) a.n_rows_max = a.n_rows[r];
+        a.x_rank[r] = X + lo * d;
+        a.y_rank[r] = y + lo;
+        a.alpha_out[r] = alpha + lo;
+    }
+    a.mbox_local_alloc = true;
+    a.stream = st;
+    a.alpha0 = alpha0; a.f0 = f0;
+    a.f_out = f_out; a.f_out_kind = f_kind; a.f_out_global = true;
+    a.trace = trace; a.trace_cap = trace ? trace_cap : 0;
+    rc = solve(a);
+    out = a.out;
+    return rc;
+}
+
+}  // namespace svmint
+
+using namespace svmint;
+
+namespace {
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+void fill_info(svm_info* info, const SolveOut& o, const svm_params& p, const double* alpha,
+               const double* f, const int8_t* y, long long n, double t_total) {
+    if (!info) return;
+    memset(info, 0, sizeof(*info));
+    info->iterations = o.iterations;
+    info->converged = (o.state == ST_CONVERGED);
+    info->b_up = o.b_up;
+    info->b_low = o.b_low;
+    info->gap = o.b_low - o.b_up;
+    info->seconds_solve = o.seconds_solve;
+    info->seconds_total = t_total;
+    info->launches = o.launches;
+    if (alpha) {
+        int nsv = 0;
+        double w = 0.0;
+        for (long long j = 0; j < n; ++j) {
+            nsv += alpha[j] > p.sv_epsilon;
+            if (f && y) w += alpha[j] * (1.0 - (double)y[j] * f[j]);
+        }
+        info->n_sv = nsv;
+        info->dual_objective = 0.5 * w;               // W = 1/2 sum a_i (1 - y_i f_i)
+    }
+}
+
+}  // namespace
+
+extern "C" int svm_train_ex(const float* X, const int8_t* y, int64_t n, int64_t d,
+                            const svm_params* p_in, double* alpha, double* b, svm_info* info,
+                            const svm_debug* dbg) {
+    const double t0 = now_s();
+    if (!X || !y || !alpha || !b) return fail(SVM_EINVAL, "null pointer");
+    svm_params p;
+    int rc = check_params(n, d, p_in, &p);
+    if (rc) return rc;
+    if (dbg && ((dbg->alpha0 == nullptr) != (dbg->f0 == nullptr)))
+        return fail(SVM_EINVAL, "warm start needs both alpha0 and f0");
+    cudaStream_t st;
+    CKR(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    float* dX = nullptr; int8_t* dy = nullptr; double* dA = nullptr; double* dA0 = nullptr; double* dF0 = nullptr;
+    std::vector<double> fbuf;
+    SolveOut o;
+    do {
+        if (cudaMallocAsync(&dX, (size_t)n * d * 4, st) != cudaSuccess ||
+            cudaMallocAsync(&dy, (size_t)n, st) != cudaSuccess ||
+            cudaMallocAsync(&dA, (size_t)n * 8, st) != cudaSuccess) {
+            rc = fail(SVM_ENOMEM, "device allocation of the training set failed");
+            break;
+        }
+        if (cudaMemcpyAsync(dX, X, (size_t)n * d * 4, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+            cudaMemcpyAsync(dy, y, (size_t)n, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+            rc = fail(SVM_ECUDA, "H2D copy failed");
+            break;
+        }
+        if (dbg && dbg->alpha0) {
+            if (cudaMallocAsync(&dA0, (size_t)n * 8, st) != cudaSuccess ||
+                cudaMallocAsync(&dF0, (size_t)n * 8, st) != cudaSuccess) {
+                rc = fail(SVM_ENOMEM, "warm start allocation failed");
+                break;
+            }
+            cudaMemcpyAsync(dA0, dbg->alpha0, (size_t)n * 8, cudaMemcpyHostToDevice, st);
+            cudaMemcpyAsync(dF0, dbg->f0, (size_t)n * 8, cudaMemcpyHostToDevice, st);
+        }
+        if ((rc = validate_device(dX, dy, n, d, st, nullptr))) break;
+        fbuf.resize((size_t)n);
+        rc = train_device(dX, dy, n, d, p, dA, dA0, dF0, fbuf.data(), cudaMemcpyDeviceToHost,
+                          dbg ? (long long*)dbg->pair_trace : nullptr, dbg ? dbg->pair_trace_cap : 0, st, o);
+        if (rc) break;
+        if (cudaMemcpyAsync(alpha, dA, (size_t)n * 8, cudaMemcpyDeviceToHost, st) != cudaSuccess) {
+            rc = fail(SVM_ECUDA, "D2H copy failed");
+            break;
+        }
+    } while (0);
+    if (dX) cudaFreeAsync(dX, st);
+    if (dy) cudaFreeAsync(dy, st);
+    if (dA) cudaFreeAsync(dA, st);
+    if (dA0) cudaFreeAsync(dA0, st);
+    if (dF0) cudaFreeAsync(dF0, st);
+    cudaError_t se = cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+    if (rc) return rc;
+    if (se != cudaSuccess) return fail(SVM_ECUDA, cudaGetErrorString(se));
+    *b = -(o.b_up + o.b_low) / 2.0;
+    if (dbg && dbg->f_out) memcpy(dbg->f_out, fbuf.data(), (size_t)n * 8);
+    fill_info(info, o, p, alpha, fbuf.data(), y, n, now_s() - t0);
+    return SVM_OK;
+}
+
+extern "C" int svm_train(const float* X, const int8_t* y, int64_t n, int64_t d, double C,
+                         int kernel, double gamma, double tol, double* alpha, double* b) {
+    svm_params p;
+    memset(&p, 0, sizeof(p));
+    p.C = C; p.kernel = kernel; p.gamma = gamma; p.tol = tol;
+    return svm_train_ex(X, y, n, d, &p, alpha, b, nullptr, nullptr);
+}
+
+extern "C" int svm_train_dev(const float* X, const int8_t* y, int64_t n, int64_t d,
+                             const svm_params* p_in, double* alpha, double* b, svm_info* info,
+                             const svm_debug* dbg, void* cuda_stream) {
+    const double t0 = now_s();
+    if (!X || !y || !alpha || !b) return fail(SVM_EINVAL, "null pointer");
+    svm_params p;
+    int rc = check_params(n, d, p_in, &p);
+    if (rc) return rc;
+    if (dbg && (dbg->alpha0 || dbg->f0)) return fail(SVM_EINVAL, "warm start is a host-API hook");
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    if ((rc = validate_device(X, y, n, d, st, nullptr))) return rc;
+    SolveOut o;
+    double* f_dev = nullptr;
+    CKR(cudaMallocAsync(&f_dev, (size_t)n * 8, st));
+    rc = train_device(X, y, n, d, p, alpha, nullptr, nullptr, f_dev, cudaMemcpyDeviceToDevice,
+                      dbg ? (long long*)dbg->pair_trace : nullptr, dbg ? dbg->pair_trace_cap : 0, st, o);
+    if (rc) { cudaFreeAsync(f_dev, st); return rc; }
+    *b = -(o.b_up + o.b_low) / 2.0;
+    if (info || (dbg && dbg->f_out)) {
+        std::vector<double> ha((size_t)n), hf((size_t)n);
+        std::vector<int8_t> hy((size_t)n);
+        CKR(cudaMemcpyAsync(ha.data(), alpha, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+        CKR(cudaMemcpyAsync(hf.data(), f_dev, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+        CKR(cudaMemcpyAsync(hy.data(), y, (size_t)n, cudaMemcpyDeviceToHost, st));
+        CKR(cudaStreamSynchronize(st));
+        if (dbg && dbg->f_out) memcpy(dbg->f_out, hf.data(), (size_t)n * 8);
+        fill_info(info, o, p, ha.data(), hf.data(), hy.data(), n, now_s() - t0);
+    }
+    CKR(cudaFreeAsync(f_dev, st));
+    return SVM_OK;
+}
+
+extern "C" int svm_predict_dev(const float* X_sv, const double* coef, int64_t n_sv, int64_t d,
+                               double b, int kernel, double gamma, const float* X_test, int64_t m,
+                               double* dec, void* cuda_stream) {
+    if (d < 1 || m < 0 || n_sv < 0) return fail(SVM_EINVAL, "bad sizes");
+    if (m == 0) return SVM_OK;
+    if (!dec || !X_test || (n_sv > 0 && (!X_sv || !coef))) return fail(SVM_EINVAL, "null pointer");
+    if (kernel != SVM_LINEAR && kernel != SVM_RBF) return fail(SVM_EINVAL, "unknown kernel");
+    if (kernel == SVM_RBF && !(gamma > 0.0)) return fail(SVM_EINVAL, "RBF gamma must be > 0");
+    return predict_device(X_sv, coef, n_sv, d, b, kernel, gamma, X_test, m, dec,
+                          (cudaStream_t)cuda_stream);
+}
+
+extern "C" int svm_predict(const float* X_sv, const double* coef, int64_t n_sv, int64_t d,
+                           double b, int kernel, double gamma, const float* X_test, int64_t m,
+                           double* dec) {
+    if (d < 1 || m < 0 || n_sv < 0) return fail(SVM_EINVAL, "bad sizes");
+    if (m == 0) return SVM_OK;
+    if (!dec || !X_test || (n_sv > 0 && (!X_sv || !coef))) return fail(SVM_EINVAL, "null pointer");
+    cudaStream_t st;
+    CKR(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    float *dS = nullptr, *dT = nullptr;
+    double *dC = nullptr, *dD = nullptr;
+    int rc = SVM_OK;
+    do {
+        if ((n_sv > 0 && (cudaMallocAsync(&dS, (size_t)n_sv * d * 4, st) != cudaSuccess ||
+                          cudaMallocAsync(&dC, (size_t)n_sv * 8, st) != cudaSuccess)) ||
+            cudaMallocAsync(&dT, (size_t)m * d * 4, st) != cudaSuccess ||
+            cudaMallocAsync(&dD, (size_t)m * 8, st) != cudaSuccess) {
+            rc = fail(SVM_ENOMEM, "device allocation for predict failed");
+            break;
+        }
+        if (n_sv > 0) {
+            cudaMemcpyAsync(dS, X_sv, (size_t)n_sv * d * 4, cudaMemcpyHostToDevice, st);
+            cudaMemcpyAsync(dC, coef, (size_t)n_sv * 8, cudaMemcpyHostToDevice, st);
+        }
+        cudaMemcpyAsync(dT, X_test, (size_t)m * d * 4, cudaMemcpyHostToDevice, st);
+        rc = svm_predict_dev(dS, dC, n_sv, d, b, kernel, gamma, dT, m, dD, st);
+        if (rc) break;
+        if (cudaMemcpyAsync(dec, dD, (size_t)m * 8, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+            rc = fail(SVM_ECUDA, "D2H copy failed");
+    } while (0);
+    if (dS) cudaFreeAsync(dS, st);
+    if (dC) cudaFreeAsync(dC, st);
+    if (dT) cudaFreeAsync(dT, st);
+    if (dD) cudaFreeAsync(dD, st);
+    cudaError_t se = cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+    if (rc) return rc;
+    if (se != cudaSuccess) return fail(SVM_ECUDA, cudaGetErrorString(se));
+    return SVM_OK;
+}
+
+extern "C" const char* svm_last_error(void) { return g_err.c_str(); }
+extern "C" const char* svm_version(void) { return "svmb200 0.1 sm_100a"; }

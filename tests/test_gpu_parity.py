@@ -1,0 +1,259 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same
+seeded inputs.  Marked `gpu`; run on a B200.
+
+The arithmetic contract makes both sides take every decision in
+fp64 on identical values, so beyond BASELINE.json's tolerances (dual objective 1e-5
+relative, decision values 1e-4 absolute, identical labels, identical SV sets with alpha
+within 1e-6 C) the tests also require the identical pair trajectory and bit-equal alpha.
+"""
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+from gen import workloads as W
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def S():
+    import paper_2311_14908_b200 as S
+    S.lib()
+    return S
+
+
+def _assert_bj_parity(X, y, w, r_gpu, r_or, Xt=None):
+    """BASELINE.json north_star tolerances."""
+    C = w.C
+    a_g, a_o = r_gpu["alpha"], r_or.alpha
+    W_g = O.dual_objective_from_f(a_g, y, r_gpu["f"]) if "f" in r_gpu else None
+    W_o = O.dual_objective_from_f(a_o, y, r_or.f)
+    if W_g is not None:
+        assert abs(W_g - W_o) <= 1e-5 * abs(W_o) + 1e-12
+    assert np.max(np.abs(a_g - a_o)) <= 1e-6 * C
+    sv_g, sv_o = a_g > 1e-8, a_o > 1e-8
+    assert np.array_equal(sv_g, sv_o)
+    if Xt is not None:
+        sv = sv_o
+        d_o = O.decision(X[sv], (a_o * y)[sv], r_or.b, w.kernel, w.gamma, Xt)
+        d_g = O.decision(X[sv_g], (a_g * y)[sv_g], r_gpu["b"], w.kernel, w.gamma, Xt)
+        assert np.max(np.abs(d_g - d_o)) <= 1e-4
+        assert np.array_equal(np.sign(d_g), np.sign(d_o))
+
+
+def _run_pair(S, w, X, y, trace=True, **params):
+    cap = 10 * len(y) + 10000 if trace else 0
+    r_or = O.train(X, y, w.C, w.kernel, w.gamma, w.tol, trace_cap=cap,
+                   max_iter=params.get("max_iter", 0))
+    r_g = S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol, want_f=True, trace_cap=cap, **params)
+    return r_g, r_or
+
+
+def _assert_exact(r_g, r_or):
+    info = r_g["info"]
+    assert info["iterations"] == r_or.iterations
+    assert bool(info["converged"]) == r_or.converged
+    if "trace" in r_g and "trace" in r_or:
+        np.testing.assert_array_equal(r_g["trace"], r_or.trace)
+    np.testing.assert_array_equal(r_g["alpha"], r_or.alpha)
+    np.testing.assert_array_equal(r_g["f"], r_or.f)
+    assert r_g["b"] == r_or.b
+    assert info["b_up"] == r_or.b_up and info["b_low"] == r_or.b_low
+
+
+# ---------------------------------------------------------------- kernel value / exp
+def test_device_exp_matches_oracle_through_predict(S):
+    """One support vector at the origin, coef 1, b 0: dec(x) = exp(-gamma x^2), so the
+    device exp is checked against the oracle on 2^16 arguments (the fp32 x makes x^2
+    exact, the same fp64 argument reaches both exps)."""
+    rng = np.random.default_rng(0)
+    x = np.concatenate([rng.uniform(0, 40, 40000), np.exp(rng.uniform(-30, 3.5, 25536))]).astype(np.float32)
+    Xt = x.reshape(-1, 1)
+    sv = np.zeros((1, 1), np.float32)
+    for gamma in (0.5, 0.0125, 1.0 / 54):
+        d_g = S.svm_predict(sv, np.ones(1), 0.0, S.RBF, gamma, Xt)
+        d_o = O.decision(sv, np.ones(1), 0.0, O.RBF, gamma, Xt)
+        np.testing.assert_array_equal(d_g, d_o)
+
+
+# ---------------------------------------------------------------- closed forms via GPU
+def test_two_point_closed_form(S):
+    X = np.array([[1.0], [3.0]], np.float32); y = np.array([1, -1], np.int8)
+    alpha, b = S.svm_train(X, y, 10.0, S.LINEAR, 0.0, 1e-3)
+    np.testing.assert_allclose(alpha, [0.5, 0.5], atol=1e-15)
+    assert b == pytest.approx(2.0, abs=1e-15)
+    dec = S.svm_predict(X, alpha * y, b, S.LINEAR, 0.0, np.array([[2.0], [1.0]], np.float32))
+    np.testing.assert_allclose(dec, [0.0, 1.0], atol=1e-14)
+
+
+def test_eta_zero_and_clipping(S):
+    X = np.array([[0.0], [0.0], [2.0]], np.float32); y = np.array([1, -1, -1], np.int8)
+    w = W.Workload("eta0", "", 3, 1, O.RBF, 0.5, 1.0, 1e-3, 0, 0, 0, None)
+    r_g, r_or = _run_pair(S, w, X, y)
+    _assert_exact(r_g, r_or)
+    X = np.array([[1.0], [3.0]], np.float32); y = np.array([1, -1], np.int8)
+    w = W.Workload("clip", "", 2, 1, O.LINEAR, 0.0, 0.25, 1e-3, 0, 0, 0, None)
+    r_g, r_or = _run_pair(S, w, X, y)
+    _assert_exact(r_g, r_or)
+    assert r_g["alpha"].tolist() == [0.25, 0.25]
+
+
+# ---------------------------------------------------------------- full trajectories
+SMALL = [("W1", 200), ("W2", 3000), ("W3", 1500), ("W4", 6000), ("W5", 3000)]
+
+
+@pytest.mark.parametrize("name,n", SMALL)
+def test_trajectory_parity(S, name, n):
+    w = W.get(name)
+    X, y = w.train(n)
+    Xt, _ = w.test(500)
+    r_g, r_or = _run_pair(S, w, X, y)
+    _assert_exact(r_g, r_or)
+    _assert_bj_parity(X, y, w, r_g, r_or, Xt)
+
+
+@pytest.mark.parametrize("vr,ctas", [(1, 7), (2, 0), (3, 0), (8, 0), (4, 9)])
+def test_partition_independence(S, vr, ctas):
+    """Same result for any number of (virtual) ranks and CTAs (S:L197 deterministic
+    combine): exercises the multi-rank mailbox protocol on one GPU."""
+    w = W.get("W5")
+    X, y = w.train(2500)
+    r_g, r_or = _run_pair(S, w, X, y, virtual_ranks=vr, ctas=ctas)
+    _assert_exact(r_g, r_or)
+
+
+def test_ragged_and_tiny(S):
+    """n smaller than the CTA count (empty CTAs), odd d, duplicate rows with opposite
+    labels, a ragged last tile."""
+    rng = np.random.default_rng(4)
+    for n, d in ((2, 1), (5, 3), (37, 7), (149, 5), (1031, 13)):
+        X = rng.integers(0, 3, size=(n, d)).astype(np.float32)   # many duplicates / ties
+        y = np.where(rng.random(n) < 0.5, 1, -1).astype(np.int8)
+        y[0], y[-1] = 1, -1
+        for kern, gamma in ((O.LINEAR, 0.0), (O.RBF, 0.3)):
+            w = W.Workload("t", "", n, d, kern, gamma, 2.0, 1e-3, 0, 0, 0, None)
+            r_g, r_or = _run_pair(S, w, X, y)
+            _assert_exact(r_g, r_or)
+
+
+def test_launch_chunking_and_max_iter(S):
+    """Host convergence checks every set of iterations: splitting the solve
+    into launches of 7 iterations gives the same result; max_iter stops early with
+    converged = 0 exactly where the oracle stops."""
+    w = W.get("W2")
+    X, y = w.train(1200)
+    r_g, r_or = _run_pair(S, w, X, y, iters_per_launch=7)
+    _assert_exact(r_g, r_or)
+    assert r_g["info"]["launches"] > 1
+    r_g, r_or = _run_pair(S, w, X, y, max_iter=333)
+    _assert_exact(r_g, r_or)
+    assert r_g["info"]["converged"] == 0 and r_g["info"]["iterations"] == 333
+
+
+def test_warm_start_segment_parity(S):
+    """Resume from the oracle's state after k steps: the GPU then reproduces the rest of
+    the oracle's trajectory."""
+    w = W.get("W3")
+    X, y = w.train(1200)
+    full = O.train(X, y, w.C, w.kernel, w.gamma, w.tol, trace_cap=100000)
+    k = full.iterations // 2
+    part = O.train(X, y, w.C, w.kernel, w.gamma, w.tol, max_iter=k)
+    r_g = S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol, alpha0=part.alpha, f0=part.f,
+                         want_f=True, trace_cap=100000)
+    assert r_g["info"]["iterations"] == full.iterations - k
+    np.testing.assert_array_equal(r_g["trace"], full.trace[k:])
+    np.testing.assert_array_equal(r_g["alpha"], full.alpha)
+
+
+def test_device_api_matches_host_api(S):
+    import torch
+    w = W.get("W4")
+    X, y = w.train(5000)
+    r_h = S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol, want_f=True)
+    Xd = torch.from_numpy(X).cuda(); yd = torch.from_numpy(y).cuda()
+    r_d = S.svm_train_dev(Xd, yd, w.C, w.kernel, w.gamma, w.tol, want_f=True)
+    np.testing.assert_array_equal(r_d["alpha"].cpu().numpy(), r_h["alpha"])
+    assert r_d["b"] == r_h["b"]
+
+
+def test_errors(S):
+    X = np.zeros((4, 2), np.float32)
+    with pytest.raises(S.SvmError, match="ESINGLECLASS"):
+        S.svm_train(X, np.ones(4, np.int8), 1.0, S.LINEAR)
+    with pytest.raises(S.SvmError, match="ELABEL"):
+        S.svm_train(X, np.array([1, -1, 2, 1], np.int8), 1.0, S.LINEAR)
+    Xn = X.copy(); Xn[1, 1] = np.nan
+    with pytest.raises(S.SvmError, match="ENONFINITE"):
+        S.svm_train(Xn, np.array([1, -1, 1, -1], np.int8), 1.0, S.LINEAR)
+
+
+# ---------------------------------------------------------------- predict
+@pytest.mark.parametrize("name,n,m", [("W1", 200, 300), ("W2", 2000, 1000), ("W3", 1000, 300)])
+def test_predict_exact_parity(S, name, n, m):
+    w = W.get(name)
+    X, y = w.train(n)
+    r = O.train(X, y, w.C, w.kernel, w.gamma, w.tol)
+    sv = r.alpha > 1e-8
+    Xt, _ = w.test(m)
+    d_o = O.decision(X[sv], (r.alpha * y)[sv], r.b, w.kernel, w.gamma, Xt)
+    d_g = S.svm_predict(X[sv], (r.alpha * y)[sv], r.b, w.kernel, w.gamma, Xt)
+    np.testing.assert_array_equal(d_g, d_o)
+    # n_sv = 0 -> dec = b
+    d0 = S.svm_predict(np.zeros((0, X.shape[1]), np.float32), np.zeros(0), 0.25, w.kernel, w.gamma, Xt)
+    assert np.all(d0 == 0.25)
+
+
+# ---------------------------------------------------------------- full-size configs
+def test_w2_full_matches_stored_oracle(S):
+    """Adult-like at full size (BASELINE.json configs[1], the bench workload): the whole
+    42,790-step trajectory against the oracle result stored by
+    oracle/tools/make_golden.py."""
+    path = os.path.join(GOLD, "W2_oracle.npz")
+    if not os.path.exists(path):
+        pytest.skip("golden W2_oracle.npz not generated")
+    g = np.load(path)
+    w = W.get("W2")
+    X, y = w.train()
+    r = S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol, want_f=True,
+                       trace_cap=int(g["iterations"]) + 1)
+    assert r["info"]["iterations"] == int(g["iterations"])
+    sha = hashlib.sha256(np.ascontiguousarray(r["trace"], dtype=np.int64).tobytes()).hexdigest()
+    assert sha == str(g["trace_sha"])
+    np.testing.assert_array_equal(r["alpha"], g["alpha"])
+    np.testing.assert_array_equal(r["f"], g["f"])
+    assert r["b"] == float(g["b"])
+
+
+@pytest.mark.parametrize("name,k", [("W3", 60), ("W4", 30), ("W5", 12)])
+def test_full_size_prefix_parity(S, name, k):
+    """Full-size configs in the bench launch configuration: the first k SMO steps equal
+    the oracle's (alpha and f bit for bit over all n rows)."""
+    w = W.get(name)
+    X, y = w.train()
+    r_or = O.train(X, y, w.C, w.kernel, w.gamma, w.tol, max_iter=k, trace_cap=k)
+    r_g = S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol, max_iter=k, want_f=True, trace_cap=k)
+    _assert_exact(r_g, r_or)
+
+
+@pytest.mark.parametrize("name", ["W3", "W4"])
+def test_full_size_converged_properties(S, name):
+    """Properties that hold at any size on the GPU's converged full-size solution:
+    box feasibility, sum alpha y = 0, gap <= 2 tol, and f on 300 sampled rows equals
+    the oracle's from-scratch sum_j alpha_j y_j K_ij - y_i."""
+    w = W.get(name)
+    X, y = w.train()
+    r = S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol, want_f=True)
+    a, f = r["alpha"], r["f"]
+    assert r["info"]["converged"] == 1
+    assert np.all(a >= 0) and np.all(a <= w.C)
+    assert abs(np.dot(a, y.astype(float))) <= 1e-9 * max(1.0, w.C * np.sqrt(len(y)))
+    assert r["info"]["gap"] <= 2 * w.tol
+    sv = a > 0
+    rows = np.random.default_rng(1).choice(len(y), 300, replace=False)
+    f_ref = O.decision(X[sv], (a * y)[sv], 0.0, w.kernel, w.gamma, X[rows]) - y[rows]
+    np.testing.assert_allclose(f[rows], f_ref, atol=1e-6)
