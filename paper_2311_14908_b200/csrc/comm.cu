@@ -73,8 +73,7 @@ extern "C" int svm_comm_init(void** out, int rank, int world, const uint8_t id[1
     CKR(cudaStreamSynchronize(c->st));
     cudaFree(dv);
     // mailbox + peer mapping
-    const int g_total = world * c->ctas_per_rank;
-    c->mbox_bytes = sizeof(Mailbox) + 2 * (size_t)g_total * sizeof(Partial);
+    c->mbox_bytes = svmk::mbox_bytes(c->ctas_per_rank, world);
     CKR(cudaMalloc(&c->mbox_local, c->mbox_bytes));
     CKR(cudaMemset(c->mbox_local, 0, c->mbox_bytes));
     cudaIpcMemHandle_t h;

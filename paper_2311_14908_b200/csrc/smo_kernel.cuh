@@ -6,28 +6,28 @@
 //
 //   * Rows are sharded over ranks (GPUs, or CTA groups of one GPU) and, inside a
 //     rank, over CTAs: CTA c owns a contiguous row block for the whole solve and keeps
-//     its solver state -- f (fp64), alpha (fp64), flags (y, I_up, I_low) -- in shared
-//     memory.  Only X is streamed per iteration.
+//     its solver state -- f (fp64), flags (y, I_up, I_low) and, when it fits, alpha --
+//     in shared memory.  Only X is streamed per iteration.
 //   * X lives in HBM in a CTA-blocked, feature-major layout ("xblk"): per CTA, tiles of
-//     rt rows, each tile [d_pad][rows] fp32.  A producer warp streams it through a ring
-//     of shared-memory stages with cp.async.bulk (TMA bulk copies) + mbarriers; 8
-//     consumer warps compute, one thread per row (RPT rows per thread).
-//   * Per iteration (a2-a7 of SURVEY.md §8):
-//       combine   every CTA reads the 48-byte candidate records of all CTAs of all
-//                 ranks from its rank-local mailbox, reduces them lexicographically
-//                 (f, then lowest global index) -> (i_up, i_low), identical everywhere
-//       test      b_low - b_up <= 2 tol -> converged (device-latched, same decision
-//                 in every CTA)
-//       update    thread 0 of every CTA gathers x_up, x_low from the row-major replica,
-//                 computes eta, the clipped step t and the snapped alphas (fp64,
-//                 SPEC.md L203-211); the owner CTA stores its alphas/flags
-//       row pass  for each owned row j: D_u = sum_k (x_jk - x_uk)^2, D_l likewise
-//                 (ascending k, one fma per term), K = exp_cr(-gamma D) (RBF) or the dot
-//                 product (linear); f_j = fma(c_l, K_l, fma(c_u, K_u, f_j)); status;
-//                 local (f, index) candidates -> warp shuffle -> CTA record
-//       exchange  the record is stored into every rank's mailbox (peer pointers when
-//                 the ranks are GPUs), then a release fence + one atomic add per rank
-//                 on a monotonic arrival counter.
+//     rt rows, each tile [d_pad][rows] fp32.  Warp roles (one CTA per SM):
+//       warps 0-7  consumers: one thread per RPT rows; distances, kernel values,
+//                  f-update, status, local (f, index) candidates
+//       warp 8     scalar warp: candidate record publish, cross-CTA / cross-rank
+//                  exchange, combine, pivot gather, pair update (serial fp64), all
+//                  overlapped with the consumers' streaming of the next tile
+//       warp 9     producer: TMA bulk copies (cp.async.bulk) of X stages into a
+//                  shared-memory ring, mbarrier full/empty pipeline
+//   * Per iteration (rows a2-a7 of SURVEY.md §8):
+//       C  consumers hand their warp candidates to the scalar warp (named barrier 3)
+//       scalar warp: CTA record -> every rank's mailbox (peer pointers when the ranks
+//          are GPUs) + release atomic on a monotonic arrival counter; wait for all
+//          records; lexicographic combine (f, then lowest global index) -> (i_up,
+//          i_low), identical in every CTA; convergence test b_low - b_up <= 2 tol
+//          (device-latched); gather x_up, x_low from the row-major replica
+//       A  consumers start streaming (named barrier 1)
+//       scalar warp: eta, clipped step t, snapped alphas, c_u, c_l;
+//          owner CTA updates its alpha/flags
+//       B  consumers apply f_j = fma(c_l, K_l, fma(c_u, K_u, f_j)) (named barrier 2)
 //   * Exact readings: no contraction (--fmad=false), explicit fma where the oracle has
 //     one, correctly rounded exp, exact comparisons on alpha.  Results do not depend on
 //     the number of ranks / CTAs.
@@ -40,33 +40,41 @@
 
 namespace svmk {
 
-constexpr int MAXR = 8;          // max ranks (GPUs or virtual)
-constexpr int NT = 256;          // consumer threads per CTA
-constexpr int NWC = NT / 32;     // consumer warps
-constexpr int NTHREADS = NT + 32;  // + one producer warp
-constexpr int MAX_STAGES = 8;
+constexpr int MAXR = 8;            // max ranks (GPUs or virtual)
+constexpr int NT = 256;            // consumer threads per CTA
+constexpr int NWC = NT / 32;       // consumer warps
+constexpr int SCALAR_WARP = NWC;   // warp 8
+constexpr int PRODUCER_WARP = NWC + 1;
+constexpr int NTHREADS = NT + 64;  // + scalar warp + producer warp
+constexpr int NSYNC = NT + 32;     // participants of the named barriers
+constexpr int MAX_STAGES = 16;
+enum { BAR_A = 1, BAR_B = 2, BAR_C = 3, BAR_D = 4, BAR_E = 5, BAR_F = 6 };
 
 enum { ST_RUNNING = 0, ST_CONVERGED = 1, ST_MAXITER = 2, ST_LIMIT = 3, ST_TIMEOUT = -8 };
 enum { FL_POS = 1, FL_UP = 2, FL_LOW = 4 };
 
-struct __align__(16) Partial {   // one CTA's candidate record (48 B)
+// One CTA's candidate record (48 B).
+struct __align__(16) Partial {
     double f_up, f_low, a_up, a_low;
-    int32_t i_up, i_low;         // global row index, -1 if the set is empty
+    int32_t i_up, i_low;           // global row index, -1 if the set is empty
     int32_t y_up, y_low;
 };
 
 struct __align__(128) Mailbox {
-    unsigned long long count;    // monotonic number of records received
+    unsigned long long count;      // monotonic number of records received
     unsigned long long pad[15];
 };
-// partials follow the header: Partial parts[2][g_total]
+// records follow the header: Partial parts[2][g_total] (double-buffered by parity)
 __host__ __device__ inline Partial* mbox_parts(Mailbox* m, int parity, int g_total) {
     return reinterpret_cast<Partial*>(m + 1) + (size_t)parity * g_total;
 }
+__host__ __device__ inline size_t mbox_bytes(int cpr, int world) {
+    return sizeof(Mailbox) + 2 * (size_t)cpr * world * sizeof(Partial);
+}
 
-struct Ctl {                     // per rank solver control, persists across launches
-    long long it;                // SMO updates done
-    long long seq;               // exchanges done
+struct Ctl {                       // per rank solver control, persists across launches
+    long long it;                  // SMO updates done
+    long long seq;                 // exchanges done
     int state;
     int pad;
     double b_up, b_low;
@@ -80,8 +88,8 @@ struct Params {
     int d, d_pad, kc, n_chunks, stages, rt;
     int world, rank_base, ctas_per_rank;
     long long n_global;
-    const float* xr;             // row-major replica [n_global][d]
-    long long cta_stride;        // floats per CTA block in xblk
+    const float* xr;               // row-major replica [n_global][d]
+    long long cta_stride;          // floats per CTA block in xblk
     long long row_off[MAXR];
     int n_rows[MAXR];
     const float* xblk[MAXR];
@@ -94,9 +102,17 @@ struct Params {
     long long trace_cap;
     unsigned long long* progress;  // host-mapped, may be null
     int check_interval;
-    int state_cap;               // rows per CTA the shared-memory state can hold
+    int state_cap;                 // rows per CTA the shared-memory state can hold
+    int resident;                  // 1: the CTA's whole X block stays in shared memory (one tile)
     long long timeout_ns;
+    int sys_scope;                 // 1 when mailboxes live on other GPUs (system scope)
+    unsigned long long* timers;    // optional [8] per-phase cycle totals of CTA 0
 };
+
+// phase timers: scalar warp lane 0 of CTA 0 ...
+enum { PH_WAITC = 0, PH_PUBLISH, PH_EXCH, PH_COMBINE, PH_SCALAR, PH_WAITA,
+       // ... and consumer thread 0 of CTA 0
+       PH_ROWS, PH_WAITB, PH_N };
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -120,7 +136,7 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
                  : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
     return ok != 0;
 }
-__device__ __forceinline__ long long globaltimer_ns() {
+__device__ __forceinline__ long long globaltimer() {
     long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
@@ -132,7 +148,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     long long t0 = 0;
     while (!mbar_try_wait(bar, parity)) {
         if ((++spins & 4095u) == 0) {
-            const long long now = globaltimer_ns();
+            const long long now = globaltimer();
             if (t0 == 0) t0 = now;
             else if (now - t0 > 30ll * 1000 * 1000 * 1000) asm volatile("trap;");
         }
@@ -147,13 +163,33 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ long long globaltimer() {
-    long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
+__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
 }
-__device__ __forceinline__ void bar_consumers() {
-    asm volatile("bar.sync 1, %0;" :: "n"(NT) : "memory");
+__device__ __forceinline__ void st_volatile_v2(unsigned long long* p, unsigned long long a,
+                                               unsigned long long b) {
+    asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" :: "l"(p), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ void ld_volatile_v2(const unsigned long long* p, unsigned long long& a,
+                                               unsigned long long& b) {
+    asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+__device__ __forceinline__ unsigned long long ll_word(uint32_t flag, uint32_t payload) {
+    return ((unsigned long long)flag << 32) | payload;
+}
+__device__ __forceinline__ void red_release_gpu(unsigned long long* p) {
+    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" :: "l"(p) : "memory");
+}
+__device__ __forceinline__ void red_release_sys(unsigned long long* p) {
+    asm volatile("red.release.sys.global.add.u64 [%0], 1;" :: "l"(p) : "memory");
+}
+__device__ __forceinline__ void named_sync(int id) {
+    asm volatile("bar.sync %0, %1;" :: "r"(id), "n"(NSYNC) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id) {
+    asm volatile("bar.arrive %0, %1;" :: "r"(id), "n"(NSYNC) : "memory");
 }
 
 // Lexicographic "better" for the two selections: smaller f wins for I_up,
@@ -174,66 +210,76 @@ __device__ __forceinline__ uint8_t flags_of(int y, double a, double C) {
 
 // ------------------------------------------------------------------ shared layout
 struct Shared {
-    // pipeline control
     volatile int stop;
     volatile int producer_done;
     volatile unsigned int issued;
-    int timeout;
-    // iteration scalars (written by consumer thread 0 after the combine)
-    int decision;                // ST_*
-    int u, l;                    // global winners
-    double f_up, f_low, a_up, a_low;
-    int y_up, y_low;
-    double cu, cl, au_new, al_new;
-    // reduction scratch
-    double red_f[2][NWC];
+    int decision;                  // ST_*, written by the scalar warp before barrier A
+    int u, l;                      // global winners of this iteration
+    double f_up, f_low;
+    double cu, cl;                 // written by the scalar warp before barrier B
+    double red_f[2][NWC];          // per consumer warp candidates (local row index)
     int red_i[2][NWC];
-    double red_a[2][NWC];
-    int red_y[2][NWC];
+    double wf[2], wa[2];           // the global winner of this iteration
+    int wi[2], wy[2];
+    double cf[2][NWC + 1];         // per warp combine results (global row index)
+    int ci[2][NWC + 1];
+    double ca[2][NWC + 1];
+    int cy[2][NWC + 1];
+    int timeout;
     unsigned long long bars[2 * MAX_STAGES];
+    double exp_tab[svmexp::EXP_TABLE_DOUBLES];
 };
 
-__device__ __forceinline__ void warp_reduce_rec(double& f, int& i, double& a, int& y, bool up) {
+template <bool UP>
+__device__ __forceinline__ void warp_reduce_fi(double& f, int& i, int width = 32) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-        double f2 = __shfl_xor_sync(0xffffffffu, f, o);
-        int i2 = __shfl_xor_sync(0xffffffffu, i, o);
-        double a2 = __shfl_xor_sync(0xffffffffu, a, o);
-        int y2 = __shfl_xor_sync(0xffffffffu, y, o);
-        bool take = up ? better_up(f2, i2, f, i) : better_low(f2, i2, f, i);
-        if (take) { f = f2; i = i2; a = a2; y = y2; }
+        if (o >= width) continue;
+        const double f2 = __shfl_xor_sync(0xffffffffu, f, o);
+        const int i2 = __shfl_xor_sync(0xffffffffu, i, o);
+        const bool take = UP ? better_up(f2, i2, f, i) : better_low(f2, i2, f, i);
+        if (take) { f = f2; i = i2; }
     }
 }
 
-// Reduce per-thread (f, i, a, y) records of both selections over the NT consumer
-// threads; every consumer thread returns with the CTA-wide result in sh.
-__device__ __forceinline__ void cta_reduce(Shared& sh, double fu, int iu, double au, int yu,
-                                           double fl, int il, double al, int yl) {
-    const int t = threadIdx.x, w = t >> 5, lane = t & 31;
-    warp_reduce_rec(fu, iu, au, yu, true);
-    warp_reduce_rec(fl, il, al, yl, false);
-    if (lane == 0) {
-        sh.red_f[0][w] = fu; sh.red_i[0][w] = iu; sh.red_a[0][w] = au; sh.red_y[0][w] = yu;
-        sh.red_f[1][w] = fl; sh.red_i[1][w] = il; sh.red_a[1][w] = al; sh.red_y[1][w] = yl;
-    }
-    bar_consumers();
-    if (t == 0) {
-        for (int k = 1; k < NWC; ++k) {
-            if (better_up(sh.red_f[0][k], sh.red_i[0][k], sh.red_f[0][0], sh.red_i[0][0])) {
-                sh.red_f[0][0] = sh.red_f[0][k]; sh.red_i[0][0] = sh.red_i[0][k];
-                sh.red_a[0][0] = sh.red_a[0][k]; sh.red_y[0][0] = sh.red_y[0][k];
-            }
-            if (better_low(sh.red_f[1][k], sh.red_i[1][k], sh.red_f[1][0], sh.red_i[1][0])) {
-                sh.red_f[1][0] = sh.red_f[1][k]; sh.red_i[1][0] = sh.red_i[1][k];
-                sh.red_a[1][0] = sh.red_a[1][k]; sh.red_y[1][0] = sh.red_y[1][k];
-            }
-        }
-    }
-    bar_consumers();
+// (the volatile shared load forces a deferred-blocking bar.sync to resolve before
+// the clock is read)
+// A (candidate up, candidate low) pair with the alpha and label of each.
+struct Cand {
+    double fu, fl, au, al;
+    int iu, il, yu, yl;
+};
+__device__ __forceinline__ void cand_init(Cand& c) {
+    c.fu = __longlong_as_double(0x7ff0000000000000ll); c.fl = -c.fu;
+    c.au = 0.0; c.al = 0.0; c.iu = INT_MAX; c.il = INT_MAX; c.yu = 0; c.yl = 0;
 }
+__device__ __forceinline__ void cand_merge(Cand& a, const Cand& b) {
+    if (b.iu != INT_MAX && better_up(b.fu, b.iu, a.fu, a.iu)) { a.fu = b.fu; a.iu = b.iu; a.au = b.au; a.yu = b.yu; }
+    if (b.il != INT_MAX && better_low(b.fl, b.il, a.fl, a.il)) { a.fl = b.fl; a.il = b.il; a.al = b.al; a.yl = b.yl; }
+}
+__device__ __forceinline__ void cand_warp_merge(Cand& c) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        Cand b;
+        b.fu = __shfl_xor_sync(0xffffffffu, c.fu, o); b.iu = __shfl_xor_sync(0xffffffffu, c.iu, o);
+        b.au = __shfl_xor_sync(0xffffffffu, c.au, o); b.yu = __shfl_xor_sync(0xffffffffu, c.yu, o);
+        b.fl = __shfl_xor_sync(0xffffffffu, c.fl, o); b.il = __shfl_xor_sync(0xffffffffu, c.il, o);
+        b.al = __shfl_xor_sync(0xffffffffu, c.al, o); b.yl = __shfl_xor_sync(0xffffffffu, c.yl, o);
+        cand_merge(c, b);
+    }
+}
+#define SVM_PHASE(on, ph)                                                    \
+    do {                                                                     \
+        if (on) {                                                            \
+            (void)*(volatile int*)&sh.decision;                              \
+            const long long c_ = clock64();                                  \
+            ph_acc[ph] += (unsigned long long)(c_ - ph_t);                   \
+            ph_t = c_;                                                       \
+        }                                                                    \
+    } while (0)
 
 // ------------------------------------------------------------------ the kernel
-template <int KERNEL, int RPT>
+template <int KERNEL, int RPT, bool A_SMEM>
 __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Shared& sh = *reinterpret_cast<Shared*>(smem_raw);
@@ -241,7 +287,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
     double* piv_u = reinterpret_cast<double*>(smem_raw + off); off += (size_t)P.d_pad * 8;
     double* piv_l = reinterpret_cast<double*>(smem_raw + off); off += (size_t)P.d_pad * 8;
     double* f_s = reinterpret_cast<double*>(smem_raw + off); off += (size_t)P.state_cap * 8;
-    double* a_s = reinterpret_cast<double*>(smem_raw + off); off += (size_t)P.state_cap * 8;
+    double* a_s = reinterpret_cast<double*>(smem_raw + off); if (A_SMEM) off += (size_t)P.state_cap * 8;
     uint8_t* fl_s = smem_raw + off; off += (size_t)P.state_cap;
     off = (off + 127) & ~size_t(127);
     float* ring = reinterpret_cast<float*>(smem_raw + off);
@@ -250,10 +296,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
     uint64_t* empty = full + MAX_STAGES;
 
     const int t = threadIdx.x;
+    const int warp = t >> 5, lane = t & 31;
     const int rank = P.rank_base + blockIdx.x / P.ctas_per_rank;
     const int cta = blockIdx.x % P.ctas_per_rank;
-    const int g_total = P.world * P.ctas_per_rank;
-    const int gcta = rank * P.ctas_per_rank + cta;
     const int n_r = P.n_rows[rank];
     const int r0 = (int)(((long long)n_r * cta) / P.ctas_per_rank);
     const int r1 = (int)(((long long)n_r * (cta + 1)) / P.ctas_per_rank);
@@ -261,32 +306,42 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
     const long long gbase = P.row_off[rank] + r0;            // global index of local row 0
     const int n_tiles = (R + P.rt - 1) / P.rt;
     const float* xcta = P.xblk[rank] + (long long)cta * P.cta_stride;
-    Mailbox* my_mb = P.mbox[rank];
-    Ctl* ctl = P.ctl[rank];
+    double* alpha_g = P.alpha[rank] + r0;                    // this CTA's alpha (global)
+    const double C = P.C;
 
     if (t == 0) {
         sh.stop = 0; sh.producer_done = 0; sh.issued = 0; sh.timeout = 0;
         for (int s = 0; s < P.stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NWC); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    // load the CTA's state into shared memory
+    for (int e = t; e < svmexp::EXP_TABLE_DOUBLES; e += NTHREADS) sh.exp_tab[e] = svmexp::table_entry(e);
     for (int j = t; j < R; j += NTHREADS) {
         f_s[j] = P.f[rank][r0 + j];
-        a_s[j] = P.alpha[rank][r0 + j];
+        if (A_SMEM) a_s[j] = alpha_g[j];
         fl_s[j] = P.flags[rank][r0 + j];
     }
     __syncthreads();
+    const svmexp::PtrTab tab{sh.exp_tab};
 
-    // ================================================================ producer warp
-    if (t >= NT) {
-        if (t == NT && n_tiles > 0) {
-            unsigned int s = 0;
+    // ============================================================ producer warp
+    if (warp == PRODUCER_WARP) {
+        if (P.resident) {
+            if (lane == 0 && n_tiles > 0) {
+                const int rp = (R + 3) & ~3;
+                const uint32_t bytes = (uint32_t)P.d_pad * rp * 4u;
+                mbar_arrive_tx(&full[0], bytes);
+                bulk_g2s(ring, xcta, bytes, &full[0]);
+            }
+            if (lane == 0) { sh.issued = 0; __threadfence_block(); sh.producer_done = 1; }
+            return;
+        }
+        if (lane == 0 && n_tiles > 0) {
+            unsigned int s = 0, slot = 0, par = 0;
+            bool wrapped = false;
             int tile = 0, chunk = 0;
             for (;;) {
-                const int slot = s % P.stages;
-                const unsigned int round = s / P.stages;
-                if (s >= (unsigned)P.stages) {
-                    while (!mbar_try_wait(&empty[slot], (round - 1) & 1)) {
+                if (wrapped) {
+                    while (!mbar_try_wait(&empty[slot], par ^ 1u)) {
                         if (sh.stop) break;
                     }
                 }
@@ -299,46 +354,31 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                 bulk_g2s(ring + (size_t)slot * stage_floats, src, bytes, &full[slot]);
                 ++s;
                 sh.issued = s;
+                if (++slot == (unsigned)P.stages) { slot = 0; par ^= 1u; wrapped = true; }
                 if (++chunk == P.n_chunks) { chunk = 0; if (++tile == n_tiles) tile = 0; }
             }
         }
-        if (t == NT) { __threadfence_block(); sh.producer_done = 1; }
+        if (lane == 0) { __threadfence_block(); sh.producer_done = 1; }
         return;
     }
 
-    // ================================================================ consumers
-    long long it = ctl->it;            // read by every CTA; written only at kernel end
+    unsigned long long ph_acc[PH_N] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long ph_t = clock64();
+    const bool is_scalar = (warp == SCALAR_WARP);
+    const bool timing = P.timers != nullptr && blockIdx.x == 0 && (t == 0 || (is_scalar && lane == 0));
+    int final_state = ST_RUNNING;
+    Ctl* ctl = P.ctl[rank];
+    Mailbox* my_mb = P.mbox[rank];
+    long long it = ctl->it;                 // written only at kernel end by CTA 0
     long long seq = ctl->seq;
     const long long it_start = it;
-    unsigned int consumed = 0;
-    const double C = P.C;
+    unsigned int cslot = 0, cpar = 0, consumed = 0;
+    const double INF = __longlong_as_double(0x7ff0000000000000ll);
 
-    // ---- publish this CTA's candidate record for exchange `seq + 1`
-    auto publish = [&](double fu, int ju, double fl, int jl) {
-        // (ju, jl are local row indices or INT_MAX)
-        cta_reduce(sh, fu, ju, 0.0, 0, fl, jl, 0.0, 0);
-        if (t == 0) {
-            Partial p;
-            const int lu = sh.red_i[0][0], ll = sh.red_i[1][0];
-            p.f_up = sh.red_f[0][0];
-            p.f_low = sh.red_f[1][0];
-            p.i_up = (lu == INT_MAX) ? -1 : (int)(gbase + lu);
-            p.i_low = (ll == INT_MAX) ? -1 : (int)(gbase + ll);
-            p.a_up = (lu == INT_MAX) ? 0.0 : a_s[lu];
-            p.a_low = (ll == INT_MAX) ? 0.0 : a_s[ll];
-            p.y_up = (lu == INT_MAX) ? 0 : ((fl_s[lu] & FL_POS) ? 1 : -1);
-            p.y_low = (ll == INT_MAX) ? 0 : ((fl_s[ll] & FL_POS) ? 1 : -1);
-            const int parity = (int)((seq + 1) & 1);
-            for (int r = 0; r < P.world; ++r) mbox_parts(P.mbox[r], parity, g_total)[gcta] = p;
-            __threadfence_system();
-            for (int r = 0; r < P.world; ++r) atomicAdd_system(&P.mbox[r]->count, 1ull);
-        }
-        ++seq;
-    };
-
+    if (P.resident && n_tiles > 0 && !is_scalar) mbar_wait(&full[0], 0);
     // ---- initial selection from the current state (no update)
-    {
-        double fu = __longlong_as_double(0x7ff0000000000000ll), fl = -fu;
+    if (!is_scalar) {
+        double fu = INF, fl = -INF;
         int ju = INT_MAX, jl = INT_MAX;
         for (int j = t; j < R; j += NT) {
             const uint8_t g = fl_s[j];
@@ -346,116 +386,200 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
             if ((g & FL_UP) && better_up(fj, j, fu, ju)) { fu = fj; ju = j; }
             if ((g & FL_LOW) && better_low(fj, j, fl, jl)) { fl = fj; jl = j; }
         }
-        publish(fu, ju, fl, jl);
+        warp_reduce_fi<true>(fu, ju);
+        warp_reduce_fi<false>(fl, jl);
+        if (lane == 0) {
+            sh.red_f[0][warp] = fu; sh.red_i[0][warp] = ju;
+            sh.red_f[1][warp] = fl; sh.red_i[1][warp] = jl;
+        }
     }
 
-    int final_state = ST_RUNNING;
     for (;;) {
-        // ================= wait for exchange `seq`, then combine
-        if (t == 0) {
-            const unsigned long long target = (unsigned long long)seq * g_total;
-            long long t0 = 0;
-            unsigned int spins = 0;
-            while (ld_acquire_sys(&my_mb->count) < target) {
-                if ((++spins & 1023u) == 0) {
-                    const long long now = globaltimer();
-                    if (t0 == 0) t0 = now;
-                    else if (now - t0 > P.timeout_ns) { sh.timeout = 1; break; }
+        named_sync(BAR_C);                  // consumer candidates are in sh.red_*
+        SVM_PHASE(timing, is_scalar ? PH_WAITC : PH_ROWS);
+        // ---- exchange seq + 1 (a6): the scalar warp stores the CTA record into every
+        // rank's mailbox (peer pointers when the ranks are GPUs) and bumps each rank's
+        // arrival counter with a release reduction; it then waits for all g_total
+        // records of this exchange and reduces them lexicographically (identical in
+        // every CTA of every rank).  Measured on B200 (tools/exchange_bench.cu) this is
+        // the fastest of the grid-wide exchanges tried (~2 us at 148 CTAs).
+        ++seq;
+        if (is_scalar) {
+            const int g_total = P.world * P.ctas_per_rank;
+            const int par = (int)(seq & 1);
+            double fu = lane < NWC ? sh.red_f[0][lane] : INF;
+            int ju = lane < NWC ? sh.red_i[0][lane] : INT_MAX;
+            double fl = lane < NWC ? sh.red_f[1][lane] : -INF;
+            int jl = lane < NWC ? sh.red_i[1][lane] : INT_MAX;
+            warp_reduce_fi<true>(fu, ju, NWC);
+            warp_reduce_fi<false>(fl, jl, NWC);
+            if (lane == 0) {
+                Partial p;
+                p.f_up = fu; p.f_low = fl;
+                p.i_up = (ju == INT_MAX) ? -1 : (int)(gbase + ju);
+                p.i_low = (jl == INT_MAX) ? -1 : (int)(gbase + jl);
+                p.a_up = (ju == INT_MAX) ? 0.0 : (A_SMEM ? a_s[ju] : alpha_g[ju]);
+                p.a_low = (jl == INT_MAX) ? 0.0 : (A_SMEM ? a_s[jl] : alpha_g[jl]);
+                p.y_up = (ju == INT_MAX) ? 0 : ((fl_s[ju] & FL_POS) ? 1 : -1);
+                p.y_low = (jl == INT_MAX) ? 0 : ((fl_s[jl] & FL_POS) ? 1 : -1);
+                const int gcta = rank * P.ctas_per_rank + cta;
+                for (int r = 0; r < P.world; ++r) mbox_parts(P.mbox[r], par, g_total)[gcta] = p;
+                if (P.sys_scope) {
+                    for (int r = 0; r < P.world; ++r) red_release_sys(&P.mbox[r]->count);
+                } else {
+                    for (int r = 0; r < P.world; ++r) red_release_gpu(&P.mbox[r]->count);
                 }
             }
-            __threadfence();
+            SVM_PHASE(timing, PH_PUBLISH);
+            int timeout = 0;
+            if (lane == 0) {
+                const unsigned long long target = (unsigned long long)seq * g_total;
+                long long t0 = 0;
+                unsigned int spins = 0;
+                while ((P.sys_scope ? ld_acquire_sys(&my_mb->count) : ld_acquire_gpu(&my_mb->count)) < target) {
+                    if ((++spins & 1023u) == 0) {
+                        const long long now = globaltimer();
+                        if (t0 == 0) t0 = now;
+                        else if (now - t0 > P.timeout_ns) { timeout = 1; break; }
+                    }
+                }
+            }
+            timeout = __shfl_sync(0xffffffffu, timeout, 0);
+            SVM_PHASE(timing, PH_EXCH);
+            Cand c;
+            cand_init(c);
+            if (!timeout) {
+                const Partial* parts = mbox_parts(my_mb, par, g_total);
+                for (int g0 = 0; g0 < g_total; g0 += 32 * 5) {
+                    double2 pf[5], pa[5];
+                    int4 pi[5];
+#pragma unroll
+                    for (int q = 0; q < 5; ++q) {       // issue every load, then reduce
+                        const int g = g0 + q * 32 + lane;
+                        if (g < g_total) {
+                            pf[q] = __ldcg(reinterpret_cast<const double2*>(&parts[g]));
+                            pa[q] = __ldcg(reinterpret_cast<const double2*>(&parts[g]) + 1);
+                            pi[q] = __ldcg(reinterpret_cast<const int4*>(&parts[g]) + 2);
+                        } else {
+                            pi[q] = make_int4(-1, -1, 0, 0);
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < 5; ++q) {
+                        Cand r;
+                        r.fu = pf[q].x; r.fl = pf[q].y; r.au = pa[q].x; r.al = pa[q].y;
+                        r.iu = pi[q].x < 0 ? INT_MAX : pi[q].x; r.il = pi[q].y < 0 ? INT_MAX : pi[q].y;
+                        r.yu = pi[q].z; r.yl = pi[q].w;
+                        cand_merge(c, r);
+                    }
+                }
+            }
+            cand_warp_merge(c);
+            if (lane == 0) {
+                sh.timeout = timeout;
+                sh.wf[0] = c.fu; sh.wi[0] = c.iu; sh.wa[0] = c.au; sh.wy[0] = c.yu;
+                sh.wf[1] = c.fl; sh.wi[1] = c.il; sh.wa[1] = c.al; sh.wy[1] = c.yl;
+            }
+            __syncwarp();
+            __threadfence_block();
         }
-        bar_consumers();
+        named_sync(BAR_F);
+        SVM_PHASE(timing, is_scalar ? PH_COMBINE : PH_WAITA);
+        const double fu = sh.wf[0], fl = sh.wf[1], au = sh.wa[0], al = sh.wa[1];
+        const int iu = sh.wi[0], il = sh.wi[1], yu = sh.wy[0], yl = sh.wy[1];
+        int dec = ST_RUNNING;
+        if (sh.timeout) dec = ST_TIMEOUT;
+        else if (iu == INT_MAX || il == INT_MAX) dec = ST_CONVERGED;
+        else if (fl - fu <= 2.0 * P.tol) dec = ST_CONVERGED;
+        else if (it == P.max_iter) dec = ST_MAXITER;
+        else if (P.iter_limit > 0 && it - it_start == P.iter_limit) dec = ST_LIMIT;
+        if (dec != ST_RUNNING) {
+            final_state = dec;
+            if (t == 0) { sh.u = iu; sh.l = il; sh.f_up = fu; sh.f_low = fl; }
+            break;
+        }
+        // ---- pivot rows x_up, x_low (fp64 in shared memory), all threads
         {
-            const Partial* parts = mbox_parts(my_mb, (int)(seq & 1), g_total);
-            double fu = __longlong_as_double(0x7ff0000000000000ll), fl = -fu, au = 0.0, al = 0.0;
-            int iu = INT_MAX, il = INT_MAX, yu = 0, yl = 0;
-            if (!sh.timeout) {
-                for (int g = t; g < g_total; g += NT) {
-                    const double pfu = __ldcg(&parts[g].f_up), pfl = __ldcg(&parts[g].f_low);
-                    const int piu = __ldcg(&parts[g].i_up), pil = __ldcg(&parts[g].i_low);
-                    if (piu >= 0 && better_up(pfu, piu, fu, iu)) {
-                        fu = pfu; iu = piu; au = __ldcg(&parts[g].a_up); yu = __ldcg(&parts[g].y_up);
-                    }
-                    if (pil >= 0 && better_low(pfl, pil, fl, il)) {
-                        fl = pfl; il = pil; al = __ldcg(&parts[g].a_low); yl = __ldcg(&parts[g].y_low);
-                    }
+            const float* xu_g = P.xr + (long long)iu * P.d;
+            const float* xl_g = P.xr + (long long)il * P.d;
+            for (int k0 = 0; k0 < P.d_pad; k0 += NSYNC * 4) {
+                float vu[4], vl[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int k = k0 + q * NSYNC + t;
+                    vu[q] = (k < P.d) ? __ldg(&xu_g[k]) : 0.0f;
+                    vl[q] = (k < P.d) ? __ldg(&xl_g[k]) : 0.0f;
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int k = k0 + q * NSYNC + t;
+                    if (k < P.d_pad) { piv_u[k] = (double)vu[q]; piv_l[k] = (double)vl[q]; }
                 }
             }
-            cta_reduce(sh, fu, iu, au, yu, fl, il, al, yl);
         }
-        if (t == 0) {
-            int dec = ST_RUNNING;
-            const int u = sh.red_i[0][0], l = sh.red_i[1][0];
-            if (sh.timeout) dec = ST_TIMEOUT;
-            else if (u == INT_MAX || l == INT_MAX) dec = ST_CONVERGED;
-            else if (sh.red_f[1][0] - sh.red_f[0][0] <= 2.0 * P.tol) dec = ST_CONVERGED;
-            else if (it == P.max_iter) dec = ST_MAXITER;
-            else if (P.iter_limit > 0 && it - it_start == P.iter_limit) dec = ST_LIMIT;
-            sh.decision = dec;
-            sh.u = u; sh.l = l;
-            sh.f_up = sh.red_f[0][0]; sh.f_low = sh.red_f[1][0];
-            sh.a_up = sh.red_a[0][0]; sh.a_low = sh.red_a[1][0];
-            sh.y_up = sh.red_y[0][0]; sh.y_low = sh.red_y[1][0];
-        }
-        bar_consumers();
-        if (sh.decision != ST_RUNNING) { final_state = sh.decision; break; }
-
-        // ================= pair update (a2): gather x_up, x_low; eta; clipped step
-        const int u = sh.u, l = sh.l;
-        for (int k = t; k < P.d_pad; k += NT) {
-            piv_u[k] = (k < P.d) ? (double)P.xr[(long long)u * P.d + k] : 0.0;
-            piv_l[k] = (k < P.d) ? (double)P.xr[(long long)l * P.d + k] : 0.0;
-        }
-        bar_consumers();
-        if (t == 0) {
-            double Kuu, Kll, Kul;
-            if (KERNEL == 1) {
-                double acc = 0.0;
-                for (int k = 0; k < P.d; ++k) { const double dv = piv_u[k] - piv_l[k]; acc = fma(dv, dv, acc); }
-                Kuu = 1.0; Kll = 1.0;
-                Kul = (u == l) ? 1.0 : svmexp::exp_cr(-(P.gamma * acc));
-            } else {
-                double s_uu = 0.0, s_ll = 0.0, s_ul = 0.0;
-                for (int k = 0; k < P.d; ++k) {
-                    s_uu = fma(piv_u[k], piv_u[k], s_uu);
-                    s_ll = fma(piv_l[k], piv_l[k], s_ll);
-                    s_ul = fma(piv_u[k], piv_l[k], s_ul);
+        named_sync(BAR_A);
+        SVM_PHASE(timing, is_scalar ? PH_COMBINE : PH_WAITA);
+        const int u = iu, l = il;
+        if (is_scalar) {
+            // ---- pair update (a2): eta, clipped step, snapped alphas (lane 0)
+            if (lane == 0) {
+                double Kuu, Kll, Kul;
+                if (KERNEL == 1) {
+                    double acc = 0.0;
+#pragma unroll 8
+                    for (int k = 0; k < P.d; ++k) { const double dv = piv_u[k] - piv_l[k]; acc = fma(dv, dv, acc); }
+                    Kuu = 1.0; Kll = 1.0;
+                    Kul = (u == l) ? 1.0 : svmexp::exp_cr_t(-(P.gamma * acc), tab);
+                } else {
+                    double s_uu = 0.0, s_ll = 0.0, s_ul = 0.0;
+#pragma unroll 8
+                    for (int k = 0; k < P.d; ++k) {
+                        s_uu = fma(piv_u[k], piv_u[k], s_uu);
+                        s_ll = fma(piv_l[k], piv_l[k], s_ll);
+                        s_ul = fma(piv_u[k], piv_l[k], s_ul);
+                    }
+                    Kuu = s_uu; Kll = s_ll; Kul = s_ul;
                 }
-                Kuu = s_uu; Kll = s_ll; Kul = s_ul;
+                const double eta = Kuu + Kll - 2.0 * Kul;
+                const double gap = fl - fu;
+                const double yu_d = (double)yu, yl_d = (double)yl;
+                const double tu = (yu == 1) ? C - au : au;
+                const double tl = (yl == 1) ? al : C - al;
+                double tt = gap / (eta > 1e-12 ? eta : 1e-12);
+                if (tu < tt) tt = tu;
+                if (tl < tt) tt = tl;
+                const double au2 = (tt == tu) ? (yu == 1 ? C : 0.0) : au + yu_d * tt;
+                const double al2 = (tt == tl) ? (yl == 1 ? 0.0 : C) : al - yl_d * tt;
+                sh.cu = yu_d * (au2 - au);
+                sh.cl = yl_d * (al2 - al);
+                // owner CTA: alpha and flags of the two rows
+                const long long lu = (long long)u - gbase, ll = (long long)l - gbase;
+                if (lu >= 0 && lu < R) {
+                    if (A_SMEM) a_s[lu] = au2; else alpha_g[lu] = au2;
+                    fl_s[lu] = flags_of(yu, au2, C);
+                }
+                if (ll >= 0 && ll < R) {
+                    if (A_SMEM) a_s[ll] = al2; else alpha_g[ll] = al2;
+                    fl_s[ll] = flags_of(yl, al2, C);
+                }
+                if (P.trace && rank == 0 && cta == 0 && it < P.trace_cap) {
+                    P.trace[2 * it] = u; P.trace[2 * it + 1] = l;
+                }
+                if (P.progress && rank == 0 && cta == 0 && (it % P.check_interval) == 0)
+                    *(volatile unsigned long long*)P.progress = (unsigned long long)it;
+                __threadfence_block();
             }
-            const double eta = Kuu + Kll - 2.0 * Kul;
-            const double gap = sh.f_low - sh.f_up;
-            const double yu = (double)sh.y_up, yl = (double)sh.y_low;
-            const double au = sh.a_up, al = sh.a_low;
-            const double tu = (sh.y_up == 1) ? C - au : au;
-            const double tl = (sh.y_low == 1) ? al : C - al;
-            double tt = gap / (eta > 1e-12 ? eta : 1e-12);
-            if (tu < tt) tt = tu;
-            if (tl < tt) tt = tl;
-            const double au2 = (tt == tu) ? (sh.y_up == 1 ? C : 0.0) : au + yu * tt;
-            const double al2 = (tt == tl) ? (sh.y_low == 1 ? 0.0 : C) : al - yl * tt;
-            sh.cu = yu * (au2 - au);
-            sh.cl = yl * (al2 - al);
-            sh.au_new = au2; sh.al_new = al2;
-            // owner CTA updates its shared-memory state for the two rows
-            const long long lu = (long long)u - gbase, ll = (long long)l - gbase;
-            if (lu >= 0 && lu < R) { a_s[lu] = au2; fl_s[lu] = flags_of(sh.y_up, au2, C); }
-            if (ll >= 0 && ll < R) { a_s[ll] = al2; fl_s[ll] = flags_of(sh.y_low, al2, C); }
-            if (P.trace && rank == 0 && cta == 0 && it < P.trace_cap) {
-                P.trace[2 * it] = u; P.trace[2 * it + 1] = l;
-            }
-            if (P.progress && rank == 0 && cta == 0 && P.check_interval > 0 &&
-                (it % P.check_interval) == 0) {
-                *(volatile unsigned long long*)P.progress = (unsigned long long)it;
-            }
+            __syncwarp();
+            SVM_PHASE(timing, PH_SCALAR);
+            named_arrive(BAR_B);
+            ++it;
+            continue;
         }
-        bar_consumers();
-        const double cu = sh.cu, cl = sh.cl;
-
-        // ================= row pass (a3-a5)
-        double bfu = __longlong_as_double(0x7ff0000000000000ll), bfl = -bfu;
+        // ================= consumers: row pass (a3-a5)
+        double cu = 0.0, cl = 0.0;
+        double bfu = INF, bfl = -INF;
         int bju = INT_MAX, bjl = INT_MAX;
+        if (n_tiles == 0) named_sync(BAR_B);
         for (int tile = 0; tile < n_tiles; ++tile) {
             const int rows_t = min(P.rt, R - tile * P.rt);
             const int rp = (rows_t + 3) & ~3;
@@ -464,9 +588,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
 #pragma unroll
             for (int q = 0; q < RPT; ++q) { du[q] = 0.0; dl[q] = 0.0; }
             for (int ch = 0; ch < P.n_chunks; ++ch) {
-                const int slot = consumed % P.stages;
-                mbar_wait(&full[slot], (consumed / P.stages) & 1);
-                const float* st = ring + (size_t)slot * stage_floats;
+                if (!P.resident) mbar_wait(&full[cslot], cpar);
+                const float* st = P.resident ? ring + (size_t)ch * P.kc * rp : ring + (size_t)cslot * stage_floats;
                 const int k0 = ch * P.kc;
                 if (active) {
                     if (RPT == 4) {
@@ -490,6 +613,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                                 du[3] = fma(x3, xu, du[3]); dl[3] = fma(x3, xl, dl[3]);
                             }
                         }
+                    } else if (RPT == 2) {
+                        const float2* sp = reinterpret_cast<const float2*>(st) + t;
+                        const int ld2 = rp >> 1;
+#pragma unroll 4
+                        for (int kk = 0; kk < P.kc; ++kk) {
+                            const float2 v = sp[kk * ld2];
+                            const double xu = piv_u[k0 + kk], xl = piv_l[k0 + kk];
+                            const double x0 = v.x, x1 = v.y;
+                            if (KERNEL == 1) {
+                                double e;
+                                e = x0 - xu; du[0] = fma(e, e, du[0]); e = x0 - xl; dl[0] = fma(e, e, dl[0]);
+                                e = x1 - xu; du[1] = fma(e, e, du[1]); e = x1 - xl; dl[1] = fma(e, e, dl[1]);
+                            } else {
+                                du[0] = fma(x0, xu, du[0]); dl[0] = fma(x0, xl, dl[0]);
+                                du[1] = fma(x1, xu, du[1]); dl[1] = fma(x1, xl, dl[1]);
+                            }
+                        }
                     } else {
                         const float* sp = st + t;
 #pragma unroll 8
@@ -507,8 +647,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                     }
                 }
                 __syncwarp();
-                if ((t & 31) == 0) mbar_arrive(&empty[slot]);
-                ++consumed;
+                if (!P.resident) {
+                    if (lane == 0) mbar_arrive(&empty[cslot]);
+                    ++consumed;
+                    if (++cslot == (unsigned)P.stages) { cslot = 0; cpar ^= 1u; }
+                }
+            }
+            if (tile == 0) {
+                SVM_PHASE(timing, PH_ROWS);
+                named_sync(BAR_B);          // c_u, c_l and the owner's flags are ready
+                SVM_PHASE(timing, PH_WAITB);
+                cu = sh.cu; cl = sh.cl;
             }
             if (active) {
 #pragma unroll
@@ -518,8 +667,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                         const long long jg = gbase + j;
                         double ku, kl;
                         if (KERNEL == 1) {
-                            ku = (jg == u) ? 1.0 : svmexp::exp_cr(-(P.gamma * du[q]));
-                            kl = (jg == l) ? 1.0 : svmexp::exp_cr(-(P.gamma * dl[q]));
+                            ku = (jg == u) ? 1.0 : svmexp::exp_cr_t(-(P.gamma * du[q]), tab);
+                            kl = (jg == l) ? 1.0 : svmexp::exp_cr_t(-(P.gamma * dl[q]), tab);
                         } else {
                             ku = du[q]; kl = dl[q];
                         }
@@ -532,11 +681,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                 }
             }
         }
+        warp_reduce_fi<true>(bfu, bju);
+        warp_reduce_fi<false>(bfl, bjl);
+        if (lane == 0) {
+            sh.red_f[0][warp] = bfu; sh.red_i[0][warp] = bju;
+            sh.red_f[1][warp] = bfl; sh.red_i[1][warp] = bjl;
+        }
         ++it;
-        publish(bfu, bju, bfl, bjl);
     }
-
-    // ================= shutdown: stop the producer, drain issued stages
+    // ---- shutdown: stop the producer and drain the stages it issued
     if (t == 0) {
         sh.stop = 1;
         __threadfence_block();
@@ -544,22 +697,27 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
             const int done = sh.producer_done;
             const unsigned int iss = sh.issued;
             if (consumed < iss) {
-                const int slot = consumed % P.stages;
-                mbar_wait(&full[slot], (consumed / P.stages) & 1);
-                for (int w = 0; w < NWC; ++w) mbar_arrive(&empty[slot]);
+                mbar_wait(&full[cslot], cpar);
+                for (int w = 0; w < NWC; ++w) mbar_arrive(&empty[cslot]);
                 ++consumed;
+                if (++cslot == (unsigned)P.stages) { cslot = 0; cpar ^= 1u; }
             } else if (done) {
                 break;
             }
         }
     }
-    bar_consumers();
-    for (int j = t; j < R; j += NT) {
-        P.f[rank][r0 + j] = f_s[j];
-        P.alpha[rank][r0 + j] = a_s[j];
-        P.flags[rank][r0 + j] = fl_s[j];
-    }
-    if (t == 0 && cta == 0) {
+    if (timing)
+        for (int k = 0; k < PH_N; ++k) atomicAdd(&P.timers[k], ph_acc[k]);
+    named_sync(BAR_D);
+    // ---- write the CTA's state back (consumers) and the rank control (scalar warp)
+    if (warp < NWC) {
+        for (int j = t; j < R; j += NT) {
+            P.f[rank][r0 + j] = f_s[j];
+            if (A_SMEM) alpha_g[j] = a_s[j];
+            P.flags[rank][r0 + j] = fl_s[j];
+        }
+    } else if (lane == 0 && cta == 0) {
+        Ctl* ctl = P.ctl[rank];
         ctl->it = it;
         ctl->seq = seq;
         ctl->state = final_state;

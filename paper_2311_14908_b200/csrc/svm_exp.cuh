@@ -28,8 +28,10 @@
 
 #if defined(__CUDACC__)
 #define SVM_HD __host__ __device__ __forceinline__
+#define SVM_HDM __host__ __device__ __forceinline__
 #else
 #define SVM_HD static inline
+#define SVM_HDM inline
 #endif
 
 namespace svmexp {
@@ -45,11 +47,6 @@ static const double h_T_lo[32] = {SVM_EXP_T_LO_INIT};
 static const double h_IF_hi[16] = {SVM_EXP_IF_HI_INIT};
 static const double h_IF_lo[16] = {SVM_EXP_IF_LO_INIT};
 
-#if defined(__CUDA_ARCH__)
-#define SVM_TAB(name, i) __ldg(&d_##name[i])
-#else
-#define SVM_TAB(name, i) (h_##name[i])
-#endif
 
 struct dd { double hi, lo; };
 
@@ -104,7 +101,37 @@ SVM_HD bool rounding_safe(double hi, double lo, int shift) {
     return fabs(fabs(lo) - g) > margin;
 }
 
-SVM_HD double exp_cr(double x) {
+// Table accessors: host arrays, device global arrays (read-only path), or a caller-
+// provided pointer (e.g. a shared-memory copy laid out T_hi[32] T_lo[32] IF_hi[16] IF_lo[16]).
+struct HostTab {
+    SVM_HDM double T_hi(int j) const { return h_T_hi[j]; }
+    SVM_HDM double T_lo(int j) const { return h_T_lo[j]; }
+    SVM_HDM double IF_hi(int i) const { return h_IF_hi[i]; }
+    SVM_HDM double IF_lo(int i) const { return h_IF_lo[i]; }
+};
+#if defined(__CUDACC__)
+struct GlobalTab {
+    __device__ __forceinline__ double T_hi(int j) const { return __ldg(&d_T_hi[j]); }
+    __device__ __forceinline__ double T_lo(int j) const { return __ldg(&d_T_lo[j]); }
+    __device__ __forceinline__ double IF_hi(int i) const { return __ldg(&d_IF_hi[i]); }
+    __device__ __forceinline__ double IF_lo(int i) const { return __ldg(&d_IF_lo[i]); }
+};
+struct PtrTab {
+    const double* p;
+    __device__ __forceinline__ double T_hi(int j) const { return p[j]; }
+    __device__ __forceinline__ double T_lo(int j) const { return p[32 + j]; }
+    __device__ __forceinline__ double IF_hi(int i) const { return p[64 + i]; }
+    __device__ __forceinline__ double IF_lo(int i) const { return p[80 + i]; }
+};
+// copy of the tables in the PtrTab layout (96 doubles)
+__device__ __forceinline__ double table_entry(int e) {
+    return e < 32 ? d_T_hi[e] : e < 64 ? d_T_lo[e - 32] : e < 80 ? d_IF_hi[e - 64] : d_IF_lo[e - 80];
+}
+#endif
+constexpr int EXP_TABLE_DOUBLES = 96;
+
+template <class Tab>
+SVM_HDM double exp_cr_t(double x, const Tab& tab) {
     if (x == 0.0) return 1.0;
     if (x < -708.0) return 0.0;
     double N = rint(x * SVM_EXP_INV_L32);
@@ -118,15 +145,16 @@ SVM_HD double exp_cr(double x) {
     double rlo = (s.lo - p2.lo) - N * SVM_EXP_L32_3;
     dd r = two_sum(s.hi, rlo);
     double rh = r.hi, rl = r.lo;
+    double Th = tab.T_hi(j), Tl = tab.T_lo(j);
     // fast phase
-    double t = SVM_TAB(IF_hi, 10);
-    t = fma(t, rh, SVM_TAB(IF_hi, 9));
-    t = fma(t, rh, SVM_TAB(IF_hi, 8));
-    t = fma(t, rh, SVM_TAB(IF_hi, 7));
-    t = fma(t, rh, SVM_TAB(IF_hi, 6));
-    t = fma(t, rh, SVM_TAB(IF_hi, 5));
-    t = fma(t, rh, SVM_TAB(IF_hi, 4));
-    t = fma(t, rh, SVM_TAB(IF_hi, 3));
+    double t = tab.IF_hi(10);
+    t = fma(t, rh, tab.IF_hi(9));
+    t = fma(t, rh, tab.IF_hi(8));
+    t = fma(t, rh, tab.IF_hi(7));
+    t = fma(t, rh, tab.IF_hi(6));
+    t = fma(t, rh, tab.IF_hi(5));
+    t = fma(t, rh, tab.IF_hi(4));
+    t = fma(t, rh, tab.IF_hi(3));
     double rh2 = rh * rh;
     double tail = t * (rh2 * rh);
     dd q = two_prod(rh, rh);
@@ -134,7 +162,6 @@ SVM_HD double exp_cr(double x) {
     dd b = two_sum(a.hi, 0.5 * q.hi);
     double lo = (a.lo + b.lo) + (rl + (0.5 * q.lo + (rh * rl + tail)));
     dd S = fast_two_sum(b.hi, lo);
-    double Th = SVM_TAB(T_hi, j), Tl = SVM_TAB(T_lo, j);
     dd P = two_prod(Th, S.hi);
     double pl = P.lo + (Th * S.lo + Tl * S.hi);
     dd R = fast_two_sum(P.hi, pl);
@@ -145,9 +172,9 @@ SVM_HD double exp_cr(double x) {
 #endif
     if (!rounding_safe(R.hi, R.lo, 67)) {
         // slow phase: exp(r) with a degree-13 double-double Horner scheme
-        dd p; p.hi = SVM_TAB(IF_hi, 13); p.lo = SVM_TAB(IF_lo, 13);
+        dd p; p.hi = tab.IF_hi(13); p.lo = tab.IF_lo(13);
         for (int i = 12; i >= 0; --i) {
-            dd c; c.hi = SVM_TAB(IF_hi, i); c.lo = SVM_TAB(IF_lo, i);
+            dd c; c.hi = tab.IF_hi(i); c.lo = tab.IF_lo(i);
             p = dd_add(dd_mul(p, r), c);
         }
         dd T; T.hi = Th; T.lo = Tl;
@@ -155,6 +182,14 @@ SVM_HD double exp_cr(double x) {
     }
     double scale = from_bits((uint64_t)(k + 1023) << 52);  // k >= -1022: normal
     return R.hi * scale;
+}
+
+SVM_HD double exp_cr(double x) {
+#if defined(__CUDA_ARCH__)
+    return exp_cr_t(x, GlobalTab());
+#else
+    return exp_cr_t(x, HostTab());
+#endif
 }
 
 }  // namespace svmexp

@@ -12,6 +12,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -125,6 +126,8 @@ int check_params(long long n, long long d, const svm_params* p, svm_params* q) {
 struct Plan {
     int G = 0;        // CTAs per rank
     int rpt = 1, rt = 256, kc = 16, d_pad = 0, n_chunks = 0, stages = 0, state_cap = 0;
+    bool alpha_smem = true;
+    bool resident = false;
     long long cta_stride = 0;
     size_t smem = 0;
 };
@@ -133,17 +136,27 @@ int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl) {
     pl.G = G;
     pl.state_cap = (int)((n_r_max + G - 1) / G);
     if (pl.state_cap < 1) pl.state_cap = 1;
-    pl.rpt = (pl.state_cap >= 2 * NT * 4) ? 4 : 1;
+    // rows per consumer thread: as few tiles per CTA as possible, at most 4 rows
+    pl.rpt = pl.state_cap <= NT ? 1 : (pl.state_cap <= 2 * NT ? 2 : 4);
     pl.rt = NT * pl.rpt;
-    pl.kc = (pl.rt >= 1024) ? 4 : 16;
+    pl.kc = 8192 / pl.rt;                                  // 32 KB stages
     pl.d_pad = (d + pl.kc - 1) / pl.kc * pl.kc;
     pl.n_chunks = pl.d_pad / pl.kc;
     const int n_tiles = (pl.state_cap + pl.rt - 1) / pl.rt;
     pl.cta_stride = (long long)n_tiles * pl.d_pad * pl.rt;
+    pl.alpha_smem = pl.state_cap <= 2048;                  // else alpha stays in HBM
     size_t fixed = (sizeof(Shared) + 127) & ~size_t(127);
-    fixed += 2 * (size_t)pl.d_pad * 8 + (size_t)pl.state_cap * 17;
+    fixed += 2 * (size_t)pl.d_pad * 8 + (size_t)pl.state_cap * (pl.alpha_smem ? 17 : 9);
     fixed = (fixed + 127) & ~size_t(127);
     const size_t stage_bytes = (size_t)pl.kc * pl.rt * 4;
+    // resident mode: the whole (single-tile) X block of a CTA fits next to the state
+    const size_t resident_bytes = (size_t)pl.d_pad * ((pl.state_cap + 3) & ~3) * 4;
+    pl.resident = n_tiles == 1 && fixed + resident_bytes <= (size_t)max_smem && getenv("SVMB200_NO_RESIDENT") == nullptr;
+    if (pl.resident) {
+        pl.stages = 1;
+        pl.smem = fixed + resident_bytes;
+        return SVM_OK;
+    }
     if ((size_t)max_smem <= fixed + 2 * stage_bytes)
         return fail(SVM_ENOMEM, "rows per CTA (" + std::to_string(pl.state_cap) +
                                     ") exceed the shared-memory state capacity; shard over more GPUs");
@@ -155,9 +168,14 @@ int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl) {
 
 typedef void (*KernelFn)(const Params);
 
-KernelFn pick_kernel(int kernel, int rpt) {
-    if (kernel == SVM_RBF) return rpt == 4 ? smo_persistent<1, 4> : smo_persistent<1, 1>;
-    return rpt == 4 ? smo_persistent<0, 4> : smo_persistent<0, 1>;
+template <int K>
+KernelFn pick_rpt(int rpt, bool a_smem) {
+    if (a_smem) return rpt == 4 ? smo_persistent<K, 4, true> : rpt == 2 ? smo_persistent<K, 2, true> : smo_persistent<K, 1, true>;
+    return rpt == 4 ? smo_persistent<K, 4, false> : rpt == 2 ? smo_persistent<K, 2, false> : smo_persistent<K, 1, false>;
+}
+
+KernelFn pick_kernel(int kernel, int rpt, bool a_smem) {
+    return kernel == SVM_RBF ? pick_rpt<1>(rpt, a_smem) : pick_rpt<0>(rpt, a_smem);
 }
 
 int device_limits(int* n_sm, int* max_smem) {
@@ -177,7 +195,7 @@ int solve(SolveArgs& a) {
     Plan pl;
     int rc = make_plan(a.n_rows_max, (int)a.d, a.ctas_per_rank, a.max_smem, pl);
     if (rc) return rc;
-    KernelFn fn = pick_kernel(p.kernel, pl.rpt);
+    KernelFn fn = pick_kernel(p.kernel, pl.rpt, pl.alpha_smem);
     CKR(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
     int per_sm = 0;
     CKR(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, NTHREADS, pl.smem));
@@ -187,8 +205,7 @@ int solve(SolveArgs& a) {
 
     cudaStream_t st = a.stream;
     const int world = a.world;
-    const int g_total = world * a.ctas_per_rank;
-    const size_t mbox_bytes = sizeof(Mailbox) + 2 * (size_t)g_total * sizeof(Partial);
+    const size_t mbox_bytes = svmk::mbox_bytes(a.ctas_per_rank, world);
 
     // ---- per-rank device state (a1)
     std::vector<void*> owned;
@@ -210,8 +227,10 @@ int solve(SolveArgs& a) {
     P.stages = pl.stages; P.rt = pl.rt;
     P.world = world; P.rank_base = a.rank_base; P.ctas_per_rank = a.ctas_per_rank;
     P.n_global = a.n_global; P.xr = a.xr; P.cta_stride = pl.cta_stride;
-    P.check_interval = p.check_interval; P.state_cap = pl.state_cap;
+    P.check_interval = p.check_interval; P.state_cap = pl.state_cap; P.resident = pl.resident ? 1 : 0;
     P.timeout_ns = a.timeout_ns;
+    P.sys_scope = a.mbox_local_alloc ? 0 : 1;
+    const bool want_timers = getenv("SVMB200_PHASE_TIMERS") != nullptr;
     for (int r = 0; r < world; ++r) { P.row_off[r] = a.row_off[r]; P.n_rows[r] = (int)a.n_rows[r]; P.mbox[r] = a.mbox[r]; }
 
     for (int r = a.rank_base; r < a.rank_base + a.nranks_here; ++r) {
@@ -242,6 +261,12 @@ int solve(SolveArgs& a) {
         if ((rc = dalloc((void**)&dtrace, (size_t)a.trace_cap * 16))) { release(); return rc; }
         CKR(cudaMemsetAsync(dtrace, 0xff, (size_t)a.trace_cap * 16, st));
         P.trace = dtrace; P.trace_cap = a.trace_cap;
+    }
+    if (want_timers) {
+        unsigned long long* tm;
+        if ((rc = dalloc((void**)&tm, 8 * sizeof(unsigned long long)))) { release(); return rc; }
+        CKR(cudaMemsetAsync(tm, 0, 8 * sizeof(unsigned long long), st));
+        P.timers = tm;
     }
     unsigned long long* progress_h = nullptr;
     if (cudaHostAlloc(&progress_h, 64, cudaHostAllocMapped) == cudaSuccess) {
@@ -290,6 +315,17 @@ int solve(SolveArgs& a) {
         for (int r = a.rank_base; r < a.rank_base + a.nranks_here; ++r)
             CKR(cudaMemcpyAsync(a.f_out + (a.f_out_global ? a.row_off[r] : 0), P.f[r],
                                 (size_t)a.n_rows[r] * 8, a.f_out_kind, st));
+    }
+    if (P.timers) {
+        unsigned long long tm[8];
+        CKR(cudaMemcpyAsync(tm, P.timers, sizeof(tm), cudaMemcpyDeviceToHost, st));
+        CKR(cudaStreamSynchronize(st));
+        const char* nm[8] = {"waitC", "publish", "exch", "combine", "scalar", "waitA", "rows", "waitB"};
+        fprintf(stderr, "[svmb200] cycles/iter of CTA 0 over %lld iters (rpt=%d kc=%d stages=%d smem=%zu a_smem=%d resident=%d):",
+                hc.it, pl.rpt, pl.kc, pl.stages, pl.smem, (int)pl.alpha_smem, (int)pl.resident);
+        for (int k = 0; k < 8; ++k)
+            fprintf(stderr, " %s=%.0f", nm[k], hc.it ? (double)tm[k] / hc.it : 0.0);
+        fprintf(stderr, "\n");
     }
     if (dtrace) {
         const long long nt = hc.it < a.trace_cap ? hc.it : a.trace_cap;

@@ -1,0 +1,32 @@
+"""Per-phase cycle breakdown of the persistent SMO kernel (profiling aid).
+
+  SVMB200_PHASE_TIMERS=1 python tools/phase_probe.py W2 W3:0 W4:20000 W5:3000
+(workload[:max_iter]; 0 = run to convergence)."""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ.setdefault("SVMB200_PHASE_TIMERS", "1")
+
+import torch  # noqa: E402
+
+import paper_2311_14908_b200 as S  # noqa: E402
+from gen import workloads as W  # noqa: E402
+
+for spec in sys.argv[1:]:
+    name, _, mi = spec.partition(":")
+    w = W.get(name)
+    X, y = w.train()
+    Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    kw = dict(max_iter=int(mi)) if mi and int(mi) > 0 else {}
+    for extra in ({},):
+        S.svm_train_dev(Xd, yd, w.C, w.kernel, w.gamma, w.tol, **kw, **extra)   # warm
+        torch.cuda.synchronize()
+        t0 = time.time()
+        r = S.svm_train_dev(Xd, yd, w.C, w.kernel, w.gamma, w.tol, **kw, **extra)
+        torch.cuda.synchronize()
+        it = r["info"]["iterations"]
+        print(f"{name} {extra} iters={it} solve={r['info']['seconds_solve']:.4f}s "
+              f"us/iter={1e6 * r['info']['seconds_solve'] / it:.2f} GB/s={X.nbytes * it / r['info']['seconds_solve'] / 1e9:.0f}",
+              flush=True)
