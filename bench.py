@@ -177,10 +177,9 @@ def run_ours(args):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > L2 (126 MB)
     comm = None
     if world > 1:
-        uid = S.svm_comm_unique_id() if rank == 0 else bytes(128)
-        t = torch.tensor(list(uid), dtype=torch.uint8, device=dev)
-        dist.broadcast(t, 0)
-        comm = S.svm_comm_init(rank, world, bytes(t.cpu().tolist()), local)
+        from paper_2311_14908_b200.dist import broadcast_uid
+        uid = broadcast_uid(S.svm_comm_unique_id() if rank == 0 else None, dev)
+        comm = S.svm_comm_init(rank, world, uid, local)
 
     def train_once():
         if world == 1:
@@ -191,13 +190,13 @@ def run_ours(args):
         # support vectors of the whole model (alpha gathered across ranks at N > 1)
         alpha = r["alpha"]
         if world > 1:
-            parts = [torch.empty(b[1] - b[0], dtype=torch.float64, device=dev) for b in blocks]
-            dist.all_gather(parts, alpha.contiguous())
-            alpha = torch.cat(parts)
+            from paper_2311_14908_b200.dist import gather_rows
+            alpha = gather_rows(alpha.contiguous(), blocks, dev)
         sv = alpha > 1e-8
         coef = (alpha * yd_full.to(torch.float64))[sv].contiguous()
         Xsv = Xd_full[sv].contiguous()
-        return S.svm_predict_dev(Xsv, coef, r["b"], w.kernel, w.gamma, Xt_d, stream=stream), int(sv.sum())
+        return S.svm_predict_dev(Xsv, coef, r["b"], w.kernel, w.gamma, Xt_d, stream=stream,
+                                 mode=args.predict_mode), int(sv.sum())
 
     def barrier():
         if world > 1:
@@ -234,10 +233,10 @@ def run_ours(args):
     launches = infos[-1]["launches"]
 
     def gmax(vals):
-        v = torch.tensor([statistics.mean(vals)], dtype=torch.float64, device=dev)
         if world > 1:
-            dist.all_reduce(v, op=dist.ReduceOp.MAX)
-        return float(v.item())
+            from paper_2311_14908_b200.dist import max_over_ranks
+            return max_over_ranks(statistics.mean(vals), dev)
+        return statistics.mean(vals)
 
     train_s = gmax(t_train)
     step_s = gmax(t_step)
@@ -253,7 +252,7 @@ def run_ours(args):
             t0 = time.perf_counter()
             rr = S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol)
             svh = rr["alpha"] > 1e-8
-            S.svm_predict(X[svh], (rr["alpha"] * y)[svh], rr["b"], w.kernel, w.gamma, Xt)
+            S.svm_predict(X[svh], (rr["alpha"] * y)[svh], rr["b"], w.kernel, w.gamma, Xt, mode=args.predict_mode)
             e2e_t.append(time.perf_counter() - t0)
         nsv_h = int(svh.sum())
         e2e = {"value": statistics.mean(e2e_t), "unit": "s",
@@ -303,7 +302,9 @@ def run_ours(args):
                    "sample": f"first {k_it} SMO iterations of {w.name} (n={n}) on {thr} host threads "
                              f"({ips:.1f} iters/s); time-to-converge projected to the {iters} iterations "
                              f"of the identical trajectory"}
-        per_launch_launches = (1 + 2 + launches + 1) if world == 1 else (1 + 2 + launches + 1)
+        # validate + build_xblk + init_state + persistent launches; predict: exact 1 kernel,
+        # tensor 4 (2 packs, coef pad, tcgen05 kernel)
+        per_launch_launches = 3 + launches + (4 if args.predict_mode == 1 else 1)
         line = {
             "metric": METRIC, "value": train_s, "unit": "s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
@@ -311,6 +312,7 @@ def run_ours(args):
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{w.name}: {w.config}", "n": n, "d": d, "kernel": "rbf" if w.kernel else "linear",
                        "gamma": w.gamma, "C": w.C, "tol": w.tol, "predict_rows": m, "n_sv": nsv,
+                       "predict": "tcgen05 3xTF32" if args.predict_mode == 1 else "fp64 exact",
                        "parallelism": f"rows sharded over {world} GPU(s)", "l2": "flushed between steps (256 MB write)"},
             "iterations": iters,
             "smo_iters_per_s": iters / train_s,
@@ -341,6 +343,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="W2")
     ap.add_argument("--predict-rows", type=int, default=-1)
+    ap.add_argument("--predict-mode", type=int, default=1, help="0 exact fp64 SIMT, 1 tcgen05 3xTF32")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -122,6 +122,20 @@ int svm_predict_dev(const float* X_sv, const double* coef, int64_t n_sv, int64_t
                     int kernel, double gamma, const float* X_test, int64_t m, double* dec,
                     void* cuda_stream);
 
+/* Prediction mode.  EXACT: fp64 SIMT, the arithmetic of R13/R14/R19, decision
+ * values bit-identical to any implementation of those readings.  TENSOR: the contraction
+ * T * SV^T on the 5th-generation tensor cores (tcgen05.mma kind::tf32, operands split
+ * "3xTF32" = hi*hi + hi*lo + lo*hi, fp32 accumulation in TMEM) with an fp64 epilogue
+ * (distance, exp, coefficient sum); BASELINE.json tolerance 1e-4 absolute. */
+typedef enum { SVM_PREDICT_EXACT = 0, SVM_PREDICT_TENSOR = 1 } svm_predict_mode;
+
+int svm_predict_ex(const float* X_sv, const double* coef, int64_t n_sv, int64_t d, double b,
+                   int kernel, double gamma, const float* X_test, int64_t m, double* dec,
+                   int mode);
+int svm_predict_dev_ex(const float* X_sv, const double* coef, int64_t n_sv, int64_t d, double b,
+                       int kernel, double gamma, const float* X_test, int64_t m, double* dec,
+                       int mode, void* cuda_stream);
+
 /* ---- multi-GPU, one process per GPU (torchrun) -----------------------------------
  * svm_comm_unique_id fills 128 bytes on rank 0 that the caller broadcasts (e.g. with
  * torch.distributed); every rank then calls svm_comm_init.  svm_train_shard trains on

@@ -15,7 +15,7 @@ from typing import Optional
 
 import numpy as np
 
-__all__ = ["LINEAR", "RBF", "SvmError", "lib", "svm_train", "svm_train_ex", "svm_train_dev",
+__all__ = ["LINEAR", "RBF", "PREDICT_EXACT", "PREDICT_TENSOR", "SvmError", "lib", "svm_train", "svm_train_ex", "svm_train_dev",
            "svm_predict", "svm_predict_dev", "svm_comm_unique_id", "svm_comm_init",
            "svm_train_shard", "svm_comm_destroy", "Params", "Info", "version"]
 
@@ -75,6 +75,8 @@ def lib():
         L.svm_train_dev.argtypes = [P, P, i64, i64, P, P, P, P, P, P]
         L.svm_predict.argtypes = [P, P, i64, i64, f64, i32, f64, P, i64, P]
         L.svm_predict_dev.argtypes = [P, P, i64, i64, f64, i32, f64, P, i64, P, P]
+        L.svm_predict_ex.argtypes = [P, P, i64, i64, f64, i32, f64, P, i64, P, i32]
+        L.svm_predict_dev_ex.argtypes = [P, P, i64, i64, f64, i32, f64, P, i64, P, i32, P]
         L.svm_comm_unique_id.argtypes = [P]
         L.svm_comm_init.argtypes = [ctypes.POINTER(ctypes.c_void_p), i32, i32, P, i32]
         L.svm_train_shard.argtypes = [P, P, P, i64, i64, i64, i64, P, P, P, P, P]
@@ -83,6 +85,7 @@ def lib():
         L.svm_last_error.restype = ctypes.c_char_p
         L.svm_version.restype = ctypes.c_char_p
         for name in ("svm_train", "svm_train_ex", "svm_train_dev", "svm_predict", "svm_predict_dev",
+                     "svm_predict_ex", "svm_predict_dev_ex",
                      "svm_comm_unique_id", "svm_comm_init", "svm_train_shard"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
@@ -190,28 +193,35 @@ def svm_train_dev(X, y, C: float, kernel: int, gamma: float = 0.0, tol: float = 
     return out
 
 
-def svm_predict(X_sv, coef, b: float, kernel: int, gamma: float, X_test) -> np.ndarray:
-    """Host arrays -> decision values [m] fp64 (dec = K(X_test, SV) coef + b)."""
+PREDICT_EXACT = 0
+PREDICT_TENSOR = 1
+
+
+def svm_predict(X_sv, coef, b: float, kernel: int, gamma: float, X_test,
+                mode: int = PREDICT_EXACT) -> np.ndarray:
+    """Host arrays -> decision values [m] fp64 (dec = K(X_test, SV) coef + b).
+    mode PREDICT_EXACT (fp64 SIMT, bit-exact) or PREDICT_TENSOR (tcgen05 3xTF32)."""
     X_test = np.ascontiguousarray(X_test, dtype=np.float32)
     m, d = X_test.shape
     X_sv = np.ascontiguousarray(X_sv, dtype=np.float32).reshape(-1, d)
     coef = np.ascontiguousarray(coef, dtype=np.float64)
     assert coef.shape[0] == X_sv.shape[0]
     dec = np.empty(m)
-    _check(lib().svm_predict(_ptr(X_sv), _ptr(coef), coef.shape[0], d, float(b), int(kernel),
-                             float(gamma), _ptr(X_test), m, _ptr(dec)))
+    _check(lib().svm_predict_ex(_ptr(X_sv), _ptr(coef), coef.shape[0], d, float(b), int(kernel),
+                                float(gamma), _ptr(X_test), m, _ptr(dec), int(mode)))
     return dec
 
 
-def svm_predict_dev(X_sv, coef, b: float, kernel: int, gamma: float, X_test, stream=None):
+def svm_predict_dev(X_sv, coef, b: float, kernel: int, gamma: float, X_test, stream=None,
+                    mode: int = PREDICT_EXACT):
     """torch CUDA tensors -> decision values tensor [m] fp64."""
     import torch
     m, d = X_test.shape
     dec = torch.empty(m, dtype=torch.float64, device=X_test.device)
-    _check(lib().svm_predict_dev(ctypes.c_void_p(X_sv.data_ptr()), ctypes.c_void_p(coef.data_ptr()),
-                                 coef.shape[0], d, float(b), int(kernel), float(gamma),
-                                 ctypes.c_void_p(X_test.data_ptr()), m,
-                                 ctypes.c_void_p(dec.data_ptr()), _stream_ptr(stream)))
+    _check(lib().svm_predict_dev_ex(ctypes.c_void_p(X_sv.data_ptr()), ctypes.c_void_p(coef.data_ptr()),
+                                    coef.shape[0], d, float(b), int(kernel), float(gamma),
+                                    ctypes.c_void_p(X_test.data_ptr()), m,
+                                    ctypes.c_void_p(dec.data_ptr()), int(mode), _stream_ptr(stream)))
     return dec
 
 

@@ -8,6 +8,7 @@
 // ascending s -- the oracle's order, so decision values match it bit for bit.
 #include <cuda_runtime.h>
 
+#include "predict_tc.cuh"
 #include "svm_exp.cuh"
 #include "svm_internal.h"
 
@@ -69,9 +70,48 @@ __global__ void __launch_bounds__(TI) k_predict_exact(const float* __restrict__ 
     if (i < m) dec[i] = acc + b;
 }
 
+__global__ void k_pad_coef(const double* __restrict__ coef, long long n, long long n_pad, double* __restrict__ out) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad; i += (long long)gridDim.x * blockDim.x)
+        out[i] = i < n ? coef[i] : 0.0;
+}
+
+// Tensor-core path (predict_tc.cuh): pack both operands to 3xTF32 core-matrix blocks,
+// then one CTA per 128 test rows.
+int predict_device_tc(const float* X_sv, const double* coef, long long n_sv, long long d, double b,
+                      int kernel, double gamma, const float* X_test, long long m, double* dec,
+                      cudaStream_t st) {
+    using namespace svmtc;
+    const long long m_pad = (m + BM - 1) / BM * BM;
+    const long long n_pad = (n_sv + BN - 1) / BN * BN;
+    const int k_chunks = (int)((d + BK - 1) / BK);
+    float *pa = nullptr, *pb = nullptr;
+    double *qt = nullptr, *qs = nullptr, *cf = nullptr;
+    const size_t a_floats = (size_t)m_pad * k_chunks * BK * 2, b_floats = (size_t)n_pad * k_chunks * BK * 2;
+    if (cudaMallocAsync(&pa, a_floats * 4, st) != cudaSuccess || cudaMallocAsync(&pb, b_floats * 4, st) != cudaSuccess ||
+        cudaMallocAsync(&qt, m_pad * 8, st) != cudaSuccess || cudaMallocAsync(&qs, n_pad * 8, st) != cudaSuccess ||
+        cudaMallocAsync(&cf, n_pad * 8, st) != cudaSuccess) {
+        if (pa) cudaFreeAsync(pa, st); if (pb) cudaFreeAsync(pb, st);
+        if (qt) cudaFreeAsync(qt, st); if (qs) cudaFreeAsync(qs, st); if (cf) cudaFreeAsync(cf, st);
+        return fail(SVM_ENOMEM, "predict workspace allocation failed");
+    }
+    k_pack_3xtf32<<<1184, 256, 0, st>>>(X_test, m, (int)d, k_chunks, m_pad, pa, qt);
+    k_pack_3xtf32<<<1184, 256, 0, st>>>(X_sv, n_sv, (int)d, k_chunks, n_pad, pb, qs);
+    k_pad_coef<<<256, 256, 0, st>>>(coef, n_sv, n_pad, cf);
+    const size_t smem = (size_t)STAGES * STAGE_BYTES;
+    auto fn = kernel == SVM_RBF ? k_predict_tc<1> : k_predict_tc<0>;
+    CKR(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    fn<<<(unsigned)(m_pad / BM), NTHREADS, smem, st>>>(pa, pb, qt, qs, cf, k_chunks, (int)(n_pad / BN), m, b,
+                                                        gamma, dec);
+    CKR(cudaGetLastError());
+    cudaFreeAsync(pa, st); cudaFreeAsync(pb, st); cudaFreeAsync(qt, st); cudaFreeAsync(qs, st); cudaFreeAsync(cf, st);
+    return SVM_OK;
+}
+
 int predict_device(const float* X_sv, const double* coef, long long n_sv, long long d, double b,
                    int kernel, double gamma, const float* X_test, long long m, double* dec,
-                   cudaStream_t st) {
+                   cudaStream_t st, int mode) {
+    if (mode == SVM_PREDICT_TENSOR && n_sv > 0)
+        return predict_device_tc(X_sv, coef, n_sv, d, b, kernel, gamma, X_test, m, dec, st);
     const long long grid = (m + TI - 1) / TI;
     if (grid > 0x7fffffffll) return fail(SVM_EINVAL, "too many test rows");
     if (kernel == SVM_RBF)

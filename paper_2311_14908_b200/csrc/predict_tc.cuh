@@ -1,0 +1,260 @@
+// predict_tc.cuh -- batched decision values on the 5th-generation tensor cores.
+//
+//   dec_i = sum_s coef_s K(sv_s, t_i) + b
+//   RBF:    K = exp(-gamma (|t|^2 + |s|^2 - 2 t.s)),  linear: K = t.s
+//
+// The contraction T * SV^T (m x n_sv x d) is a dense GEMM that is never materialised:
+// each CTA owns 128 test rows, streams the support vectors in tiles of 128, and the
+// epilogue turns every 128 x 128 accumulator tile into kernel values and reduces it
+// over the support vectors on the fly.
+//
+//   * operands in "3xTF32": x = hi + lo with hi = x rounded to tf32 and lo = tf32(x - hi);
+//     t.s = hi.hi + hi.lo + lo.hi (three tcgen05.mma kind::tf32 into one fp32 TMEM
+//     accumulator), ~2^-21 relative per product instead of tf32's 2^-11
+//   * operands are pre-packed once into the K-major, no-swizzle core-matrix layout of
+//     tcgen05 shared-memory descriptors (8 rows x 16 bytes per core matrix, LBO = 128 B
+//     between K-adjacent core matrices, SBO = 1024 B between 8-row groups), so every
+//     stage is four contiguous cp.async.bulk copies (A hi/lo, B hi/lo; 16 KB each)
+//   * warp roles: warp 0 producer (bulk copies, mbarrier ring), warp 1 MMA issuer (one
+//     thread; TMEM allocation), warps 2-5 epilogue (tcgen05.ld 32x32b, one test row per
+//     thread); two 128-column TMEM accumulators so the epilogue of tile j overlaps the
+//     MMAs of tile j + 1
+//   * epilogue in fp64: D = |t|^2 + |s|^2 - 2 (t.s) from exact fp64 norms, K = exp(-gamma D)
+//     (CUDA's fp64 exp), dec accumulated with fp64 fma -- fp32 there would cost up to
+//     1e-3 on Adult-like data (C = 100, 15 distinct kernel values, correlated rounding).
+// Not bit-exact (tensor cores); parity vs the oracle is BASELINE.json's 1e-4 absolute.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace svmtc {
+
+constexpr int BM = 128;          // test rows per CTA (MMA M)
+constexpr int BN = 128;          // support vectors per tile (MMA N)
+constexpr int BK = 32;           // tf32 elements per stage (128 B per row)
+constexpr int STAGES = 3;
+constexpr int TILE_FLOATS = BM * BK;           // 4096 floats = 16 KB per operand block
+constexpr int STAGE_BYTES = 4 * TILE_FLOATS * 4;  // A hi, A lo, B hi, B lo
+constexpr int NTHREADS = 192;
+constexpr int TMEM_COLS = 2 * BN;
+
+// element (r, k) of a [rows][BK] block in the core-matrix order
+__host__ __device__ inline int packed_index(int r, int k) {
+    return (((r >> 3) * (BK / 4) + (k >> 2)) << 5) + ((r & 7) << 2) + (k & 3);
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok = 0;
+    while (!ok) {
+        asm volatile("{\n\t.reg .pred p;\n\t"
+                     "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+// shared-memory matrix descriptor: K-major, no swizzle, LBO 128 B, SBO 1024 B, sm100 version 1
+__device__ __forceinline__ uint64_t smem_desc(const void* p) {
+    const uint64_t a = (smem_u32(p) >> 4) & 0x3fffu;
+    return a | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(1024 >> 4) << 32) | (1ull << 46);
+}
+// instruction descriptor: D f32, A/B tf32, both K-major, N = BN, M = BM
+constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                           ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
+    asm volatile("{\n\t.reg .pred p;\n\t"
+                 "setp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+                 :: "r"(tmem_d), "l"(da), "l"(db), "r"(IDESC), "r"(accumulate) : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                 :: "r"(smem_u32(bar)) : "memory");
+}
+
+template <int KERNEL>
+__global__ void __launch_bounds__(NTHREADS, 1)
+k_predict_tc(const float* __restrict__ A,   // packed test rows [m_tiles][k_chunks][2][BM*BK]
+             const float* __restrict__ B,   // packed SVs       [n_tiles][k_chunks][2][BN*BK]
+             const double* __restrict__ qt, // |t_i|^2 [m_pad]
+             const double* __restrict__ qs, // |s|^2   [n_pad]
+             const double* __restrict__ cf, // coef    [n_pad] (0 for padding)
+             int k_chunks, int n_tiles, long long m, double b, double gamma,
+             double* __restrict__ dec) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    float* stage_base = reinterpret_cast<float*>(smem_raw);
+    __shared__ uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
+    __shared__ uint32_t tmem_base_sh;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int mt = blockIdx.x;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                     :: "r"(smem_u32(&tmem_base_sh)), "n"(TMEM_COLS) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = tmem_base_sh;
+
+    if (warp == 0) {
+        // ---------------- producer
+        if (lane == 0) {
+            const float* a_tile = A + (size_t)mt * k_chunks * 2 * TILE_FLOATS;
+            int slot = 0;
+            uint32_t par = 0;
+            bool wrapped = false;
+            for (int nt = 0; nt < n_tiles; ++nt) {
+                const float* b_tile = B + (size_t)nt * k_chunks * 2 * TILE_FLOATS;
+                for (int kc = 0; kc < k_chunks; ++kc) {
+                    if (wrapped) mbar_wait(&empty[slot], par ^ 1u);
+                    float* st = stage_base + (size_t)slot * 4 * TILE_FLOATS;
+                    mbar_arrive_tx(&full[slot], STAGE_BYTES);
+                    bulk_g2s(st, a_tile + (size_t)kc * 2 * TILE_FLOATS, 2 * TILE_FLOATS * 4, &full[slot]);
+                    bulk_g2s(st + 2 * TILE_FLOATS, b_tile + (size_t)kc * 2 * TILE_FLOATS, 2 * TILE_FLOATS * 4, &full[slot]);
+                    if (++slot == STAGES) { slot = 0; par ^= 1u; wrapped = true; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer
+        int slot = 0;
+        uint32_t par = 0;
+        for (int nt = 0; nt < n_tiles; ++nt) {
+            const int acc = nt & 1;
+            const uint32_t tacc = tmem + acc * BN;
+            if (nt >= 2) mbar_wait(&tempty[acc], ((nt >> 1) - 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            for (int kc = 0; kc < k_chunks; ++kc) {
+                mbar_wait(&full[slot], par);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                if (lane == 0) {
+                    const float* st = stage_base + (size_t)slot * 4 * TILE_FLOATS;
+                    const float* ahi = st;
+                    const float* alo = st + TILE_FLOATS;
+                    const float* bhi = st + 2 * TILE_FLOATS;
+                    const float* blo = st + 3 * TILE_FLOATS;
+#pragma unroll
+                    for (int k8 = 0; k8 < BK / 8; ++k8) {
+                        const int off = k8 * 64;            // 2 core matrices (256 B) per K = 8
+                        const uint32_t first = (kc == 0 && k8 == 0) ? 0u : 1u;
+                        mma_tf32(tacc, smem_desc(ahi + off), smem_desc(bhi + off), first);
+                        mma_tf32(tacc, smem_desc(ahi + off), smem_desc(blo + off), 1u);
+                        mma_tf32(tacc, smem_desc(alo + off), smem_desc(bhi + off), 1u);
+                    }
+                    mma_commit(&empty[slot]);               // frees the stage when done
+                    if (kc == k_chunks - 1) mma_commit(&tfull[acc]);
+                }
+                __syncwarp();
+                if (++slot == STAGES) { slot = 0; par ^= 1u; }
+            }
+        }
+    } else {
+        // ---------------- epilogue: warps 2..5 -> TMEM lane quarter (warp % 4)
+        const int quarter = warp & 3;
+        const int row = quarter * 32 + lane;
+        const long long gi = (long long)mt * BM + row;
+        const double q_t = qt[(long long)mt * BM + row];
+        double acc_d = 0.0;
+        for (int nt = 0; nt < n_tiles; ++nt) {
+            const int acc = nt & 1;
+            mbar_wait(&tfull[acc], (nt >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const double* qs_t = qs + (size_t)nt * BN;
+            const double* cf_t = cf + (size_t)nt * BN;
+#pragma unroll 1
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+                uint32_t v[32];
+                const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN + c0;
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+                    "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                      "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+                      "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),
+                      "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),
+                      "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll 8
+                for (int j = 0; j < 32; ++j) {
+                    const double dot = (double)__uint_as_float(v[j]);
+                    double kv;
+                    if (KERNEL == 1) {
+                        const double dist = fmax(q_t + __ldg(&qs_t[c0 + j]) - 2.0 * dot, 0.0);
+                        kv = exp(-gamma * dist);
+                    } else {
+                        kv = dot;
+                    }
+                    acc_d = fma(__ldg(&cf_t[c0 + j]), kv, acc_d);
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+        if (gi < m) dec[gi] = acc_d + b;
+    }
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "n"(TMEM_COLS) : "memory");
+    }
+}
+
+// Pack rows [rows][d] fp32 (row-major) into [tiles][k_chunks][hi|lo][BM*BK] tf32 blocks;
+// also |x|^2 in fp64.  Padding rows / features are zero.
+__global__ void k_pack_3xtf32(const float* __restrict__ X, long long rows, int d, int k_chunks,
+                              long long rows_pad, float* __restrict__ out, double* __restrict__ norms) {
+    const long long total = rows_pad * (long long)k_chunks * BK;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long r = e / ((long long)k_chunks * BK);
+        const int k = (int)(e - r * (long long)k_chunks * BK);
+        const float x = (r < rows && k < d) ? X[r * d + k] : 0.0f;
+        uint32_t hb;
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(x));
+        const float hi = __uint_as_float(hb);
+        uint32_t lb;
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lb) : "f"(x - hi));
+        const float lo = __uint_as_float(lb);
+        const long long tile = r / BM;
+        const int rr = (int)(r - tile * BM), kc = k / BK, kk = k - kc * BK;
+        float* blk = out + ((size_t)tile * k_chunks + kc) * 2 * TILE_FLOATS;
+        blk[packed_index(rr, kk)] = hi;
+        blk[TILE_FLOATS + packed_index(rr, kk)] = lo;
+    }
+    for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < rows_pad;
+         r += (long long)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        if (r < rows)
+            for (int k = 0; k < d; ++k) { const double v = X[r * d + k]; s = fma(v, v, s); }
+        norms[r] = s;
+    }
+}
+
+}  // namespace svmtc

@@ -68,6 +68,6 @@ int solve(SolveArgs& a);
 // predict.cu
 int predict_device(const float* X_sv, const double* coef, long long n_sv, long long d, double b,
                    int kernel, double gamma, const float* X_test, long long m, double* dec,
-                   cudaStream_t st);
+                   cudaStream_t st, int mode);
 
 }  // namespace svmint

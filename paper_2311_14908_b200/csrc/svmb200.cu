@@ -517,21 +517,29 @@ extern "C" int svm_train_dev(const float* X, const int8_t* y, int64_t n, int64_t
     return SVM_OK;
 }
 
-extern "C" int svm_predict_dev(const float* X_sv, const double* coef, int64_t n_sv, int64_t d,
-                               double b, int kernel, double gamma, const float* X_test, int64_t m,
-                               double* dec, void* cuda_stream) {
+extern "C" int svm_predict_dev_ex(const float* X_sv, const double* coef, int64_t n_sv, int64_t d,
+                                  double b, int kernel, double gamma, const float* X_test, int64_t m,
+                                  double* dec, int mode, void* cuda_stream) {
     if (d < 1 || m < 0 || n_sv < 0) return fail(SVM_EINVAL, "bad sizes");
     if (m == 0) return SVM_OK;
     if (!dec || !X_test || (n_sv > 0 && (!X_sv || !coef))) return fail(SVM_EINVAL, "null pointer");
     if (kernel != SVM_LINEAR && kernel != SVM_RBF) return fail(SVM_EINVAL, "unknown kernel");
     if (kernel == SVM_RBF && !(gamma > 0.0)) return fail(SVM_EINVAL, "RBF gamma must be > 0");
+    if (mode != SVM_PREDICT_EXACT && mode != SVM_PREDICT_TENSOR) return fail(SVM_EINVAL, "unknown predict mode");
     return predict_device(X_sv, coef, n_sv, d, b, kernel, gamma, X_test, m, dec,
-                          (cudaStream_t)cuda_stream);
+                          (cudaStream_t)cuda_stream, mode);
 }
 
-extern "C" int svm_predict(const float* X_sv, const double* coef, int64_t n_sv, int64_t d,
-                           double b, int kernel, double gamma, const float* X_test, int64_t m,
-                           double* dec) {
+extern "C" int svm_predict_dev(const float* X_sv, const double* coef, int64_t n_sv, int64_t d,
+                               double b, int kernel, double gamma, const float* X_test, int64_t m,
+                               double* dec, void* cuda_stream) {
+    return svm_predict_dev_ex(X_sv, coef, n_sv, d, b, kernel, gamma, X_test, m, dec,
+                              SVM_PREDICT_EXACT, cuda_stream);
+}
+
+extern "C" int svm_predict_ex(const float* X_sv, const double* coef, int64_t n_sv, int64_t d,
+                              double b, int kernel, double gamma, const float* X_test, int64_t m,
+                              double* dec, int mode) {
     if (d < 1 || m < 0 || n_sv < 0) return fail(SVM_EINVAL, "bad sizes");
     if (m == 0) return SVM_OK;
     if (!dec || !X_test || (n_sv > 0 && (!X_sv || !coef))) return fail(SVM_EINVAL, "null pointer");
@@ -553,7 +561,7 @@ extern "C" int svm_predict(const float* X_sv, const double* coef, int64_t n_sv, 
             cudaMemcpyAsync(dC, coef, (size_t)n_sv * 8, cudaMemcpyHostToDevice, st);
         }
         cudaMemcpyAsync(dT, X_test, (size_t)m * d * 4, cudaMemcpyHostToDevice, st);
-        rc = svm_predict_dev(dS, dC, n_sv, d, b, kernel, gamma, dT, m, dD, st);
+        rc = svm_predict_dev_ex(dS, dC, n_sv, d, b, kernel, gamma, dT, m, dD, mode, st);
         if (rc) break;
         if (cudaMemcpyAsync(dec, dD, (size_t)m * 8, cudaMemcpyDeviceToHost, st) != cudaSuccess)
             rc = fail(SVM_ECUDA, "D2H copy failed");
@@ -567,6 +575,12 @@ extern "C" int svm_predict(const float* X_sv, const double* coef, int64_t n_sv, 
     if (rc) return rc;
     if (se != cudaSuccess) return fail(SVM_ECUDA, cudaGetErrorString(se));
     return SVM_OK;
+}
+
+extern "C" int svm_predict(const float* X_sv, const double* coef, int64_t n_sv, int64_t d,
+                           double b, int kernel, double gamma, const float* X_test, int64_t m,
+                           double* dec) {
+    return svm_predict_ex(X_sv, coef, n_sv, d, b, kernel, gamma, X_test, m, dec, SVM_PREDICT_EXACT);
 }
 
 extern "C" const char* svm_last_error(void) { return g_err.c_str(); }

@@ -257,3 +257,36 @@ def test_full_size_converged_properties(S, name):
     rows = np.random.default_rng(1).choice(len(y), 300, replace=False)
     f_ref = O.decision(X[sv], (a * y)[sv], 0.0, w.kernel, w.gamma, X[rows]) - y[rows]
     np.testing.assert_allclose(f[rows], f_ref, atol=1e-6)
+
+
+# ---------------------------------------------------------------- tensor-core predict
+@pytest.mark.parametrize("name,n,m", [("W1", 200, 300), ("W2", 3000, 1500), ("W3", 1500, 400),
+                                      ("W4", 4000, 600), ("W5", 3000, 700)])
+def test_predict_tensor_core_tolerance(S, name, n, m):
+    """tcgen05 3xTF32 path: decision values within BASELINE.json's 1e-4 of the oracle's,
+    identical labels wherever the oracle's |dec| exceeds that tolerance (ragged m and
+    n_sv: neither is a multiple of the 128-row tiles)."""
+    w = W.get(name)
+    X, y = w.train(n)
+    r = O.train(X, y, w.C, w.kernel, w.gamma, w.tol)
+    sv = r.alpha > 1e-8
+    Xt, _ = w.test(m)
+    d_o = O.decision(X[sv], (r.alpha * y)[sv], r.b, w.kernel, w.gamma, Xt)
+    d_t = S.svm_predict(X[sv], (r.alpha * y)[sv], r.b, w.kernel, w.gamma, Xt, mode=S.PREDICT_TENSOR)
+    err = np.max(np.abs(d_t - d_o))
+    assert err <= 1e-4, err
+    clear = np.abs(d_o) > 1e-4
+    assert np.array_equal(np.sign(d_t[clear]), np.sign(d_o[clear]))
+
+
+def test_predict_tensor_core_device_api(S):
+    import torch
+    w = W.get("W5")
+    X, y = w.train(2000)
+    r = O.train(X, y, w.C, w.kernel, w.gamma, w.tol)
+    sv = r.alpha > 1e-8
+    Xt, _ = w.test(1000)
+    d_o = O.decision(X[sv], (r.alpha * y)[sv], r.b, w.kernel, w.gamma, Xt)
+    dev = S.svm_predict_dev(torch.from_numpy(X[sv]).cuda(), torch.from_numpy((r.alpha * y)[sv]).cuda(), r.b,
+                            w.kernel, w.gamma, torch.from_numpy(Xt).cuda(), mode=S.PREDICT_TENSOR)
+    assert np.max(np.abs(dev.cpu().numpy() - d_o)) <= 1e-4
