@@ -53,23 +53,27 @@ enum { BAR_A = 1, BAR_B = 2, BAR_C = 3, BAR_D = 4, BAR_E = 5, BAR_F = 6 };
 enum { ST_RUNNING = 0, ST_CONVERGED = 1, ST_MAXITER = 2, ST_LIMIT = 3, ST_TIMEOUT = -8 };
 enum { FL_POS = 1, FL_UP = 2, FL_LOW = 4 };
 
-// One CTA's candidate record (48 B).
-struct __align__(16) Partial {
-    double f_up, f_low, a_up, a_low;
-    int32_t i_up, i_low;           // global row index, -1 if the set is empty
-    int32_t y_up, y_low;
+// One CTA's candidate record in "LL" form: twelve 8-byte words, each = (32-bit flag << 32)
+// | 32-bit payload, flag = exchange sequence number.  Aligned 8-byte stores are single-copy
+// atomic, so a record whose twelve flags all read `seq` is complete: no release fence is
+// needed on the writer's side.  Payload words: 0-1 f_up, 2-3 f_low, 4-5 a_up, 6-7 a_low
+// (lo, hi halves), 8 i_up, 9 i_low (global row, -1 = empty set), 10 y_up | y_low << 16.
+constexpr int REC_ROW_WORDS = 8;   // binary rows up to 256 features travel in the record
+constexpr int NREP = 4;            // replicas of every record (spreads the all-to-all reads)
+struct __align__(16) Record {
+    unsigned long long w[12 + 2 * REC_ROW_WORDS];   // base words, then the two candidate bit rows
 };
 
 struct __align__(128) Mailbox {
-    unsigned long long count;      // monotonic number of records received
+    unsigned long long count;      // monotonic arrivals (relaxed: a hint that all records landed)
     unsigned long long pad[15];
 };
-// records follow the header: Partial parts[2][g_total] (double-buffered by parity)
-__host__ __device__ inline Partial* mbox_parts(Mailbox* m, int parity, int g_total) {
-    return reinterpret_cast<Partial*>(m + 1) + (size_t)parity * g_total;
+// records follow the header: Record recs[NREP][2][g_total] (replica, exchange parity)
+__host__ __device__ inline Record* mbox_parts(Mailbox* m, int rep, int parity, int g_total) {
+    return reinterpret_cast<Record*>(m + 1) + ((size_t)rep * 2 + parity) * g_total;
 }
 __host__ __device__ inline size_t mbox_bytes(int cpr, int world) {
-    return sizeof(Mailbox) + 2 * (size_t)cpr * world * sizeof(Partial);
+    return sizeof(Mailbox) + (size_t)NREP * 2 * cpr * world * sizeof(Record);
 }
 
 struct Ctl {                       // per rank solver control, persists across launches
@@ -104,15 +108,22 @@ struct Params {
     int check_interval;
     int state_cap;                 // rows per CTA the shared-memory state can hold
     int resident;                  // 1: the CTA's whole X block stays in shared memory (one tile)
+    int bin_words;                 // > 0: X is exactly binary (every value 0 or 1) and stored as
+                                   // bit rows of bin_words 32-bit words (SURVEY §8(f) compact
+                                   // encoding); distances are popcounts -- exact, so identical to
+                                   // the fp64 recurrence R13
+    const uint32_t* xrbits;        // bit rows [n_global][bin_words] (pivot gather)
+    int rec_rows;                  // 1: candidate bit rows travel in the records (bin_words <= 8)
+    int nrep;                      // record replicas written (1..NREP); readers pick cta % nrep
     long long timeout_ns;
     int sys_scope;                 // 1 when mailboxes live on other GPUs (system scope)
     unsigned long long* timers;    // optional [8] per-phase cycle totals of CTA 0
 };
 
-// phase timers: scalar warp lane 0 of CTA 0 ...
-enum { PH_WAITC = 0, PH_PUBLISH, PH_EXCH, PH_COMBINE, PH_SCALAR, PH_WAITA,
-       // ... and consumer thread 0 of CTA 0
-       PH_ROWS, PH_WAITB, PH_N };
+// phase timers (cycles, CTA 0): scalar warp lane 0 ...
+enum { PH_S_WAITC = 0, PH_S_PUBLISH, PH_S_POLL, PH_S_READ, PH_S_PIVOT, PH_S_KUL,
+       // ... and consumer thread 0
+       PH_C_EXCH, PH_C_PIVOT, PH_C_DIST, PH_C_WAITB, PH_C_UPDATE, PH_C_REDUCE, PH_N };
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -268,6 +279,68 @@ __device__ __forceinline__ void cand_warp_merge(Cand& c) {
         cand_merge(c, b);
     }
 }
+__device__ __forceinline__ void ll_store(Record* rec, uint32_t fg, const Cand& c) {
+    unsigned long long* w = rec->w;
+    const unsigned long long bu = (unsigned long long)__double_as_longlong(c.fu);
+    const unsigned long long bl = (unsigned long long)__double_as_longlong(c.fl);
+    const unsigned long long au = (unsigned long long)__double_as_longlong(c.au);
+    const unsigned long long al = (unsigned long long)__double_as_longlong(c.al);
+    const uint32_t iu = c.iu == INT_MAX ? 0xffffffffu : (uint32_t)c.iu;
+    const uint32_t il = c.il == INT_MAX ? 0xffffffffu : (uint32_t)c.il;
+    const uint32_t yy = (uint32_t)((c.yu & 0xffff) | (c.yl << 16));
+    st_volatile_v2(w + 0, ll_word(fg, (uint32_t)bu), ll_word(fg, (uint32_t)(bu >> 32)));
+    st_volatile_v2(w + 2, ll_word(fg, (uint32_t)bl), ll_word(fg, (uint32_t)(bl >> 32)));
+    st_volatile_v2(w + 4, ll_word(fg, (uint32_t)au), ll_word(fg, (uint32_t)(au >> 32)));
+    st_volatile_v2(w + 6, ll_word(fg, (uint32_t)al), ll_word(fg, (uint32_t)(al >> 32)));
+    st_volatile_v2(w + 8, ll_word(fg, iu), ll_word(fg, il));
+    st_volatile_v2(w + 10, ll_word(fg, yy), ll_word(fg, 0u));
+}
+// the two candidate bit rows (W words each) after the 12 base words
+__device__ __forceinline__ void ll_store_rows(Record* rec, uint32_t fg, const uint32_t* ru, const uint32_t* rl, int W) {
+    unsigned long long* w = rec->w + 12;
+    for (int h = 0; h < W; h += 2) {
+        st_volatile_v2(w + h, ll_word(fg, ru[h]), ll_word(fg, h + 1 < W ? ru[h + 1] : 0u));
+        st_volatile_v2(w + REC_ROW_WORDS + h, ll_word(fg, rl[h]), ll_word(fg, h + 1 < W ? rl[h + 1] : 0u));
+    }
+}
+// One attempt: true (and c filled) when every word carries flag fg.
+__device__ __forceinline__ bool ll_try_load(const Record* rec, uint32_t fg, Cand& c) {
+    unsigned long long v[12];
+#pragma unroll
+    for (int h = 0; h < 6; ++h) ld_volatile_v2(rec->w + 2 * h, v[2 * h], v[2 * h + 1]);
+    bool ok = true;
+#pragma unroll
+    for (int h = 0; h < 12; ++h) ok = ok && (uint32_t)(v[h] >> 32) == fg;
+    if (!ok) return false;
+    c.fu = __longlong_as_double((long long)((v[0] & 0xffffffffull) | (v[1] << 32)));
+    c.fl = __longlong_as_double((long long)((v[2] & 0xffffffffull) | (v[3] << 32)));
+    c.au = __longlong_as_double((long long)((v[4] & 0xffffffffull) | (v[5] << 32)));
+    c.al = __longlong_as_double((long long)((v[6] & 0xffffffffull) | (v[7] << 32)));
+    const int iu = (int)(uint32_t)v[8], il = (int)(uint32_t)v[9];
+    c.iu = iu < 0 ? INT_MAX : iu;
+    c.il = il < 0 ? INT_MAX : il;
+    const uint32_t py = (uint32_t)v[10];
+    c.yu = (int)(int16_t)(py & 0xffff);
+    c.yl = (int)(int16_t)(py >> 16);
+    return true;
+}
+__device__ __forceinline__ void red_relaxed_gpu(unsigned long long* p) {
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" :: "l"(p) : "memory");
+}
+__device__ __forceinline__ void red_relaxed_sys(unsigned long long* p) {
+    asm volatile("red.relaxed.sys.global.add.u64 [%0], 1;" :: "l"(p) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_gpu(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 #define SVM_PHASE(on, ph)                                                    \
     do {                                                                     \
         if (on) {                                                            \
@@ -284,11 +357,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Shared& sh = *reinterpret_cast<Shared*>(smem_raw);
     size_t off = (sizeof(Shared) + 127) & ~size_t(127);
-    double* piv_u = reinterpret_cast<double*>(smem_raw + off); off += (size_t)P.d_pad * 8;
-    double* piv_l = reinterpret_cast<double*>(smem_raw + off); off += (size_t)P.d_pad * 8;
+    // pivots interleaved: piv[k] = (x_up[k], x_low[k]) -> one 16-byte broadcast load per k
+    double2* piv = reinterpret_cast<double2*>(smem_raw + off); off += (size_t)P.d_pad * 16;
     double* f_s = reinterpret_cast<double*>(smem_raw + off); off += (size_t)P.state_cap * 8;
     double* a_s = reinterpret_cast<double*>(smem_raw + off); if (A_SMEM) off += (size_t)P.state_cap * 8;
     uint8_t* fl_s = smem_raw + off; off += (size_t)P.state_cap;
+    off = (off + 7) & ~size_t(7);
+    // binary RBF: K for every possible Hamming distance, K_tab[D] = exp_cr(-(gamma D))
+    double* ktab = reinterpret_cast<double*>(smem_raw + off);
+    if (P.bin_words) off += (size_t)(32 * P.bin_words + 1) * 8;
     off = (off + 127) & ~size_t(127);
     float* ring = reinterpret_cast<float*>(smem_raw + off);
     const int stage_floats = P.kc * P.rt;
@@ -322,13 +399,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
     }
     __syncthreads();
     const svmexp::PtrTab tab{sh.exp_tab};
+    if (KERNEL == 1 && P.bin_words) {
+        for (int e = t; e <= 32 * P.bin_words; e += NTHREADS) ktab[e] = svmexp::exp_cr_t(-(P.gamma * (double)e), tab);
+        __syncthreads();
+    }
 
     // ============================================================ producer warp
     if (warp == PRODUCER_WARP) {
         if (P.resident) {
             if (lane == 0 && n_tiles > 0) {
                 const int rp = (R + 3) & ~3;
-                const uint32_t bytes = (uint32_t)P.d_pad * rp * 4u;
+                const uint32_t bytes = P.bin_words ? (uint32_t)(n_tiles * P.bin_words * P.rt * 4)
+                                                   : (uint32_t)P.d_pad * rp * 4u;
                 mbar_arrive_tx(&full[0], bytes);
                 bulk_g2s(ring, xcta, bytes, &full[0]);
             }
@@ -362,7 +444,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
         return;
     }
 
-    unsigned long long ph_acc[PH_N] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long ph_acc[PH_N] = {};
     long long ph_t = clock64();
     const bool is_scalar = (warp == SCALAR_WARP);
     const bool timing = P.timers != nullptr && blockIdx.x == 0 && (t == 0 || (is_scalar && lane == 0));
@@ -396,97 +478,159 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
 
     for (;;) {
         named_sync(BAR_C);                  // consumer candidates are in sh.red_*
-        SVM_PHASE(timing, is_scalar ? PH_WAITC : PH_ROWS);
-        // ---- exchange seq + 1 (a6): the scalar warp stores the CTA record into every
-        // rank's mailbox (peer pointers when the ranks are GPUs) and bumps each rank's
-        // arrival counter with a release reduction; it then waits for all g_total
-        // records of this exchange and reduces them lexicographically (identical in
-        // every CTA of every rank).  Measured on B200 (tools/exchange_bench.cu) this is
-        // the fastest of the grid-wide exchanges tried (~2 us at 148 CTAs).
+        SVM_PHASE(timing, is_scalar ? PH_S_WAITC : PH_C_REDUCE);
+        // ---- exchange seq + 1 (a6).  The scalar warp stores the CTA record (LL form)
+        // into every rank's mailbox -- peer pointers when the ranks are GPUs -- and bumps
+        // each rank's arrival counter with a relaxed reduction (no fence: the records
+        // validate themselves).  One thread polls the local counter; then every thread of
+        // the CTA reads its share of the records (re-reading any whose flags are not yet
+        // current) and the CTA reduces them lexicographically -- identical in every CTA of
+        // every rank.  Chosen by measurement (tools/exchange_bench.cu).
         ++seq;
+        const int g_total = P.world * P.ctas_per_rank;
+        const int par = (int)(seq & 1);
+        const uint32_t fg = (uint32_t)seq;
         if (is_scalar) {
-            const int g_total = P.world * P.ctas_per_rank;
-            const int par = (int)(seq & 1);
             double fu = lane < NWC ? sh.red_f[0][lane] : INF;
             int ju = lane < NWC ? sh.red_i[0][lane] : INT_MAX;
             double fl = lane < NWC ? sh.red_f[1][lane] : -INF;
             int jl = lane < NWC ? sh.red_i[1][lane] : INT_MAX;
             warp_reduce_fi<true>(fu, ju, NWC);
             warp_reduce_fi<false>(fl, jl, NWC);
-            if (lane == 0) {
-                Partial p;
-                p.f_up = fu; p.f_low = fl;
-                p.i_up = (ju == INT_MAX) ? -1 : (int)(gbase + ju);
-                p.i_low = (jl == INT_MAX) ? -1 : (int)(gbase + jl);
-                p.a_up = (ju == INT_MAX) ? 0.0 : (A_SMEM ? a_s[ju] : alpha_g[ju]);
-                p.a_low = (jl == INT_MAX) ? 0.0 : (A_SMEM ? a_s[jl] : alpha_g[jl]);
-                p.y_up = (ju == INT_MAX) ? 0 : ((fl_s[ju] & FL_POS) ? 1 : -1);
-                p.y_low = (jl == INT_MAX) ? 0 : ((fl_s[jl] & FL_POS) ? 1 : -1);
+            // lanes 0-7 hold the CTA result; every lane writes some replica -> broadcast
+            fu = __shfl_sync(0xffffffffu, fu, 0); ju = __shfl_sync(0xffffffffu, ju, 0);
+            fl = __shfl_sync(0xffffffffu, fl, 0); jl = __shfl_sync(0xffffffffu, jl, 0);
+            {
+                Cand c;
+                c.fu = fu; c.fl = fl;
+                c.iu = (ju == INT_MAX) ? INT_MAX : (int)(gbase + ju);
+                c.il = (jl == INT_MAX) ? INT_MAX : (int)(gbase + jl);
+                c.au = (ju == INT_MAX) ? 0.0 : (A_SMEM ? a_s[ju] : alpha_g[ju]);
+                c.al = (jl == INT_MAX) ? 0.0 : (A_SMEM ? a_s[jl] : alpha_g[jl]);
+                c.yu = (ju == INT_MAX) ? 0 : ((fl_s[ju] & FL_POS) ? 1 : -1);
+                c.yl = (jl == INT_MAX) ? 0 : ((fl_s[jl] & FL_POS) ? 1 : -1);
+                uint32_t ru[REC_ROW_WORDS], rl[REC_ROW_WORDS];
+                if (P.rec_rows) {
+                    // the candidates' bit rows, from the resident block [tile][word][row]
+                    const uint32_t* xbits = reinterpret_cast<const uint32_t*>(ring);
+                    const int W = P.bin_words;
+#pragma unroll
+                    for (int h = 0; h < REC_ROW_WORDS; ++h) {
+                        ru[h] = 0u; rl[h] = 0u;
+                        if (h < W && ju != INT_MAX) {
+                            const int tl = ju / P.rt, rin = ju - tl * P.rt, rows_t = min(P.rt, R - tl * P.rt);
+                            ru[h] = xbits[(size_t)tl * W * P.rt + (size_t)h * ((rows_t + 3) & ~3) + rin];
+                        }
+                        if (h < W && jl != INT_MAX) {
+                            const int tl = jl / P.rt, rin = jl - tl * P.rt, rows_t = min(P.rt, R - tl * P.rt);
+                            rl[h] = xbits[(size_t)tl * W * P.rt + (size_t)h * ((rows_t + 3) & ~3) + rin];
+                        }
+                    }
+                }
                 const int gcta = rank * P.ctas_per_rank + cta;
-                for (int r = 0; r < P.world; ++r) mbox_parts(P.mbox[r], par, g_total)[gcta] = p;
-                if (P.sys_scope) {
-                    for (int r = 0; r < P.world; ++r) red_release_sys(&P.mbox[r]->count);
-                } else {
-                    for (int r = 0; r < P.world; ++r) red_release_gpu(&P.mbox[r]->count);
+                for (int q = lane; q < P.world * P.nrep; q += 32) {
+                    Record* rec = mbox_parts(P.mbox[q / P.nrep], q % P.nrep, par, g_total) + gcta;
+                    ll_store(rec, fg, c);
+                    if (P.rec_rows) ll_store_rows(rec, fg, ru, rl, P.bin_words);
+                }
+                __syncwarp();
+                if (lane < P.world) {
+                    if (P.sys_scope) red_relaxed_sys(&P.mbox[lane]->count);
+                    else red_relaxed_gpu(&P.mbox[lane]->count);
                 }
             }
-            SVM_PHASE(timing, PH_PUBLISH);
-            int timeout = 0;
+            SVM_PHASE(timing, PH_S_PUBLISH);
             if (lane == 0) {
                 const unsigned long long target = (unsigned long long)seq * g_total;
                 long long t0 = 0;
                 unsigned int spins = 0;
-                while ((P.sys_scope ? ld_acquire_sys(&my_mb->count) : ld_acquire_gpu(&my_mb->count)) < target) {
+                while ((P.sys_scope ? ld_relaxed_sys(&my_mb->count) : ld_relaxed_gpu(&my_mb->count)) < target) {
                     if ((++spins & 1023u) == 0) {
                         const long long now = globaltimer();
                         if (t0 == 0) t0 = now;
-                        else if (now - t0 > P.timeout_ns) { timeout = 1; break; }
+                        else if (now - t0 > P.timeout_ns) { sh.timeout = 1; break; }
                     }
                 }
             }
-            timeout = __shfl_sync(0xffffffffu, timeout, 0);
-            SVM_PHASE(timing, PH_EXCH);
+            SVM_PHASE(timing, PH_S_POLL);
+        }
+        named_sync(BAR_E);                  // all records have (nearly) landed
+        uint32_t myrow_u[REC_ROW_WORDS], myrow_l[REC_ROW_WORDS];  // bit rows of my best candidates
+        int my_iu = INT_MAX, my_il = INT_MAX;
+        {
             Cand c;
             cand_init(c);
-            if (!timeout) {
-                const Partial* parts = mbox_parts(my_mb, par, g_total);
-                for (int g0 = 0; g0 < g_total; g0 += 32 * 5) {
-                    double2 pf[5], pa[5];
-                    int4 pi[5];
+            if (!sh.timeout) {
+                const Record* recs = mbox_parts(my_mb, cta % P.nrep, par, g_total);
+                long long t0 = 0;
+                unsigned int spins = 0;
+                for (int g = t; g < g_total; g += NSYNC) {
+                    Cand r;
+                    bool ok;
+                    uint32_t wu[REC_ROW_WORDS], wl[REC_ROW_WORDS];
+                    for (;;) {
+                        ok = ll_try_load(recs + g, fg, r);
+                        if (ok && P.rec_rows) {
+                            const unsigned long long* w = recs[g].w + 12;
 #pragma unroll
-                    for (int q = 0; q < 5; ++q) {       // issue every load, then reduce
-                        const int g = g0 + q * 32 + lane;
-                        if (g < g_total) {
-                            pf[q] = __ldcg(reinterpret_cast<const double2*>(&parts[g]));
-                            pa[q] = __ldcg(reinterpret_cast<const double2*>(&parts[g]) + 1);
-                            pi[q] = __ldcg(reinterpret_cast<const int4*>(&parts[g]) + 2);
-                        } else {
-                            pi[q] = make_int4(-1, -1, 0, 0);
+                            for (int h = 0; h < REC_ROW_WORDS; h += 2) {
+                                unsigned long long a0, a1, b0, b1;
+                                if (h < P.bin_words) {
+                                    ld_volatile_v2(w + h, a0, a1);
+                                    ld_volatile_v2(w + REC_ROW_WORDS + h, b0, b1);
+                                    ok = ok && (uint32_t)(a0 >> 32) == fg && (uint32_t)(a1 >> 32) == fg &&
+                                         (uint32_t)(b0 >> 32) == fg && (uint32_t)(b1 >> 32) == fg;
+                                    wu[h] = (uint32_t)a0; wu[h + 1] = (uint32_t)a1;
+                                    wl[h] = (uint32_t)b0; wl[h + 1] = (uint32_t)b1;
+                                } else {
+                                    wu[h] = wu[h + 1] = wl[h] = wl[h + 1] = 0u;
+                                }
+                            }
+                        }
+                        if (ok) break;
+                        if ((++spins & 255u) == 0) {
+                            const long long now = globaltimer();
+                            if (t0 == 0) t0 = now;
+                            else if (now - t0 > P.timeout_ns) { sh.timeout = 1; break; }
                         }
                     }
+                    if (!ok) break;
+                    if (r.iu != INT_MAX && better_up(r.fu, r.iu, c.fu, c.iu)) {
+                        c.fu = r.fu; c.iu = r.iu; c.au = r.au; c.yu = r.yu;
+                        my_iu = r.iu;
 #pragma unroll
-                    for (int q = 0; q < 5; ++q) {
-                        Cand r;
-                        r.fu = pf[q].x; r.fl = pf[q].y; r.au = pa[q].x; r.al = pa[q].y;
-                        r.iu = pi[q].x < 0 ? INT_MAX : pi[q].x; r.il = pi[q].y < 0 ? INT_MAX : pi[q].y;
-                        r.yu = pi[q].z; r.yl = pi[q].w;
-                        cand_merge(c, r);
+                        for (int h = 0; h < REC_ROW_WORDS; ++h) myrow_u[h] = wu[h];
+                    }
+                    if (r.il != INT_MAX && better_low(r.fl, r.il, c.fl, c.il)) {
+                        c.fl = r.fl; c.il = r.il; c.al = r.al; c.yl = r.yl;
+                        my_il = r.il;
+#pragma unroll
+                        for (int h = 0; h < REC_ROW_WORDS; ++h) myrow_l[h] = wl[h];
                     }
                 }
             }
             cand_warp_merge(c);
-            if (lane == 0) {
-                sh.timeout = timeout;
-                sh.wf[0] = c.fu; sh.wi[0] = c.iu; sh.wa[0] = c.au; sh.wy[0] = c.yu;
-                sh.wf[1] = c.fl; sh.wi[1] = c.il; sh.wa[1] = c.al; sh.wy[1] = c.yl;
+            if (lane == 0 && P.bin_words && !P.rec_rows && c.iu != INT_MAX && c.il != INT_MAX) {
+                // the winner is one of the 9 warp results: pull their bit rows into this
+                // SM's L1 now, so the pivot gather after barrier F hits L1
+                asm volatile("prefetch.global.L1 [%0];" :: "l"(P.xrbits + (long long)c.iu * P.bin_words));
+                asm volatile("prefetch.global.L1 [%0];" :: "l"(P.xrbits + (long long)c.il * P.bin_words));
             }
-            __syncwarp();
-            __threadfence_block();
+            if (lane == 0) {
+                sh.cf[0][warp] = c.fu; sh.ci[0][warp] = c.iu; sh.ca[0][warp] = c.au; sh.cy[0][warp] = c.yu;
+                sh.cf[1][warp] = c.fl; sh.ci[1][warp] = c.il; sh.ca[1][warp] = c.al; sh.cy[1][warp] = c.yl;
+            }
         }
         named_sync(BAR_F);
-        SVM_PHASE(timing, is_scalar ? PH_COMBINE : PH_WAITA);
-        const double fu = sh.wf[0], fl = sh.wf[1], au = sh.wa[0], al = sh.wa[1];
-        const int iu = sh.wi[0], il = sh.wi[1], yu = sh.wy[0], yl = sh.wy[1];
+        SVM_PHASE(timing, is_scalar ? PH_S_READ : PH_C_EXCH);
+        // every thread reduces the 9 warp results in the same order -> same winners
+        double fu = sh.cf[0][0], fl = sh.cf[1][0], au = sh.ca[0][0], al = sh.ca[1][0];
+        int iu = sh.ci[0][0], il = sh.ci[1][0], yu = sh.cy[0][0], yl = sh.cy[1][0];
+#pragma unroll
+        for (int w = 1; w < NWC + 1; ++w) {
+            if (better_up(sh.cf[0][w], sh.ci[0][w], fu, iu)) { fu = sh.cf[0][w]; iu = sh.ci[0][w]; au = sh.ca[0][w]; yu = sh.cy[0][w]; }
+            if (better_low(sh.cf[1][w], sh.ci[1][w], fl, il)) { fl = sh.cf[1][w]; il = sh.ci[1][w]; al = sh.ca[1][w]; yl = sh.cy[1][w]; }
+        }
         int dec = ST_RUNNING;
         if (sh.timeout) dec = ST_TIMEOUT;
         else if (iu == INT_MAX || il == INT_MAX) dec = ST_CONVERGED;
@@ -498,8 +642,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
             if (t == 0) { sh.u = iu; sh.l = il; sh.f_up = fu; sh.f_low = fl; }
             break;
         }
-        // ---- pivot rows x_up, x_low (fp64 in shared memory), all threads
-        {
+        // ---- pivot rows x_up, x_low (fp64 in shared memory, or bit rows), all threads
+        if (P.rec_rows) {
+            uint32_t* pw = reinterpret_cast<uint32_t*>(piv);
+            if (my_iu == iu)
+                for (int h = 0; h < P.bin_words; ++h) pw[h] = myrow_u[h];
+            if (my_il == il)
+                for (int h = 0; h < P.bin_words; ++h) pw[P.bin_words + h] = myrow_l[h];
+        } else if (P.bin_words) {
+            uint32_t* pw = reinterpret_cast<uint32_t*>(piv);
+            if (t < 2 * P.bin_words) {
+                const int w = t % P.bin_words;
+                pw[t] = __ldg(&P.xrbits[(long long)(t < P.bin_words ? iu : il) * P.bin_words + w]);
+            }
+        } else {
             const float* xu_g = P.xr + (long long)iu * P.d;
             const float* xl_g = P.xr + (long long)il * P.d;
             for (int k0 = 0; k0 < P.d_pad; k0 += NSYNC * 4) {
@@ -513,30 +669,44 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const int k = k0 + q * NSYNC + t;
-                    if (k < P.d_pad) { piv_u[k] = (double)vu[q]; piv_l[k] = (double)vl[q]; }
+                    if (k < P.d_pad) piv[k] = make_double2((double)vu[q], (double)vl[q]);
                 }
             }
         }
         named_sync(BAR_A);
-        SVM_PHASE(timing, is_scalar ? PH_COMBINE : PH_WAITA);
+        SVM_PHASE(timing, is_scalar ? PH_S_PIVOT : PH_C_PIVOT);
         const int u = iu, l = il;
         if (is_scalar) {
             // ---- pair update (a2): eta, clipped step, snapped alphas (lane 0)
             if (lane == 0) {
                 double Kuu, Kll, Kul;
-                if (KERNEL == 1) {
+                if (P.bin_words) {
+                    const uint32_t* pw = reinterpret_cast<const uint32_t*>(piv);
+                    int cuu = 0, cll = 0, cul = 0, cx = 0;
+                    for (int w = 0; w < P.bin_words; ++w) {
+                        const uint32_t a = pw[w], bb = pw[P.bin_words + w];
+                        cuu += __popc(a); cll += __popc(bb); cul += __popc(a & bb); cx += __popc(a ^ bb);
+                    }
+                    if (KERNEL == 1) {
+                        Kuu = 1.0; Kll = 1.0;
+                        Kul = (u == l) ? 1.0 : ktab[cx];
+                    } else {
+                        Kuu = (double)cuu; Kll = (double)cll; Kul = (double)cul;
+                    }
+                } else if (KERNEL == 1) {
                     double acc = 0.0;
 #pragma unroll 8
-                    for (int k = 0; k < P.d; ++k) { const double dv = piv_u[k] - piv_l[k]; acc = fma(dv, dv, acc); }
+                    for (int k = 0; k < P.d; ++k) { const double2 pv = piv[k]; const double dv = pv.x - pv.y; acc = fma(dv, dv, acc); }
                     Kuu = 1.0; Kll = 1.0;
                     Kul = (u == l) ? 1.0 : svmexp::exp_cr_t(-(P.gamma * acc), tab);
                 } else {
                     double s_uu = 0.0, s_ll = 0.0, s_ul = 0.0;
 #pragma unroll 8
                     for (int k = 0; k < P.d; ++k) {
-                        s_uu = fma(piv_u[k], piv_u[k], s_uu);
-                        s_ll = fma(piv_l[k], piv_l[k], s_ll);
-                        s_ul = fma(piv_u[k], piv_l[k], s_ul);
+                        const double2 pv = piv[k];
+                        s_uu = fma(pv.x, pv.x, s_uu);
+                        s_ll = fma(pv.y, pv.y, s_ll);
+                        s_ul = fma(pv.x, pv.y, s_ul);
                     }
                     Kuu = s_uu; Kll = s_ll; Kul = s_ul;
                 }
@@ -567,10 +737,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                 }
                 if (P.progress && rank == 0 && cta == 0 && (it % P.check_interval) == 0)
                     *(volatile unsigned long long*)P.progress = (unsigned long long)it;
-                __threadfence_block();
             }
             __syncwarp();
-            SVM_PHASE(timing, PH_SCALAR);
+            SVM_PHASE(timing, PH_S_KUL);
             named_arrive(BAR_B);
             ++it;
             continue;
@@ -587,7 +756,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
             double du[RPT], dl[RPT];
 #pragma unroll
             for (int q = 0; q < RPT; ++q) { du[q] = 0.0; dl[q] = 0.0; }
-            for (int ch = 0; ch < P.n_chunks; ++ch) {
+            if (P.bin_words) {
+                if (active) {
+                    // bit rows resident in shared memory: [tile][word][row], popcounts
+                    const uint32_t* xb = reinterpret_cast<const uint32_t*>(ring) + (size_t)tile * P.bin_words * P.rt + t;
+                    const uint32_t* pw = reinterpret_cast<const uint32_t*>(piv);
+                    int cu_ = 0, cl_ = 0;
+                    for (int w = 0; w < P.bin_words; ++w) {
+                        const uint32_t xv = xb[(size_t)w * rp];
+                        if (KERNEL == 1) { cu_ += __popc(xv ^ pw[w]); cl_ += __popc(xv ^ pw[P.bin_words + w]); }
+                        else { cu_ += __popc(xv & pw[w]); cl_ += __popc(xv & pw[P.bin_words + w]); }
+                    }
+                    du[0] = (double)cu_; dl[0] = (double)cl_;
+                }
+            }
+            for (int ch = 0; ch < (P.bin_words ? 0 : P.n_chunks); ++ch) {
                 if (!P.resident) mbar_wait(&full[cslot], cpar);
                 const float* st = P.resident ? ring + (size_t)ch * P.kc * rp : ring + (size_t)cslot * stage_floats;
                 const int k0 = ch * P.kc;
@@ -598,7 +781,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
 #pragma unroll 4
                         for (int kk = 0; kk < P.kc; ++kk) {
                             const float4 v = sp[kk * ld4];
-                            const double xu = piv_u[k0 + kk], xl = piv_l[k0 + kk];
+                            const double2 pv = piv[k0 + kk]; const double xu = pv.x, xl = pv.y;
                             const double x0 = v.x, x1 = v.y, x2 = v.z, x3 = v.w;
                             if (KERNEL == 1) {
                                 double e;
@@ -619,7 +802,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
 #pragma unroll 4
                         for (int kk = 0; kk < P.kc; ++kk) {
                             const float2 v = sp[kk * ld2];
-                            const double xu = piv_u[k0 + kk], xl = piv_l[k0 + kk];
+                            const double2 pv = piv[k0 + kk]; const double xu = pv.x, xl = pv.y;
                             const double x0 = v.x, x1 = v.y;
                             if (KERNEL == 1) {
                                 double e;
@@ -635,7 +818,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
 #pragma unroll 8
                         for (int kk = 0; kk < P.kc; ++kk) {
                             const double x0 = sp[kk * rp];
-                            const double xu = piv_u[k0 + kk], xl = piv_l[k0 + kk];
+                            const double2 pv = piv[k0 + kk]; const double xu = pv.x, xl = pv.y;
                             if (KERNEL == 1) {
                                 double e;
                                 e = x0 - xu; du[0] = fma(e, e, du[0]);
@@ -654,9 +837,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                 }
             }
             if (tile == 0) {
-                SVM_PHASE(timing, PH_ROWS);
+                SVM_PHASE(timing, PH_C_DIST);
                 named_sync(BAR_B);          // c_u, c_l and the owner's flags are ready
-                SVM_PHASE(timing, PH_WAITB);
+                SVM_PHASE(timing, PH_C_WAITB);
                 cu = sh.cu; cl = sh.cl;
             }
             if (active) {
@@ -666,7 +849,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                     if (j < R) {
                         const long long jg = gbase + j;
                         double ku, kl;
-                        if (KERNEL == 1) {
+                        if (KERNEL == 1 && P.bin_words) {
+                            ku = (jg == u) ? 1.0 : ktab[(int)du[q]];
+                            kl = (jg == l) ? 1.0 : ktab[(int)dl[q]];
+                        } else if (KERNEL == 1) {
                             ku = (jg == u) ? 1.0 : svmexp::exp_cr_t(-(P.gamma * du[q]), tab);
                             kl = (jg == l) ? 1.0 : svmexp::exp_cr_t(-(P.gamma * dl[q]), tab);
                         } else {
@@ -681,6 +867,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                 }
             }
         }
+        SVM_PHASE(timing, PH_C_UPDATE);
         warp_reduce_fi<true>(bfu, bju);
         warp_reduce_fi<false>(bfl, bjl);
         if (lane == 0) {

@@ -53,6 +53,46 @@ __global__ void k_build_xblk(const float* __restrict__ X, long long n_r, int d, 
     }
 }
 
+// counts values of X that are not exactly 0 or 1
+__global__ void k_count_nonbinary(const float* __restrict__ X, long long nx, unsigned long long* out) {
+    unsigned long long c = 0;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < nx; e += (long long)gridDim.x * blockDim.x) {
+        const float v = X[e];
+        c += (v != 0.0f && v != 1.0f);
+    }
+    if (c) atomicAdd(out, c);
+}
+
+// bit rows: bit k of word k/32 of row r = X[r][k]
+__global__ void k_pack_bits(const float* __restrict__ X, long long n, int d, int W, uint32_t* __restrict__ out) {
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n * W; e += (long long)gridDim.x * blockDim.x) {
+        const long long r = e / W;
+        const int w = (int)(e - r * W);
+        uint32_t v = 0;
+        for (int b = 0; b < 32; ++b) {
+            const int k = w * 32 + b;
+            if (k < d && X[r * d + k] != 0.0f) v |= 1u << b;
+        }
+        out[e] = v;
+    }
+}
+
+// CTA-blocked bit layout of one rank's rows: xb[c*cta_stride + tile*W*rt + w*rp + rin]
+__global__ void k_build_xbits(const uint32_t* __restrict__ bits, long long n_r, int W, int G, int rt,
+                              long long cta_stride, uint32_t* __restrict__ xb) {
+    const int c = blockIdx.y;
+    const long long r0 = (n_r * c) / G, r1 = (n_r * (c + 1)) / G;
+    const long long R = r1 - r0;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < R * W; e += (long long)gridDim.x * blockDim.x) {
+        const long long j = e / W;
+        const int w = (int)(e - j * W);
+        const long long tile = j / rt, rin = j - tile * rt;
+        const long long rows_t = (R - tile * rt) < rt ? (R - tile * rt) : rt;
+        const long long rp = (rows_t + 3) & ~3ll;
+        xb[(long long)c * cta_stride + tile * (long long)W * rt + w * rp + rin] = bits[(r0 + j) * W + w];
+    }
+}
+
 __global__ void k_init_state(const int8_t* __restrict__ y, long long n, double C,
                              const double* __restrict__ alpha0, const double* __restrict__ f0,
                              double* __restrict__ f, double* __restrict__ alpha,
@@ -128,16 +168,43 @@ struct Plan {
     int rpt = 1, rt = 256, kc = 16, d_pad = 0, n_chunks = 0, stages = 0, state_cap = 0;
     bool alpha_smem = true;
     bool resident = false;
+    int bin_words = 0;
     long long cta_stride = 0;
     size_t smem = 0;
 };
 
-int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl) {
+int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl, bool binary = false) {
     pl.G = G;
+    if (binary) {
+        // bit rows, resident in shared memory, one row per consumer thread
+        pl.state_cap = (int)((n_r_max + G - 1) / G);
+        if (pl.state_cap < 1) pl.state_cap = 1;
+        pl.rpt = 1; pl.rt = NT; pl.kc = 32;
+        pl.bin_words = (d + 31) / 32;
+        pl.d_pad = pl.bin_words * 32;                      // pivot region sizing only
+        pl.n_chunks = 0;
+        const int n_tiles = (pl.state_cap + pl.rt - 1) / pl.rt;
+        pl.cta_stride = (long long)n_tiles * pl.bin_words * pl.rt;
+        pl.alpha_smem = pl.state_cap <= 2048;
+        size_t fixed = (sizeof(Shared) + 127) & ~size_t(127);
+        fixed += 2 * (size_t)pl.d_pad * 8 + (size_t)pl.state_cap * (pl.alpha_smem ? 17 : 9);
+        fixed = ((fixed + 7) & ~size_t(7)) + (size_t)(32 * pl.bin_words + 1) * 8;   // K table
+        fixed = (fixed + 127) & ~size_t(127);
+        const size_t bytes = (size_t)pl.cta_stride * 4;
+        pl.resident = true;
+        pl.stages = 1;
+        pl.smem = fixed + bytes;
+        if (pl.smem > (size_t)max_smem) return fail(SVM_ENOMEM, "binary block does not fit");
+        return SVM_OK;
+    }
     pl.state_cap = (int)((n_r_max + G - 1) / G);
     if (pl.state_cap < 1) pl.state_cap = 1;
     // rows per consumer thread: as few tiles per CTA as possible, at most 4 rows
     pl.rpt = pl.state_cap <= NT ? 1 : (pl.state_cap <= 2 * NT ? 2 : 4);
+    if (const char* e = getenv("SVMB200_RPT")) {          // tuning override: 1, 2 or 4
+        const int r = atoi(e);
+        if (r == 1 || r == 2 || r == 4) pl.rpt = r;
+    }
     pl.rt = NT * pl.rpt;
     pl.kc = 8192 / pl.rt;                                  // 32 KB stages
     pl.d_pad = (d + pl.kc - 1) / pl.kc * pl.kc;
@@ -146,7 +213,7 @@ int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl) {
     pl.cta_stride = (long long)n_tiles * pl.d_pad * pl.rt;
     pl.alpha_smem = pl.state_cap <= 2048;                  // else alpha stays in HBM
     size_t fixed = (sizeof(Shared) + 127) & ~size_t(127);
-    fixed += 2 * (size_t)pl.d_pad * 8 + (size_t)pl.state_cap * (pl.alpha_smem ? 17 : 9);
+    fixed += 2 * (size_t)pl.d_pad * 8 + (size_t)pl.state_cap * (pl.alpha_smem ? 17 : 9);  // pivots + state
     fixed = (fixed + 127) & ~size_t(127);
     const size_t stage_bytes = (size_t)pl.kc * pl.rt * 4;
     // resident mode: the whole (single-tile) X block of a CTA fits next to the state
@@ -193,8 +260,26 @@ int device_limits(int* n_sm, int* max_smem) {
 int solve(SolveArgs& a) {
     const svm_params& p = a.p;
     Plan pl;
-    int rc = make_plan(a.n_rows_max, (int)a.d, a.ctas_per_rank, a.max_smem, pl);
-    if (rc) return rc;
+    int rc = SVM_OK;
+    bool binary = false;
+    if (getenv("SVMB200_NO_BINARY") == nullptr && a.d <= 1024) {
+        unsigned long long* dc = nullptr;
+        CKR(cudaMallocAsync(&dc, 8, a.stream));
+        CKR(cudaMemsetAsync(dc, 0, 8, a.stream));
+        k_count_nonbinary<<<1024, 256, 0, a.stream>>>(a.xr, a.n_global * a.d, dc);
+        unsigned long long nb = 1;
+        CKR(cudaMemcpyAsync(&nb, dc, 8, cudaMemcpyDeviceToHost, a.stream));
+        CKR(cudaFreeAsync(dc, a.stream));
+        CKR(cudaStreamSynchronize(a.stream));
+        binary = (nb == 0);
+    }
+    if (binary && make_plan(a.n_rows_max, (int)a.d, a.ctas_per_rank, a.max_smem, pl, true) != SVM_OK)
+        binary = false;
+    if (!binary) {
+        pl = Plan();
+        rc = make_plan(a.n_rows_max, (int)a.d, a.ctas_per_rank, a.max_smem, pl);
+        if (rc) return rc;
+    }
     KernelFn fn = pick_kernel(p.kernel, pl.rpt, pl.alpha_smem);
     CKR(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
     int per_sm = 0;
@@ -228,6 +313,14 @@ int solve(SolveArgs& a) {
     P.world = world; P.rank_base = a.rank_base; P.ctas_per_rank = a.ctas_per_rank;
     P.n_global = a.n_global; P.xr = a.xr; P.cta_stride = pl.cta_stride;
     P.check_interval = p.check_interval; P.state_cap = pl.state_cap; P.resident = pl.resident ? 1 : 0;
+    P.bin_words = pl.bin_words;
+    // Candidate bit rows inside the records (saves the pivot round trip) measured slower on
+    // W2 (larger records, row extraction on the publish path): off unless requested.
+    P.rec_rows = 0;
+    if (const char* e = getenv("SVMB200_RECROWS"))
+        P.rec_rows = (pl.bin_words > 0 && pl.bin_words <= REC_ROW_WORDS && atoi(e) != 0) ? 1 : 0;
+    P.nrep = NREP;                                         // 4 replicas: measured best on W2
+    if (const char* e = getenv("SVMB200_NREP")) { const int v = atoi(e); if (v >= 1 && v <= NREP) P.nrep = v; }
     P.timeout_ns = a.timeout_ns;
     P.sys_scope = a.mbox_local_alloc ? 0 : 1;
     const bool want_timers = getenv("SVMB200_PHASE_TIMERS") != nullptr;
@@ -244,7 +337,18 @@ int solve(SolveArgs& a) {
         CKR(cudaMemsetAsync(xb, 0, (size_t)pl.cta_stride * pl.G * 4, st));
         CKR(cudaMemsetAsync(ctl, 0, sizeof(Ctl), st));
         dim3 bg(256, pl.G);
-        k_build_xblk<<<bg, 256, 0, st>>>(a.x_rank[r], nr, (int)a.d, pl.d_pad, pl.G, pl.rt, pl.cta_stride, xb);
+        if (pl.bin_words) {
+            if (!P.xrbits) {
+                uint32_t* xrb;
+                if ((rc = dalloc((void**)&xrb, (size_t)a.n_global * pl.bin_words * 4))) { release(); return rc; }
+                k_pack_bits<<<1024, 256, 0, st>>>(a.xr, a.n_global, (int)a.d, pl.bin_words, xrb);
+                P.xrbits = xrb;
+            }
+            k_build_xbits<<<bg, 256, 0, st>>>(P.xrbits + a.row_off[r] * pl.bin_words, nr, pl.bin_words, pl.G,
+                                               pl.rt, pl.cta_stride, reinterpret_cast<uint32_t*>(xb));
+        } else {
+            k_build_xblk<<<bg, 256, 0, st>>>(a.x_rank[r], nr, (int)a.d, pl.d_pad, pl.G, pl.rt, pl.cta_stride, xb);
+        }
         k_init_state<<<256, 256, 0, st>>>(a.y_rank[r], nr, p.C, a.alpha0 ? a.alpha0 + a.row_off[r] : nullptr,
                                           a.f0 ? a.f0 + a.row_off[r] : nullptr, f, al, fl);
         CKR(cudaGetLastError());
@@ -264,8 +368,8 @@ int solve(SolveArgs& a) {
     }
     if (want_timers) {
         unsigned long long* tm;
-        if ((rc = dalloc((void**)&tm, 8 * sizeof(unsigned long long)))) { release(); return rc; }
-        CKR(cudaMemsetAsync(tm, 0, 8 * sizeof(unsigned long long), st));
+        if ((rc = dalloc((void**)&tm, PH_N * sizeof(unsigned long long)))) { release(); return rc; }
+        CKR(cudaMemsetAsync(tm, 0, PH_N * sizeof(unsigned long long), st));
         P.timers = tm;
     }
     unsigned long long* progress_h = nullptr;
@@ -317,13 +421,14 @@ int solve(SolveArgs& a) {
                                 (size_t)a.n_rows[r] * 8, a.f_out_kind, st));
     }
     if (P.timers) {
-        unsigned long long tm[8];
+        unsigned long long tm[PH_N];
         CKR(cudaMemcpyAsync(tm, P.timers, sizeof(tm), cudaMemcpyDeviceToHost, st));
         CKR(cudaStreamSynchronize(st));
-        const char* nm[8] = {"waitC", "publish", "exch", "combine", "scalar", "waitA", "rows", "waitB"};
-        fprintf(stderr, "[svmb200] cycles/iter of CTA 0 over %lld iters (rpt=%d kc=%d stages=%d smem=%zu a_smem=%d resident=%d):",
-                hc.it, pl.rpt, pl.kc, pl.stages, pl.smem, (int)pl.alpha_smem, (int)pl.resident);
-        for (int k = 0; k < 8; ++k)
+        const char* nm[PH_N] = {"S.waitC", "S.publish", "S.poll", "S.read", "S.pivot", "S.kul",
+                                "C.exch", "C.pivot", "C.dist", "C.waitB", "C.update", "C.reduce"};
+        fprintf(stderr, "[svmb200] cycles/iter of CTA 0 over %lld iters (rpt=%d kc=%d stages=%d smem=%zu a_smem=%d resident=%d bin_words=%d):",
+                hc.it, pl.rpt, pl.kc, pl.stages, pl.smem, (int)pl.alpha_smem, (int)pl.resident, pl.bin_words);
+        for (int k = 0; k < PH_N; ++k)
             fprintf(stderr, " %s=%.0f", nm[k], hc.it ? (double)tm[k] / hc.it : 0.0);
         fprintf(stderr, "\n");
     }

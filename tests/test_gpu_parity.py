@@ -290,3 +290,27 @@ def test_predict_tensor_core_device_api(S):
     dev = S.svm_predict_dev(torch.from_numpy(X[sv]).cuda(), torch.from_numpy((r.alpha * y)[sv]).cuda(), r.b,
                             w.kernel, w.gamma, torch.from_numpy(Xt).cuda(), mode=S.PREDICT_TENSOR)
     assert np.max(np.abs(dev.cpu().numpy() - d_o)) <= 1e-4
+
+
+def test_binary_encoding_equals_fp_path(S, monkeypatch):
+    """Exactly-binary X (Adult-like) runs on bit rows with popcount distances (compact
+    encoding); the result must equal both the oracle and the fp32-row path."""
+    w = W.get("W2")
+    X, y = w.train(2500)
+    r_or = O.train(X, y, w.C, w.kernel, w.gamma, w.tol, trace_cap=100000)
+    r_bin = S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol, want_f=True, trace_cap=100000)
+    monkeypatch.setenv("SVMB200_NO_BINARY", "1")
+    r_fp = S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol, want_f=True, trace_cap=100000)
+    _assert_exact(r_bin, r_or)
+    _assert_exact(r_fp, r_or)
+    # linear kernel on binary rows (dot = popcount of AND), ragged sizes, many ties
+    rng = np.random.default_rng(8)
+    for n, d in ((37, 5), (300, 70), (1031, 33)):
+        Xb = (rng.random((n, d)) < 0.3).astype(np.float32)
+        yb = np.where(rng.random(n) < 0.5, 1, -1).astype(np.int8)
+        yb[0], yb[-1] = 1, -1
+        for kern, gamma in ((O.LINEAR, 0.0), (O.RBF, 0.2)):
+            wb = W.Workload("b", "", n, d, kern, gamma, 1.5, 1e-3, 0, 0, 0, None)
+            monkeypatch.delenv("SVMB200_NO_BINARY", raising=False)
+            r_g, r_o = _run_pair(S, wb, Xb, yb)
+            _assert_exact(r_g, r_o)
