@@ -314,3 +314,23 @@ def test_binary_encoding_equals_fp_path(S, monkeypatch):
             monkeypatch.delenv("SVMB200_NO_BINARY", raising=False)
             r_g, r_o = _run_pair(S, wb, Xb, yb)
             _assert_exact(r_g, r_o)
+
+
+def test_train_shard_single_rank(S):
+    """The one-process-per-GPU entry point (NCCL bootstrap, IPC mailbox, system-scope
+    exchange) with world = 1 on one GPU reproduces the oracle."""
+    import torch
+    w = W.get("W5")
+    X, y = w.train(3000)
+    uid = S.svm_comm_unique_id()
+    comm = S.svm_comm_init(0, 1, uid, 0)
+    try:
+        r = S.svm_train_shard(comm, torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda(), 0, len(y),
+                              w.C, w.kernel, w.gamma, w.tol)
+    finally:
+        S.svm_comm_destroy(comm)
+    r_or = O.train(X, y, w.C, w.kernel, w.gamma, w.tol)
+    assert r["info"]["iterations"] == r_or.iterations
+    np.testing.assert_array_equal(r["alpha"].cpu().numpy(), r_or.alpha)
+    assert r["b"] == r_or.b
+    assert r["info"]["dual_objective"] == pytest.approx(O.dual_objective_from_f(r_or.alpha, y, r_or.f), rel=1e-12)
