@@ -74,10 +74,13 @@ def gaussian_blobs(n: int, seed: int, d: int = 2, m: int = 2,
     Class 0 -> +1, every other class -> -1 (binary use).  Rows are shuffled.
     Returns class ids in y when m > 2 (int8 in [0, m))."""
     rng = _rng(seed)
+    # the class centers are part of the law (shared by train and test draws), so they
+    # come from a generator fixed by (m, d, separation), not by the sample seed
+    law = _rng(9000 + 97 * m + d + int(1000 * separation))
     while True:
-        centers = rng.standard_normal((m, d)) * separation
+        centers = law.standard_normal((m, d)) * separation
         if m == 2:
-            u = rng.standard_normal(d)
+            u = law.standard_normal(d)
             u /= np.linalg.norm(u)
             centers = np.stack([0.5 * separation * u, -0.5 * separation * u])
         dist = np.linalg.norm(centers[:, None, :] - centers[None, :, :], axis=-1)

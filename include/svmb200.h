@@ -111,6 +111,17 @@ int svm_train_dev(const float* X, const int8_t* y, int64_t n, int64_t d, const s
                   double* alpha, double* b, svm_info* info, const svm_debug* dbg,
                   void* cuda_stream);
 
+/* B independent binary problems with the same controls, solved concurrently: one
+ * persistent launch splits the SMs into up to 8 CTA groups, each running its own SMO loop
+ * and exchange (no communication between problems; more than 8 problems run in successive
+ * launches).  This is the within-GPU form of the paper's task-parallel multiclass training
+ * ("running multiple parallel binary SMOs", Fig. 4).  Device pointers: X[k]
+ * row-major [n[k]][d] float32, y[k] int8, alpha[k] [n[k]] out; b_out[B] and info[B]
+ * (nullable) host out.  Each result equals svm_train_dev on that problem alone. */
+int svm_train_batch_dev(int B, const float* const* X, const int8_t* const* y, const int64_t* n,
+                        int64_t d, const svm_params* p, double* const* alpha, double* b_out,
+                        svm_info* info, void* cuda_stream);
+
 /* Decision values of m test rows (host pointers): dec[i] = sum_s coef_s K(sv_s, x_i) + b
  * with coef_s = alpha_s y_s, summed in ascending s in fp64.  n_sv = 0 gives
  * dec = b. */

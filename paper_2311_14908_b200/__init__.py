@@ -16,7 +16,7 @@ from typing import Optional
 import numpy as np
 
 __all__ = ["LINEAR", "RBF", "PREDICT_EXACT", "PREDICT_TENSOR", "SvmError", "lib", "svm_train", "svm_train_ex", "svm_train_dev",
-           "svm_predict", "svm_predict_dev", "svm_comm_unique_id", "svm_comm_init",
+           "svm_predict", "svm_predict_dev", "svm_train_batch_dev", "svm_comm_unique_id", "svm_comm_init",
            "svm_train_shard", "svm_comm_destroy", "Params", "Info", "version"]
 
 LINEAR = 0
@@ -77,6 +77,7 @@ def lib():
         L.svm_predict_dev.argtypes = [P, P, i64, i64, f64, i32, f64, P, i64, P, P]
         L.svm_predict_ex.argtypes = [P, P, i64, i64, f64, i32, f64, P, i64, P, i32]
         L.svm_predict_dev_ex.argtypes = [P, P, i64, i64, f64, i32, f64, P, i64, P, i32, P]
+        L.svm_train_batch_dev.argtypes = [i32, P, P, P, i64, P, P, P, P, P]
         L.svm_comm_unique_id.argtypes = [P]
         L.svm_comm_init.argtypes = [ctypes.POINTER(ctypes.c_void_p), i32, i32, P, i32]
         L.svm_train_shard.argtypes = [P, P, P, i64, i64, i64, i64, P, P, P, P, P]
@@ -85,7 +86,7 @@ def lib():
         L.svm_last_error.restype = ctypes.c_char_p
         L.svm_version.restype = ctypes.c_char_p
         for name in ("svm_train", "svm_train_ex", "svm_train_dev", "svm_predict", "svm_predict_dev",
-                     "svm_predict_ex", "svm_predict_dev_ex",
+                     "svm_predict_ex", "svm_predict_dev_ex", "svm_train_batch_dev",
                      "svm_comm_unique_id", "svm_comm_init", "svm_train_shard"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
@@ -223,6 +224,29 @@ def svm_predict_dev(X_sv, coef, b: float, kernel: int, gamma: float, X_test, str
                                     ctypes.c_void_p(X_test.data_ptr()), m,
                                     ctypes.c_void_p(dec.data_ptr()), int(mode), _stream_ptr(stream)))
     return dec
+
+
+def svm_train_batch_dev(problems, C: float, kernel: int, gamma: float = 0.0, tol: float = 1e-3,
+                        stream=None, **params):
+    """Independent binary problems solved concurrently (CTA groups of one persistent launch).
+    problems: list of (X [n_k, d] float32 CUDA tensor, y [n_k] int8 CUDA tensor).
+    Returns a list of dict(alpha tensor, b, info)."""
+    import torch
+    B = len(problems)
+    d = problems[0][0].shape[1]
+    alphas = [torch.empty(X.shape[0], dtype=torch.float64, device=X.device) for X, _ in problems]
+    Xp = (ctypes.c_void_p * B)(*[X.data_ptr() for X, _ in problems])
+    yp = (ctypes.c_void_p * B)(*[y.data_ptr() for _, y in problems])
+    ap = (ctypes.c_void_p * B)(*[a.data_ptr() for a in alphas])
+    ns = (ctypes.c_int64 * B)(*[X.shape[0] for X, _ in problems])
+    bs = (ctypes.c_double * B)()
+    infos = (Info * B)()
+    p = make_params(C, kernel, gamma, tol, **params)
+    for X, y in problems:
+        assert X.is_cuda and X.dtype == torch.float32 and X.is_contiguous() and X.shape[1] == d
+        assert y.is_cuda and y.dtype == torch.int8 and y.is_contiguous()
+    _check(lib().svm_train_batch_dev(B, Xp, yp, ns, d, ctypes.byref(p), ap, bs, infos, _stream_ptr(stream)))
+    return [dict(alpha=alphas[k], b=bs[k], info=infos[k].as_dict()) for k in range(B)]
 
 
 def svm_comm_unique_id() -> bytes:

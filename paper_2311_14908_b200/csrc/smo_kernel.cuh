@@ -115,6 +115,10 @@ struct Params {
     const uint32_t* xrbits;        // bit rows [n_global][bin_words] (pivot gather)
     int rec_rows;                  // 1: candidate bit rows travel in the records (bin_words <= 8)
     int nrep;                      // record replicas written (1..NREP); readers pick cta % nrep
+    int independent;               // 1: every rank is its own problem (batched OvO solves): no
+                                   // exchange between ranks, per-rank X / max_iter below
+    const float* xr_rank[MAXR];    // independent mode: row-major X of problem r
+    long long max_iter_rank[MAXR]; // independent mode: max_iter of problem r
     long long timeout_ns;
     int sys_scope;                 // 1 when mailboxes live on other GPUs (system scope)
     unsigned long long* timers;    // optional [8] per-phase cycle totals of CTA 0
@@ -451,6 +455,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
     int final_state = ST_RUNNING;
     Ctl* ctl = P.ctl[rank];
     Mailbox* my_mb = P.mbox[rank];
+    const int xworld = P.independent ? 1 : P.world;         // ranks that exchange records
+    const int xbase = P.independent ? rank : 0;             // first of them
+    const float* xr = P.independent ? P.xr_rank[rank] : P.xr;
+    const long long max_iter = P.independent ? P.max_iter_rank[rank] : P.max_iter;
     long long it = ctl->it;                 // written only at kernel end by CTA 0
     long long seq = ctl->seq;
     const long long it_start = it;
@@ -487,7 +495,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
         // current) and the CTA reduces them lexicographically -- identical in every CTA of
         // every rank.  Chosen by measurement (tools/exchange_bench.cu).
         ++seq;
-        const int g_total = P.world * P.ctas_per_rank;
+        const int g_total = xworld * P.ctas_per_rank;
         const int par = (int)(seq & 1);
         const uint32_t fg = (uint32_t)seq;
         if (is_scalar) {
@@ -527,16 +535,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                         }
                     }
                 }
-                const int gcta = rank * P.ctas_per_rank + cta;
-                for (int q = lane; q < P.world * P.nrep; q += 32) {
-                    Record* rec = mbox_parts(P.mbox[q / P.nrep], q % P.nrep, par, g_total) + gcta;
+                const int gcta = (rank - xbase) * P.ctas_per_rank + cta;
+                for (int q = lane; q < xworld * P.nrep; q += 32) {
+                    Record* rec = mbox_parts(P.mbox[xbase + q / P.nrep], q % P.nrep, par, g_total) + gcta;
                     ll_store(rec, fg, c);
                     if (P.rec_rows) ll_store_rows(rec, fg, ru, rl, P.bin_words);
                 }
                 __syncwarp();
-                if (lane < P.world) {
-                    if (P.sys_scope) red_relaxed_sys(&P.mbox[lane]->count);
-                    else red_relaxed_gpu(&P.mbox[lane]->count);
+                if (lane < xworld) {
+                    if (P.sys_scope) red_relaxed_sys(&P.mbox[xbase + lane]->count);
+                    else red_relaxed_gpu(&P.mbox[xbase + lane]->count);
                 }
             }
             SVM_PHASE(timing, PH_S_PUBLISH);
@@ -635,7 +643,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
         if (sh.timeout) dec = ST_TIMEOUT;
         else if (iu == INT_MAX || il == INT_MAX) dec = ST_CONVERGED;
         else if (fl - fu <= 2.0 * P.tol) dec = ST_CONVERGED;
-        else if (it == P.max_iter) dec = ST_MAXITER;
+        else if (it == max_iter) dec = ST_MAXITER;
         else if (P.iter_limit > 0 && it - it_start == P.iter_limit) dec = ST_LIMIT;
         if (dec != ST_RUNNING) {
             final_state = dec;
@@ -656,8 +664,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                 pw[t] = __ldg(&P.xrbits[(long long)(t < P.bin_words ? iu : il) * P.bin_words + w]);
             }
         } else {
-            const float* xu_g = P.xr + (long long)iu * P.d;
-            const float* xl_g = P.xr + (long long)il * P.d;
+            const float* xu_g = xr + (long long)iu * P.d;
+            const float* xl_g = xr + (long long)il * P.d;
             for (int k0 = 0; k0 < P.d_pad; k0 += NSYNC * 4) {
                 float vu[4], vl[4];
 #pragma unroll

@@ -56,7 +56,11 @@ struct SolveArgs {
     long long timeout_ns = 20ll * 1000 * 1000 * 1000;
     PreLaunchFn pre_launch = nullptr;
     void* user = nullptr;
-    SolveOut out;
+    bool independent = false;                  // batched independent problems (one per rank)
+    const float* xr_rank[svmk::MAXR] = {};
+    long long max_iter_rank[svmk::MAXR] = {};
+    SolveOut out;                              // rank_base's result
+    SolveOut out_rank[svmk::MAXR];             // every served rank (independent mode)
 };
 
 int check_params(long long n, long long d, const svm_params* p, svm_params* q);

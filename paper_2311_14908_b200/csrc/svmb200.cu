@@ -262,7 +262,7 @@ int solve(SolveArgs& a) {
     Plan pl;
     int rc = SVM_OK;
     bool binary = false;
-    if (getenv("SVMB200_NO_BINARY") == nullptr && a.d <= 1024) {
+    if (!a.independent && getenv("SVMB200_NO_BINARY") == nullptr && a.d <= 1024) {
         unsigned long long* dc = nullptr;
         CKR(cudaMallocAsync(&dc, 8, a.stream));
         CKR(cudaMemsetAsync(dc, 0, 8, a.stream));
@@ -314,6 +314,11 @@ int solve(SolveArgs& a) {
     P.n_global = a.n_global; P.xr = a.xr; P.cta_stride = pl.cta_stride;
     P.check_interval = p.check_interval; P.state_cap = pl.state_cap; P.resident = pl.resident ? 1 : 0;
     P.bin_words = pl.bin_words;
+    P.independent = a.independent ? 1 : 0;
+    for (int r = 0; r < world; ++r) {
+        P.xr_rank[r] = a.independent ? a.xr_rank[r] : a.xr;
+        P.max_iter_rank[r] = a.independent ? a.max_iter_rank[r] : p.max_iter;
+    }
     // Candidate bit rows inside the records (saves the pivot round trip) measured slower on
     // W2 (larger records, row extraction on the publish path): off unless requested.
     P.rec_rows = 0;
@@ -393,15 +398,21 @@ int solve(SolveArgs& a) {
     CKR(cudaEventRecord(e0, st));
     Ctl hc;
     memset(&hc, 0, sizeof(hc));
+    Ctl hcr[MAXR];
     long long launches = 0;
     for (;;) {
         void* args[] = {(void*)&P};
         cudaError_t e = cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(NTHREADS), args, pl.smem, st);
         if (e != cudaSuccess) { release(); return fail(SVM_ECUDA, std::string("cooperative launch: ") + cudaGetErrorString(e)); }
         ++launches;
-        CKR(cudaMemcpyAsync(&hc, P.ctl[a.rank_base], sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+        bool again = false;
+        for (int r = a.rank_base; r < a.rank_base + a.nranks_here; ++r) {
+            CKR(cudaMemcpyAsync(&hcr[r], P.ctl[r], sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+        }
         CKR(cudaStreamSynchronize(st));
-        if (hc.state != ST_LIMIT) break;
+        for (int r = a.rank_base; r < a.rank_base + a.nranks_here; ++r) again = again || hcr[r].state == ST_LIMIT;
+        hc = hcr[a.rank_base];
+        if (!again) break;
     }
     CKR(cudaEventRecord(e1, st));
     CKR(cudaEventSynchronize(e1));
@@ -409,6 +420,11 @@ int solve(SolveArgs& a) {
     cudaEventElapsedTime(&ms, e0, e1);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    for (int r = a.rank_base; r < a.rank_base + a.nranks_here; ++r) {
+        SolveOut& o = a.out_rank[r];
+        o.seconds_solve = ms * 1e-3; o.launches = launches; o.iterations = hcr[r].it;
+        o.state = hcr[r].state; o.b_up = hcr[r].b_up; o.b_low = hcr[r].b_low;
+    }
     a.out.seconds_solve = ms * 1e-3;
     a.out.launches = launches;
     a.out.iterations = hc.it;
@@ -439,9 +455,11 @@ int solve(SolveArgs& a) {
     release();
     CKR(cudaStreamSynchronize(st));
     if (progress_h) cudaFreeHost(progress_h);
-    if (hc.state == ST_TIMEOUT) return fail(SVM_ETIMEOUT, "device wait for the candidate exchange timed out");
-    if (hc.state != ST_CONVERGED && hc.state != ST_MAXITER)
-        return fail(SVM_ECUDA, "solver ended in state " + std::to_string(hc.state));
+    for (int r = a.rank_base; r < a.rank_base + a.nranks_here; ++r) {
+        if (hcr[r].state == ST_TIMEOUT) return fail(SVM_ETIMEOUT, "device wait for the candidate exchange timed out");
+        if (hcr[r].state != ST_CONVERGED && hcr[r].state != ST_MAXITER)
+            return fail(SVM_ECUDA, "solver ended in state " + std::to_string(hcr[r].state));
+    }
     return SVM_OK;
 }
 
@@ -619,6 +637,63 @@ extern "C" int svm_train_dev(const float* X, const int8_t* y, int64_t n, int64_t
         fill_info(info, o, p, ha.data(), hf.data(), hy.data(), n, now_s() - t0);
     }
     CKR(cudaFreeAsync(f_dev, st));
+    return SVM_OK;
+}
+
+extern "C" int svm_train_batch_dev(int B, const float* const* X, const int8_t* const* y,
+                                   const int64_t* n, int64_t d, const svm_params* p_in,
+                                   double* const* alpha, double* b_out, svm_info* info,
+                                   void* cuda_stream) {
+    const double t0 = now_s();
+    if (B < 1 || !X || !y || !n || !alpha || !b_out) return fail(SVM_EINVAL, "null pointer or B < 1");
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    int n_sm = 0, max_smem = 0;
+    int rc = device_limits(&n_sm, &max_smem);
+    if (rc) return rc;
+    for (int b0 = 0; b0 < B; b0 += MAXR) {
+        const int nb = (B - b0) < MAXR ? (B - b0) : MAXR;
+        SolveArgs a;
+        svm_params p;
+        long long n_max = 0;
+        for (int k = 0; k < nb; ++k) {
+            if (!X[b0 + k] || !y[b0 + k] || !alpha[b0 + k]) return fail(SVM_EINVAL, "null problem pointer");
+            if ((rc = check_params(n[b0 + k], d, p_in, &p))) return rc;
+            if ((rc = validate_device(X[b0 + k], y[b0 + k], n[b0 + k], d, st, nullptr))) return rc;
+            a.max_iter_rank[k] = p.max_iter;
+            if (p_in->max_iter <= 0) a.max_iter_rank[k] = (10 * n[b0 + k] > 10000) ? 10 * n[b0 + k] : 10000;
+            n_max = n[b0 + k] > n_max ? n[b0 + k] : n_max;
+        }
+        a.p = p;
+        a.n_global = n_max; a.d = d; a.xr = X[b0];
+        a.world = nb; a.rank_base = 0; a.nranks_here = nb;
+        int ctas = p.ctas > 0 ? p.ctas : n_sm;
+        if (ctas > n_sm) ctas = n_sm;
+        a.ctas_per_rank = ctas / nb;
+        a.n_sm = n_sm; a.max_smem = max_smem;
+        a.independent = true;
+        for (int k = 0; k < nb; ++k) {
+            a.row_off[k] = 0; a.n_rows[k] = n[b0 + k];
+            a.x_rank[k] = X[b0 + k]; a.y_rank[k] = y[b0 + k]; a.alpha_out[k] = alpha[b0 + k];
+            a.xr_rank[k] = X[b0 + k];
+        }
+        a.n_rows_max = n_max;
+        a.mbox_local_alloc = true;
+        a.stream = st;
+        a.f_out = nullptr;
+        if ((rc = solve(a))) return rc;
+        for (int k = 0; k < nb; ++k) {
+            const SolveOut& o = a.out_rank[k];
+            b_out[b0 + k] = -(o.b_up + o.b_low) / 2.0;
+            if (info) {
+                svm_info& in = info[b0 + k];
+                memset(&in, 0, sizeof(in));
+                in.iterations = o.iterations; in.converged = o.state == ST_CONVERGED;
+                in.b_up = o.b_up; in.b_low = o.b_low; in.gap = o.b_low - o.b_up;
+                in.seconds_solve = o.seconds_solve; in.launches = o.launches;
+                in.seconds_total = now_s() - t0;
+            }
+        }
+    }
     return SVM_OK;
 }
 

@@ -32,6 +32,14 @@ def _worker(rank, world, port, n, out_dir):
     local = torch.arange(lo, hi, dtype=torch.float64) * 0.5
     full = gather_rows(local, blocks, dev)
     t = max_over_ranks(1.0 + rank, dev)
+    # OvO: each rank trains its share of the pairs; gather_models assembles all of them
+    from paper_2311_14908_b200.multiclass import OvOModel, enumerate_pairs, gather_models
+    mdl = OvOModel(4, 1, 0.5)
+    for k, pair in enumerate(enumerate_pairs(4)):
+        if k % world == rank:
+            mdl.models[pair] = dict(b=float(k), coef=np.arange(k, dtype=np.float64))
+    gather_models(mdl)
+    np.save(os.path.join(out_dir, f"m{rank}.npy"), np.array([mdl.models[p]["b"] for p in enumerate_pairs(4)]))
     np.savez(os.path.join(out_dir, f"r{rank}.npz"), uid=np.frombuffer(got, np.uint8), full=full.numpy(),
              t=t, lo=lo, hi=hi)
     dist.destroy_process_group()
@@ -48,3 +56,5 @@ def test_two_rank_host_path(tmp_path, n):
         np.testing.assert_array_equal(r[k]["full"], np.arange(n) * 0.5)
         assert float(r[k]["t"]) == 2.0
     assert int(r[0]["lo"]) == 0 and int(r[1]["hi"]) == n and int(r[0]["hi"]) == int(r[1]["lo"])
+    for k in range(world):
+        assert np.load(os.path.join(tmp_path, f"m{k}.npy")).tolist() == [float(i) for i in range(6)]
