@@ -59,7 +59,7 @@ enum { FL_POS = 1, FL_UP = 2, FL_LOW = 4 };
 // needed on the writer's side.  Payload words: 0-1 f_up, 2-3 f_low, 4-5 a_up, 6-7 a_low
 // (lo, hi halves), 8 i_up, 9 i_low (global row, -1 = empty set), 10 y_up | y_low << 16.
 constexpr int REC_ROW_WORDS = 8;   // binary rows up to 256 features travel in the record
-constexpr int NREP = 4;            // replicas of every record (spreads the all-to-all reads)
+constexpr int NREP = 8;            // max replicas of every record (spreads the all-to-all reads)
 struct __align__(16) Record {
     unsigned long long w[12 + 2 * REC_ROW_WORDS];   // base words, then the two candidate bit rows
 };
@@ -115,6 +115,7 @@ struct Params {
     const uint32_t* xrbits;        // bit rows [n_global][bin_words] (pivot gather)
     int rec_rows;                  // 1: candidate bit rows travel in the records (bin_words <= 8)
     int nrep;                      // record replicas written (1..NREP); readers pick cta % nrep
+    int direct_poll_ns;            // >= 0: skip the counter, poll the records directly with this backoff
     int independent;               // 1: every rank is its own problem (batched OvO solves): no
                                    // exchange between ranks, per-rank X / max_iter below
     const float* xr_rank[MAXR];    // independent mode: row-major X of problem r
@@ -542,13 +543,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                     if (P.rec_rows) ll_store_rows(rec, fg, ru, rl, P.bin_words);
                 }
                 __syncwarp();
-                if (lane < xworld) {
+                if (lane < xworld && P.direct_poll_ns < 0) {
                     if (P.sys_scope) red_relaxed_sys(&P.mbox[xbase + lane]->count);
                     else red_relaxed_gpu(&P.mbox[xbase + lane]->count);
                 }
             }
             SVM_PHASE(timing, PH_S_PUBLISH);
-            if (lane == 0) {
+            if (lane == 0 && P.direct_poll_ns < 0) {
                 const unsigned long long target = (unsigned long long)seq * g_total;
                 long long t0 = 0;
                 unsigned int spins = 0;
@@ -562,7 +563,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
             }
             SVM_PHASE(timing, PH_S_POLL);
         }
-        named_sync(BAR_E);                  // all records have (nearly) landed
+        named_sync(BAR_E);                  // records published (direct mode) / landed (counter mode)
         uint32_t myrow_u[REC_ROW_WORDS], myrow_l[REC_ROW_WORDS];  // bit rows of my best candidates
         int my_iu = INT_MAX, my_il = INT_MAX;
         {
@@ -596,6 +597,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                             }
                         }
                         if (ok) break;
+                        if (P.direct_poll_ns > 0) __nanosleep(P.direct_poll_ns);
                         if ((++spins & 255u) == 0) {
                             const long long now = globaltimer();
                             if (t0 == 0) t0 = now;

@@ -324,7 +324,10 @@ int solve(SolveArgs& a) {
     P.rec_rows = 0;
     if (const char* e = getenv("SVMB200_RECROWS"))
         P.rec_rows = (pl.bin_words > 0 && pl.bin_words <= REC_ROW_WORDS && atoi(e) != 0) ? 1 : 0;
-    P.nrep = NREP;                                         // 4 replicas: measured best on W2
+    P.nrep = 4;                                            // 4 replicas: measured best on W2
+    if (const char* e = getenv("SVMB200_NREP")) { const int v = atoi(e); if (v >= 1 && v <= NREP) P.nrep = v; }
+    P.direct_poll_ns = 0;                                  // direct LL polling: measured best on W2
+    if (const char* e = getenv("SVMB200_DIRECTPOLL")) P.direct_poll_ns = atoi(e);
     if (const char* e = getenv("SVMB200_NREP")) { const int v = atoi(e); if (v >= 1 && v <= NREP) P.nrep = v; }
     P.timeout_ns = a.timeout_ns;
     P.sys_scope = a.mbox_local_alloc ? 0 : 1;
