@@ -214,6 +214,7 @@ def run_ours(args):
            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     infos = []
     nsv = 0
+    launches0 = S.kernel_launches()
     with Clocks(local) as clk:
         barrier()
         for k in range(args.steps):
@@ -226,6 +227,7 @@ def run_ours(args):
             e2.record(stream)
             infos.append(r["info"])
         barrier()
+    our_launches = S.kernel_launches() - launches0
     t_train = [a.elapsed_time(b) * 1e-3 for a, b, _ in ev]
     t_step = [a.elapsed_time(c) * 1e-3 for a, _, c in ev]
     t_solve = [i["seconds_solve"] for i in infos]
@@ -302,9 +304,6 @@ def run_ours(args):
                    "sample": f"first {k_it} SMO iterations of {w.name} (n={n}) on {thr} host threads "
                              f"({ips:.1f} iters/s); time-to-converge projected to the {iters} iterations "
                              f"of the identical trajectory"}
-        # validate + build_xblk + init_state + persistent launches; predict: exact 1 kernel,
-        # tensor 4 (2 packs, coef pad, tcgen05 kernel)
-        per_launch_launches = 3 + launches + (4 if args.predict_mode == 1 else 1)
         line = {
             "metric": METRIC, "value": train_s, "unit": "s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
@@ -324,7 +323,7 @@ def run_ours(args):
                          "kernel": "smo_persistent", "bytes_per_iter": bytes_iter},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": per_launch_launches * args.steps,
+            "gpu_launches": our_launches,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

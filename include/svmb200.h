@@ -162,6 +162,10 @@ int svm_train_shard(void* comm, const float* X_local, const int8_t* y_local, int
                     double* alpha_local, double* b, svm_info* info, void* cuda_stream);
 void svm_comm_destroy(void* comm);
 
+/* Number of CUDA kernels this library has launched from the calling thread so far
+ * (validation, staging, the persistent solver launches, prediction). */
+int64_t svm_kernel_launches(void);
+
 /* Message for the last non-OK status returned on this thread ("" if none). */
 const char* svm_last_error(void);
 

@@ -84,6 +84,7 @@ def lib():
         L.svm_comm_destroy.argtypes = [P]
         L.svm_comm_destroy.restype = None
         L.svm_last_error.restype = ctypes.c_char_p
+        L.svm_kernel_launches.restype = ctypes.c_int64
         L.svm_version.restype = ctypes.c_char_p
         for name in ("svm_train", "svm_train_ex", "svm_train_dev", "svm_predict", "svm_predict_dev",
                      "svm_predict_ex", "svm_predict_dev_ex", "svm_train_batch_dev",
@@ -91,6 +92,11 @@ def lib():
             getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib
+
+
+def kernel_launches() -> int:
+    """CUDA kernels the library launched from this thread so far."""
+    return int(lib().svm_kernel_launches())
 
 
 def version() -> str:

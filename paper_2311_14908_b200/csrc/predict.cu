@@ -97,11 +97,13 @@ int predict_device_tc(const float* X_sv, const double* coef, long long n_sv, lon
     k_pack_3xtf32<<<1184, 256, 0, st>>>(X_test, m, (int)d, k_chunks, m_pad, pa, qt);
     k_pack_3xtf32<<<1184, 256, 0, st>>>(X_sv, n_sv, (int)d, k_chunks, n_pad, pb, qs);
     k_pad_coef<<<256, 256, 0, st>>>(coef, n_sv, n_pad, cf);
+    counted(3);
     const size_t smem = (size_t)STAGES * STAGE_BYTES;
     auto fn = kernel == SVM_RBF ? k_predict_tc<1> : k_predict_tc<0>;
     CKR(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     fn<<<(unsigned)(m_pad / BM), NTHREADS, smem, st>>>(pa, pb, qt, qs, cf, k_chunks, (int)(n_pad / BN), m, b,
                                                         gamma, dec);
+    counted();
     CKR(cudaGetLastError());
     cudaFreeAsync(pa, st); cudaFreeAsync(pb, st); cudaFreeAsync(qt, st); cudaFreeAsync(qs, st); cudaFreeAsync(cf, st);
     return SVM_OK;
@@ -118,6 +120,7 @@ int predict_device(const float* X_sv, const double* coef, long long n_sv, long l
         k_predict_exact<1><<<(unsigned)grid, TI, 0, st>>>(X_sv, coef, n_sv, (int)d, b, gamma, X_test, m, dec);
     else
         k_predict_exact<0><<<(unsigned)grid, TI, 0, st>>>(X_sv, coef, n_sv, (int)d, b, gamma, X_test, m, dec);
+    counted();
     CKR(cudaGetLastError());
     return SVM_OK;
 }

@@ -12,6 +12,9 @@ namespace svmint {
 
 extern thread_local std::string g_err;
 int fail(int code, const std::string& msg);
+// kernels this library launched from the calling thread (svm_kernel_launches)
+extern thread_local long long g_launches;
+inline void counted(long long k = 1) { g_launches += k; }
 
 #define CKR(x)                                                                          \
     do {                                                                                \

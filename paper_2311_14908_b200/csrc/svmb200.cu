@@ -26,6 +26,7 @@ using namespace svmk;
 namespace svmint {
 
 thread_local std::string g_err;
+thread_local long long g_launches = 0;
 
 int fail(int code, const std::string& msg) {
     g_err = msg;
@@ -131,6 +132,7 @@ int validate_device(const float* X, const int8_t* y, long long n, long long d, c
     CKR(cudaMallocAsync(&dc, 4 * sizeof(unsigned long long), st));
     CKR(cudaMemsetAsync(dc, 0, 4 * sizeof(unsigned long long), st));
     k_validate<<<1024, 256, 0, st>>>(X, n * d, y, n, dc);
+    counted();
     unsigned long long hc[4];
     CKR(cudaMemcpyAsync(hc, dc, sizeof(hc), cudaMemcpyDeviceToHost, st));
     CKR(cudaFreeAsync(dc, st));
@@ -267,6 +269,7 @@ int solve(SolveArgs& a) {
         CKR(cudaMallocAsync(&dc, 8, a.stream));
         CKR(cudaMemsetAsync(dc, 0, 8, a.stream));
         k_count_nonbinary<<<1024, 256, 0, a.stream>>>(a.xr, a.n_global * a.d, dc);
+        counted();
         unsigned long long nb = 1;
         CKR(cudaMemcpyAsync(&nb, dc, 8, cudaMemcpyDeviceToHost, a.stream));
         CKR(cudaFreeAsync(dc, a.stream));
@@ -326,7 +329,11 @@ int solve(SolveArgs& a) {
         P.rec_rows = (pl.bin_words > 0 && pl.bin_words <= REC_ROW_WORDS && atoi(e) != 0) ? 1 : 0;
     P.nrep = 4;                                            // 4 replicas: measured best on W2
     if (const char* e = getenv("SVMB200_NREP")) { const int v = atoi(e); if (v >= 1 && v <= NREP) P.nrep = v; }
-    P.direct_poll_ns = 0;                                  // direct LL polling: measured best on W2
+    // Record reads: direct LL polling right after the publish barrier is fastest when the
+    // solve is latency-bound (X resident in shared memory: W2 4.8 vs 5.5 us/iteration);
+    // when X streams from HBM the CTAs arrive spread out and 288 pollers per CTA slow the
+    // stragglers (W3/W4/W5 +10-15%), so there one thread polls the arrival counter first.
+    P.direct_poll_ns = (pl.resident && !a.independent && a.mbox_local_alloc) ? 0 : -1;
     if (const char* e = getenv("SVMB200_DIRECTPOLL")) P.direct_poll_ns = atoi(e);
     if (const char* e = getenv("SVMB200_NREP")) { const int v = atoi(e); if (v >= 1 && v <= NREP) P.nrep = v; }
     P.timeout_ns = a.timeout_ns;
@@ -350,11 +357,14 @@ int solve(SolveArgs& a) {
                 uint32_t* xrb;
                 if ((rc = dalloc((void**)&xrb, (size_t)a.n_global * pl.bin_words * 4))) { release(); return rc; }
                 k_pack_bits<<<1024, 256, 0, st>>>(a.xr, a.n_global, (int)a.d, pl.bin_words, xrb);
+                counted();
                 P.xrbits = xrb;
             }
+            counted(2);   // build + init_state below
             k_build_xbits<<<bg, 256, 0, st>>>(P.xrbits + a.row_off[r] * pl.bin_words, nr, pl.bin_words, pl.G,
                                                pl.rt, pl.cta_stride, reinterpret_cast<uint32_t*>(xb));
         } else {
+            counted(2);   // build + init_state below
             k_build_xblk<<<bg, 256, 0, st>>>(a.x_rank[r], nr, (int)a.d, pl.d_pad, pl.G, pl.rt, pl.cta_stride, xb);
         }
         k_init_state<<<256, 256, 0, st>>>(a.y_rank[r], nr, p.C, a.alpha0 ? a.alpha0 + a.row_off[r] : nullptr,
@@ -408,6 +418,7 @@ int solve(SolveArgs& a) {
         cudaError_t e = cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(NTHREADS), args, pl.smem, st);
         if (e != cudaSuccess) { release(); return fail(SVM_ECUDA, std::string("cooperative launch: ") + cudaGetErrorString(e)); }
         ++launches;
+        counted();
         bool again = false;
         for (int r = a.rank_base; r < a.rank_base + a.nranks_here; ++r) {
             CKR(cudaMemcpyAsync(&hcr[r], P.ctl[r], sizeof(Ctl), cudaMemcpyDeviceToHost, st));
@@ -767,4 +778,5 @@ extern "C" int svm_predict(const float* X_sv, const double* coef, int64_t n_sv, 
 }
 
 extern "C" const char* svm_last_error(void) { return g_err.c_str(); }
+extern "C" int64_t svm_kernel_launches(void) { return g_launches; }
 extern "C" const char* svm_version(void) { return "svmb200 0.1 sm_100a"; }
