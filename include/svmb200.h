@@ -73,6 +73,11 @@ typedef struct {
                                (test hook for the row-sharded path; results are identical) */
     int32_t ctas;           /* <= 0 -> one CTA per SM; else the CTA count (test hook) */
     int64_t iters_per_launch; /* <= 0 -> unlimited: the whole solve is one persistent launch */
+    int32_t gram;           /* full-Gram path: 1 force, -1 never, 0 auto (one rank,
+                               20,000 <= n, 8 n^2 bytes within a third of free HBM, X not
+                               shared-memory resident).  K is precomputed once with the same
+                               arithmetic (R13/R14), so results are identical either way. */
+    int32_t pad_;
 } svm_params;
 
 typedef struct {

@@ -116,6 +116,8 @@ struct Params {
     int rec_rows;                  // 1: candidate bit rows travel in the records (bin_words <= 8)
     int nrep;                      // record replicas written (1..NREP); readers pick cta % nrep
     int direct_poll_ns;            // >= 0: skip the counter, poll the records directly with this backoff
+    const double* gram;            // full-Gram path (a9): K [n_global][n_global], rows read per
+                                   // iteration instead of streaming X (one rank only)
     int independent;               // 1: every rank is its own problem (batched OvO solves): no
                                    // exchange between ranks, per-rank X / max_iter below
     const float* xr_rank[MAXR];    // independent mode: row-major X of problem r
@@ -411,6 +413,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
 
     // ============================================================ producer warp
     if (warp == PRODUCER_WARP) {
+        if (P.gram) {
+            if (lane == 0) { sh.issued = 0; __threadfence_block(); sh.producer_done = 1; }
+            return;
+        }
         if (P.resident) {
             if (lane == 0 && n_tiles > 0) {
                 const int rp = (R + 3) & ~3;
@@ -466,7 +472,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
     unsigned int cslot = 0, cpar = 0, consumed = 0;
     const double INF = __longlong_as_double(0x7ff0000000000000ll);
 
-    if (P.resident && n_tiles > 0 && !is_scalar) mbar_wait(&full[0], 0);
+    if (P.resident && !P.gram && n_tiles > 0 && !is_scalar) mbar_wait(&full[0], 0);
     // ---- initial selection from the current state (no update)
     if (!is_scalar) {
         double fu = INF, fl = -INF;
@@ -653,7 +659,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
             break;
         }
         // ---- pivot rows x_up, x_low (fp64 in shared memory, or bit rows), all threads
-        if (P.rec_rows) {
+        if (P.gram) {
+            // rows of K are read directly; no pivot rows needed
+        } else if (P.rec_rows) {
             uint32_t* pw = reinterpret_cast<uint32_t*>(piv);
             if (my_iu == iu)
                 for (int h = 0; h < P.bin_words; ++h) pw[h] = myrow_u[h];
@@ -690,7 +698,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
             // ---- pair update (a2): eta, clipped step, snapped alphas (lane 0)
             if (lane == 0) {
                 double Kuu, Kll, Kul;
-                if (P.bin_words) {
+                if (P.gram) {
+                    const long long n = P.n_global;
+                    Kuu = __ldg(&P.gram[(long long)u * n + u]);
+                    Kll = __ldg(&P.gram[(long long)l * n + l]);
+                    Kul = __ldg(&P.gram[(long long)u * n + l]);
+                } else if (P.bin_words) {
                     const uint32_t* pw = reinterpret_cast<const uint32_t*>(piv);
                     int cuu = 0, cll = 0, cul = 0, cx = 0;
                     for (int w = 0; w < P.bin_words; ++w) {
@@ -766,7 +779,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
             double du[RPT], dl[RPT];
 #pragma unroll
             for (int q = 0; q < RPT; ++q) { du[q] = 0.0; dl[q] = 0.0; }
-            if (P.bin_words) {
+            if (P.gram) {
+                if (active) {
+                    // rows u and l of the precomputed K (fp64, already the kernel values)
+                    const double* ku_row = P.gram + (long long)u * P.n_global + gbase + tile * P.rt + t * RPT;
+                    const double* kl_row = P.gram + (long long)l * P.n_global + gbase + tile * P.rt + t * RPT;
+#pragma unroll
+                    for (int q = 0; q < RPT; ++q) {
+                        if (tile * P.rt + t * RPT + q < R) { du[q] = __ldg(&ku_row[q]); dl[q] = __ldg(&kl_row[q]); }
+                    }
+                }
+            } else if (P.bin_words) {
                 if (active) {
                     // bit rows resident in shared memory: [tile][word][row], popcounts
                     const uint32_t* xb = reinterpret_cast<const uint32_t*>(ring) + (size_t)tile * P.bin_words * P.rt + t;
@@ -780,7 +803,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                     du[0] = (double)cu_; dl[0] = (double)cl_;
                 }
             }
-            for (int ch = 0; ch < (P.bin_words ? 0 : P.n_chunks); ++ch) {
+            for (int ch = 0; ch < ((P.bin_words || P.gram) ? 0 : P.n_chunks); ++ch) {
                 if (!P.resident) mbar_wait(&full[cslot], cpar);
                 const float* st = P.resident ? ring + (size_t)ch * P.kc * rp : ring + (size_t)cslot * stage_floats;
                 const int k0 = ch * P.kc;
@@ -859,7 +882,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                     if (j < R) {
                         const long long jg = gbase + j;
                         double ku, kl;
-                        if (KERNEL == 1 && P.bin_words) {
+                        if (P.gram) {
+                            ku = du[q]; kl = dl[q];
+                        } else if (KERNEL == 1 && P.bin_words) {
                             ku = (jg == u) ? 1.0 : ktab[(int)du[q]];
                             kl = (jg == l) ? 1.0 : ktab[(int)dl[q]];
                         } else if (KERNEL == 1) {

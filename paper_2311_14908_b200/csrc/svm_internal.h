@@ -29,6 +29,7 @@ struct SolveOut {
     double b_up = 0, b_low = 0;
     double seconds_solve = 0;
     long long launches = 0;
+    bool gram = false;
 };
 
 struct SolveArgs;
@@ -71,6 +72,10 @@ int validate_device(const float* X, const int8_t* y, long long n, long long d, c
                     int* n_pos);
 int device_limits(int* n_sm, int* max_smem);
 int solve(SolveArgs& a);
+
+// gram.cu: K[i][j] for all i, j < n (fp64, row-major), same arithmetic as the row pass
+int gram_device(const float* X, long long n, long long d, int kernel, double gamma, double* K,
+                cudaStream_t st);
 
 // predict.cu
 int predict_device(const float* X_sv, const double* coef, long long n_sv, long long d, double b,

@@ -175,8 +175,24 @@ struct Plan {
     size_t smem = 0;
 };
 
-int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl, bool binary = false) {
+int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl, bool binary = false,
+              bool gram = false) {
     pl.G = G;
+    if (gram) {
+        // rows of K are read from HBM: state and control only, no X stages
+        pl.state_cap = (int)((n_r_max + G - 1) / G);
+        if (pl.state_cap < 1) pl.state_cap = 1;
+        pl.rpt = pl.state_cap <= NT ? 1 : (pl.state_cap <= 2 * NT ? 2 : 4);
+        pl.rt = NT * pl.rpt; pl.kc = 1; pl.d_pad = 1; pl.n_chunks = 0;
+        pl.cta_stride = 0;
+        pl.alpha_smem = pl.state_cap <= 2048;
+        size_t fixed = (sizeof(Shared) + 127) & ~size_t(127);
+        fixed += 2 * (size_t)8 * 8 + (size_t)pl.state_cap * (pl.alpha_smem ? 17 : 9);
+        fixed = (fixed + 127) & ~size_t(127);
+        if (fixed > (size_t)max_smem) return fail(SVM_ENOMEM, "shard too large for the shared-memory state");
+        pl.stages = 1; pl.resident = false; pl.smem = fixed;
+        return SVM_OK;
+    }
     if (binary) {
         // bit rows, resident in shared memory, one row per consumer thread
         pl.state_cap = (int)((n_r_max + G - 1) / G);
@@ -209,6 +225,10 @@ int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl, bool bina
     }
     pl.rt = NT * pl.rpt;
     pl.kc = 8192 / pl.rt;                                  // 32 KB stages
+    if (const char* e = getenv("SVMB200_KC")) {           // tuning override (features per stage)
+        const int v = atoi(e);
+        if (v >= 1 && v <= 64) pl.kc = v;
+    }
     pl.d_pad = (d + pl.kc - 1) / pl.kc * pl.kc;
     pl.n_chunks = pl.d_pad / pl.kc;
     const int n_tiles = (pl.state_cap + pl.rt - 1) / pl.rt;
@@ -278,7 +298,38 @@ int solve(SolveArgs& a) {
     }
     if (binary && make_plan(a.n_rows_max, (int)a.d, a.ctas_per_rank, a.max_smem, pl, true) != SVM_OK)
         binary = false;
-    if (!binary) {
+    // full-Gram path (a9): one rank only; forced, or auto for mid-size problems
+    double* gram = nullptr;
+    cudaEvent_t ev_gram = nullptr;
+    const bool single = (a.world == 1 && a.nranks_here == 1 && !a.independent);
+    bool want_gram = single && a.p.gram == 1;
+    if (single && a.p.gram == 0 && !binary && a.n_global >= 20000) {
+        size_t fr = 0, tot = 0;
+        if (cudaMemGetInfo(&fr, &tot) == cudaSuccess)
+            want_gram = (double)a.n_global * a.n_global * 8.0 <= (double)fr / 3.0;
+    }
+    if (a.p.gram == 1 && !single) return fail(SVM_EINVAL, "the Gram path needs a single rank");
+    if (want_gram) {
+        if (cudaMallocAsync(&gram, (size_t)a.n_global * a.n_global * 8, a.stream) != cudaSuccess) {
+            cudaGetLastError();
+            gram = nullptr;
+            if (a.p.gram == 1) return fail(SVM_ENOMEM, "Gram matrix allocation failed");
+        }
+    }
+    if (gram) {
+        binary = false;
+        pl = Plan();
+        if ((rc = make_plan(a.n_rows_max, (int)a.d, a.ctas_per_rank, a.max_smem, pl, false, true))) {
+            cudaFreeAsync(gram, a.stream);
+            return rc;
+        }
+        CKR(cudaEventCreate(&ev_gram));
+        CKR(cudaEventRecord(ev_gram, a.stream));          // the solve time includes building K
+        if ((rc = gram_device(a.xr, a.n_global, a.d, p.kernel, p.gamma, gram, a.stream))) {
+            cudaFreeAsync(gram, a.stream);
+            return rc;
+        }
+    } else if (!binary) {
         pl = Plan();
         rc = make_plan(a.n_rows_max, (int)a.d, a.ctas_per_rank, a.max_smem, pl);
         if (rc) return rc;
@@ -297,6 +348,7 @@ int solve(SolveArgs& a) {
 
     // ---- per-rank device state (a1)
     std::vector<void*> owned;
+    if (gram) owned.push_back(gram);                       // freed with the other scratch
     auto dalloc = [&](void** ptr, size_t bytes) -> int {
         cudaError_t e = cudaMallocAsync(ptr, bytes, st);
         if (e != cudaSuccess) return fail(SVM_ENOMEM, std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
@@ -317,6 +369,7 @@ int solve(SolveArgs& a) {
     P.n_global = a.n_global; P.xr = a.xr; P.cta_stride = pl.cta_stride;
     P.check_interval = p.check_interval; P.state_cap = pl.state_cap; P.resident = pl.resident ? 1 : 0;
     P.bin_words = pl.bin_words;
+    P.gram = gram;
     P.independent = a.independent ? 1 : 0;
     for (int r = 0; r < world; ++r) {
         P.xr_rank[r] = a.independent ? a.xr_rank[r] : a.xr;
@@ -352,7 +405,9 @@ int solve(SolveArgs& a) {
         CKR(cudaMemsetAsync(xb, 0, (size_t)pl.cta_stride * pl.G * 4, st));
         CKR(cudaMemsetAsync(ctl, 0, sizeof(Ctl), st));
         dim3 bg(256, pl.G);
-        if (pl.bin_words) {
+        if (gram) {
+            counted(1);   // init_state below
+        } else if (pl.bin_words) {
             if (!P.xrbits) {
                 uint32_t* xrb;
                 if ((rc = dalloc((void**)&xrb, (size_t)a.n_global * pl.bin_words * 4))) { release(); return rc; }
@@ -409,6 +464,7 @@ int solve(SolveArgs& a) {
     CKR(cudaEventCreate(&e0));
     CKR(cudaEventCreate(&e1));
     CKR(cudaEventRecord(e0, st));
+    if (ev_gram) { cudaEventDestroy(e0); e0 = ev_gram; }
     Ctl hc;
     memset(&hc, 0, sizeof(hc));
     Ctl hcr[MAXR];
@@ -469,6 +525,7 @@ int solve(SolveArgs& a) {
     release();
     CKR(cudaStreamSynchronize(st));
     if (progress_h) cudaFreeHost(progress_h);
+    a.out.gram = gram != nullptr;
     for (int r = a.rank_base; r < a.rank_base + a.nranks_here; ++r) {
         if (hcr[r].state == ST_TIMEOUT) return fail(SVM_ETIMEOUT, "device wait for the candidate exchange timed out");
         if (hcr[r].state != ST_CONVERGED && hcr[r].state != ST_MAXITER)

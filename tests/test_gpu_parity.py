@@ -334,3 +334,27 @@ def test_train_shard_single_rank(S):
     np.testing.assert_array_equal(r["alpha"].cpu().numpy(), r_or.alpha)
     assert r["b"] == r_or.b
     assert r["info"]["dual_objective"] == pytest.approx(O.dual_objective_from_f(r_or.alpha, y, r_or.f), rel=1e-12)
+
+
+@pytest.mark.parametrize("name,n,kern", [("W3", 1500, None), ("W5", 2500, None), ("W1", 200, None),
+                                         ("W4", 3000, None)])
+def test_gram_path_parity(S, name, n, kern):
+    """Full-Gram path: K precomputed once with the row pass's arithmetic,
+    then rows of K read per iteration -- identical trajectory and alpha."""
+    w = W.get(name)
+    X, y = w.train(n)
+    r_g, r_or = _run_pair(S, w, X, y, gram=1)
+    _assert_exact(r_g, r_or)
+    r_s = S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol, want_f=True, gram=-1)
+    np.testing.assert_array_equal(r_s["alpha"], r_g["alpha"])
+
+
+def test_full_size_w3_streaming_prefix(S):
+    """W3 at full size uses the Gram path by default; this keeps the streaming path
+    covered at full size too."""
+    w = W.get("W3")
+    X, y = w.train()
+    k = 40
+    r_or = O.train(X, y, w.C, w.kernel, w.gamma, w.tol, max_iter=k, trace_cap=k)
+    r_g = S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol, max_iter=k, want_f=True, trace_cap=k, gram=-1)
+    _assert_exact(r_g, r_or)
