@@ -73,11 +73,16 @@ typedef struct {
                                (test hook for the row-sharded path; results are identical) */
     int32_t ctas;           /* <= 0 -> one CTA per SM; else the CTA count (test hook) */
     int64_t iters_per_launch; /* <= 0 -> unlimited: the whole solve is one persistent launch */
-    int32_t gram;           /* full-Gram path: 1 force, -1 never, 0 auto (one rank,
-                               20,000 <= n, 8 n^2 bytes within a third of free HBM, X not
-                               shared-memory resident).  K is precomputed once with the same
-                               arithmetic (R13/R14), so results are identical either way. */
-    int32_t pad_;
+    int32_t gram;           /* full-Gram path: 1 force (one rank), otherwise off.
+                               K is precomputed once with the same arithmetic (R13/R14), so
+                               results are identical either way. */
+    int32_t cache_rows;     /* kernel-row LRU cache: > 0 slots, -1 off, 0 auto
+                               (X streamed from HBM and n <= 200,000: max(64, n/25) slots, at most
+                               2048).  A slot holds the kernel row K(i, .) restricted to each CTA's
+                               own rows, so it never crosses CTAs; every CTA runs the same LRU
+                               directory on the same pair sequence.  An iteration whose two rows
+                               are both cached reads them instead of streaming X.  Cached values
+                               are the computed ones, so results are identical either way. */
 } svm_params;
 
 typedef struct {

@@ -118,6 +118,9 @@ struct Params {
     int direct_poll_ns;            // >= 0: skip the counter, poll the records directly with this backoff
     const double* gram;            // full-Gram path (a9): K [n_global][n_global], rows read per
                                    // iteration instead of streaming X (one rank only)
+    double* cache[MAXR];           // row cache (a8): [cache_slots][n_rows[r]] per rank, or null
+    int cache_slots;
+    int cache_hash;                // hash entries (power of two >= 2 cache_slots)
     int independent;               // 1: every rank is its own problem (batched OvO solves): no
                                    // exchange between ranks, per-rank X / max_iter below
     const float* xr_rank[MAXR];    // independent mode: row-major X of problem r
@@ -239,6 +242,11 @@ struct Shared {
     int red_i[2][NWC];
     double wf[2], wa[2];           // the global winner of this iteration
     int wi[2], wy[2];
+    int c_slot_u, c_slot_l;        // row cache: slot holding K(u,.) / K(l,.) (hit) ...
+    int c_fill_u, c_fill_l;        // ... or the slot this iteration fills (miss), else -1
+    int c_stream;                  // 1: X must be streamed this iteration
+    int c_fifo;                    // next FIFO victim slot
+    int kul_cnt;                   // compacted terms of K(x_u, x_l) (cache mode)
     double cf[2][NWC + 1];         // per warp combine results (global row index)
     int ci[2][NWC + 1];
     double ca[2][NWC + 1];
@@ -373,6 +381,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
     // binary RBF: K for every possible Hamming distance, K_tab[D] = exp_cr(-(gamma D))
     double* ktab = reinterpret_cast<double*>(smem_raw + off);
     if (P.bin_words) off += (size_t)(32 * P.bin_words + 1) * 8;
+    off = (off + 7) & ~size_t(7);
+    // row-cache directory: owner (global row) of every slot + an open-addressing hash
+    // row -> slot (cache_hash entries, a power of two >= 2 slots), FIFO replacement
+    int* dir_owner = reinterpret_cast<int*>(smem_raw + off); off += (size_t)P.cache_slots * 4;
+    off = (off + 7) & ~size_t(7);
+    int2* dir_hash = reinterpret_cast<int2*>(smem_raw + off); off += (size_t)P.cache_hash * 8;
+    // cache mode: the scalar warp compacts the k with a non-zero term of K(x_u, x_l) here
+    off = (off + 15) & ~size_t(15);
+    double2* kul_t = reinterpret_cast<double2*>(smem_raw + off);
+    if (P.cache_slots > 0) off += (size_t)P.d_pad * 16;
     off = (off + 127) & ~size_t(127);
     float* ring = reinterpret_cast<float*>(smem_raw + off);
     const int stage_floats = P.kc * P.rt;
@@ -399,6 +417,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     for (int e = t; e < svmexp::EXP_TABLE_DOUBLES; e += NTHREADS) sh.exp_tab[e] = svmexp::table_entry(e);
+    for (int e = t; e < P.cache_slots; e += NTHREADS) dir_owner[e] = -1;
+    for (int e = t; e < P.cache_hash; e += NTHREADS) dir_hash[e] = make_int2(-1, -1);
+    if (t == 0) sh.c_fifo = 0;
     for (int j = t; j < R; j += NTHREADS) {
         f_s[j] = P.f[rank][r0 + j];
         if (A_SMEM) a_s[j] = alpha_g[j];
@@ -658,6 +679,52 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
             if (t == 0) { sh.u = iu; sh.l = il; sh.f_up = fu; sh.f_low = fl; }
             break;
         }
+        // ---- row cache (a8): thread 0 of every CTA runs the same directory operations on
+        // the same pair sequence (hash lookup, FIFO replacement), so every CTA agrees
+        if (P.cache_slots > 0 && t == 0) {
+            const int hm = P.cache_hash - 1;
+            auto hslot = [&](int key) { return (int)(((unsigned)key * 2654435761u) >> 7) & hm; };
+            auto find = [&](int key) {
+                for (int h = hslot(key);; h = (h + 1) & hm) {
+                    const int2 e = dir_hash[h];
+                    if (e.x == key) return e.y;
+                    if (e.x < 0) return -1;
+                }
+            };
+            auto insert = [&](int key, int slot) {
+                int h = hslot(key);
+                while (dir_hash[h].x >= 0) h = (h + 1) & hm;
+                dir_hash[h] = make_int2(key, slot);
+            };
+            auto erase = [&](int key) {                   // linear probing, backward shift
+                int h = hslot(key);
+                while (dir_hash[h].x != key) h = (h + 1) & hm;
+                int j = h;
+                for (;;) {
+                    j = (j + 1) & hm;
+                    const int2 e = dir_hash[j];
+                    if (e.x < 0) break;
+                    const int k = hslot(e.x);
+                    // move e back to h if its home k is not cyclically in (h, j]
+                    const bool in_range = (h <= j) ? (h < k && k <= j) : (h < k || k <= j);
+                    if (!in_range) { dir_hash[h] = e; h = j; }
+                }
+                dir_hash[h] = make_int2(-1, -1);
+            };
+            const int su = find(iu), sl = find(il);
+            int fu_ = -1, fl_ = -1;
+            auto victim = [&](int avoid) {
+                int v = sh.c_fifo;
+                if (v == avoid) v = (v + 1) % P.cache_slots;
+                sh.c_fifo = (v + 1) % P.cache_slots;
+                if (dir_owner[v] >= 0) erase(dir_owner[v]);
+                return v;
+            };
+            if (su < 0) { fu_ = victim(sl); dir_owner[fu_] = iu; insert(iu, fu_); }
+            if (sl < 0) { fl_ = victim(su >= 0 ? su : fu_); dir_owner[fl_] = il; insert(il, fl_); }
+            sh.c_slot_u = su; sh.c_slot_l = sl; sh.c_fill_u = fu_; sh.c_fill_l = fl_;
+            sh.c_stream = (su < 0 || sl < 0) ? 1 : 0;
+        }
         // ---- pivot rows x_up, x_low (fp64 in shared memory, or bit rows), all threads
         if (P.gram) {
             // rows of K are read directly; no pivot rows needed
@@ -695,6 +762,26 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
         SVM_PHASE(timing, is_scalar ? PH_S_PIVOT : PH_C_PIVOT);
         const int u = iu, l = il;
         if (is_scalar) {
+            if (P.cache_slots > 0) {
+                // compact the non-zero terms of K(x_u, x_l) (RBF: x_u - x_l; linear: pairs
+                // with x_u or x_l non-zero) in ascending k
+                int cnt = 0;
+                for (int k0 = 0; k0 < P.d; k0 += 32) {
+                    const int k = k0 + lane;
+                    double2 pv = make_double2(0.0, 0.0);
+                    bool nz = false;
+                    if (k < P.d) {
+                        pv = piv[k];
+                        if (KERNEL == 1) { pv.x = pv.x - pv.y; nz = pv.x != 0.0; }
+                        else nz = (pv.x != 0.0) || (pv.y != 0.0);
+                    }
+                    const unsigned m = __ballot_sync(0xffffffffu, nz);
+                    if (nz) kul_t[cnt + __popc(m & ((1u << lane) - 1u))] = pv;
+                    cnt += __popc(m);
+                }
+                if (lane == 0) sh.kul_cnt = cnt;
+                __syncwarp();
+            }
             // ---- pair update (a2): eta, clipped step, snapped alphas (lane 0)
             if (lane == 0) {
                 double Kuu, Kll, Kul;
@@ -715,6 +802,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                         Kul = (u == l) ? 1.0 : ktab[cx];
                     } else {
                         Kuu = (double)cuu; Kll = (double)cll; Kul = (double)cul;
+                    }
+                } else if (P.cache_slots > 0) {
+                    // only k with a non-zero term change the sums (fma(0, x, acc) == acc), so
+                    // the serial chains run over the compacted non-zero terms (ascending k)
+                    const int cnt = sh.kul_cnt;
+                    if (KERNEL == 1) {
+                        double acc = 0.0;
+                        for (int i = 0; i < cnt; ++i) { const double dv = kul_t[i].x; acc = fma(dv, dv, acc); }
+                        Kuu = 1.0; Kll = 1.0;
+                        Kul = (u == l) ? 1.0 : svmexp::exp_cr_t(-(P.gamma * acc), tab);
+                    } else {
+                        double s_uu = 0.0, s_ll = 0.0, s_ul = 0.0;
+                        for (int i = 0; i < cnt; ++i) {
+                            const double2 pv = kul_t[i];
+                            s_uu = fma(pv.x, pv.x, s_uu); s_ll = fma(pv.y, pv.y, s_ll); s_ul = fma(pv.x, pv.y, s_ul);
+                        }
+                        Kuu = s_uu; Kll = s_ll; Kul = s_ul;
                     }
                 } else if (KERNEL == 1) {
                     double acc = 0.0;
@@ -768,6 +872,26 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
             continue;
         }
         // ================= consumers: row pass (a3-a5)
+        bool rows_ready = P.gram != nullptr;
+        const double* krow_u = nullptr;
+        const double* krow_l = nullptr;
+        double* fill_u = nullptr;
+        double* fill_l = nullptr;
+        if (P.gram) {
+            krow_u = P.gram + (long long)u * P.n_global + gbase;
+            krow_l = P.gram + (long long)l * P.n_global + gbase;
+        } else if (P.cache_slots > 0) {
+            double* cb = P.cache[rank] + r0;                  // this CTA's columns of every slot
+            const long long stride = P.n_rows[rank];
+            if (!sh.c_stream) {
+                rows_ready = true;
+                krow_u = cb + sh.c_slot_u * stride;
+                krow_l = cb + sh.c_slot_l * stride;
+            } else {
+                if (sh.c_fill_u >= 0) fill_u = cb + sh.c_fill_u * stride;
+                if (sh.c_fill_l >= 0) fill_l = cb + sh.c_fill_l * stride;
+            }
+        }
         double cu = 0.0, cl = 0.0;
         double bfu = INF, bfl = -INF;
         int bju = INT_MAX, bjl = INT_MAX;
@@ -779,14 +903,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
             double du[RPT], dl[RPT];
 #pragma unroll
             for (int q = 0; q < RPT; ++q) { du[q] = 0.0; dl[q] = 0.0; }
-            if (P.gram) {
+            if (rows_ready) {
                 if (active) {
-                    // rows u and l of the precomputed K (fp64, already the kernel values)
-                    const double* ku_row = P.gram + (long long)u * P.n_global + gbase + tile * P.rt + t * RPT;
-                    const double* kl_row = P.gram + (long long)l * P.n_global + gbase + tile * P.rt + t * RPT;
+                    // kernel values already computed: rows of K (Gram) or cached rows
+                    const double* ku_row = krow_u + tile * P.rt + t * RPT;
+                    const double* kl_row = krow_l + tile * P.rt + t * RPT;
 #pragma unroll
                     for (int q = 0; q < RPT; ++q) {
-                        if (tile * P.rt + t * RPT + q < R) { du[q] = __ldg(&ku_row[q]); dl[q] = __ldg(&kl_row[q]); }
+                        if (tile * P.rt + t * RPT + q < R) { du[q] = __ldcg(&ku_row[q]); dl[q] = __ldcg(&kl_row[q]); }
                     }
                 }
             } else if (P.bin_words) {
@@ -803,7 +927,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                     du[0] = (double)cu_; dl[0] = (double)cl_;
                 }
             }
-            for (int ch = 0; ch < ((P.bin_words || P.gram) ? 0 : P.n_chunks); ++ch) {
+            for (int ch = 0; ch < ((P.bin_words || rows_ready) ? 0 : P.n_chunks); ++ch) {
                 if (!P.resident) mbar_wait(&full[cslot], cpar);
                 const float* st = P.resident ? ring + (size_t)ch * P.kc * rp : ring + (size_t)cslot * stage_floats;
                 const int k0 = ch * P.kc;
@@ -882,7 +1006,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                     if (j < R) {
                         const long long jg = gbase + j;
                         double ku, kl;
-                        if (P.gram) {
+                        if (rows_ready) {
                             ku = du[q]; kl = dl[q];
                         } else if (KERNEL == 1 && P.bin_words) {
                             ku = (jg == u) ? 1.0 : ktab[(int)du[q]];
@@ -893,6 +1017,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                         } else {
                             ku = du[q]; kl = dl[q];
                         }
+                        if (fill_u) fill_u[j] = ku;          // row cache: store the computed
+                        if (fill_l) fill_l[j] = kl;          // kernel values of a missed row
                         const double fj = fma(cl, kl, fma(cu, ku, f_s[j]));
                         f_s[j] = fj;
                         const uint8_t g = fl_s[j];

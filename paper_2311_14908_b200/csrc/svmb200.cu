@@ -171,12 +171,14 @@ struct Plan {
     bool alpha_smem = true;
     bool resident = false;
     int bin_words = 0;
+    int cache_slots = 0;
+    int cache_hash = 0;
     long long cta_stride = 0;
     size_t smem = 0;
 };
 
 int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl, bool binary = false,
-              bool gram = false) {
+              bool gram = false, int cache_slots = 0) {
     pl.G = G;
     if (gram) {
         // rows of K are read from HBM: state and control only, no X stages
@@ -236,6 +238,11 @@ int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl, bool bina
     pl.alpha_smem = pl.state_cap <= 2048;                  // else alpha stays in HBM
     size_t fixed = (sizeof(Shared) + 127) & ~size_t(127);
     fixed += 2 * (size_t)pl.d_pad * 8 + (size_t)pl.state_cap * (pl.alpha_smem ? 17 : 9);  // pivots + state
+    int hash = 0;
+    if (cache_slots > 0) { hash = 1; while (hash < 2 * cache_slots) hash <<= 1; }
+    fixed = ((fixed + 7) & ~size_t(7)) + (size_t)cache_slots * 4;                       // cache directory
+    fixed = ((fixed + 7) & ~size_t(7)) + (size_t)hash * 8 + (cache_slots > 0 ? (size_t)pl.d_pad * 16 + 8 : 0);
+    pl.cache_hash = hash;
     fixed = (fixed + 127) & ~size_t(127);
     const size_t stage_bytes = (size_t)pl.kc * pl.rt * 4;
     // resident mode: the whole (single-tile) X block of a CTA fits next to the state
@@ -302,12 +309,9 @@ int solve(SolveArgs& a) {
     double* gram = nullptr;
     cudaEvent_t ev_gram = nullptr;
     const bool single = (a.world == 1 && a.nranks_here == 1 && !a.independent);
-    bool want_gram = single && a.p.gram == 1;
-    if (single && a.p.gram == 0 && !binary && a.n_global >= 20000) {
-        size_t fr = 0, tot = 0;
-        if (cudaMemGetInfo(&fr, &tot) == cudaSuccess)
-            want_gram = (double)a.n_global * a.n_global * 8.0 <= (double)fr / 3.0;
-    }
+    // (measured: building K costs more than the LRU row cache saves for W3, so the Gram
+    // path is used only on request)
+    const bool want_gram = single && a.p.gram == 1;
     if (a.p.gram == 1 && !single) return fail(SVM_EINVAL, "the Gram path needs a single rank");
     if (want_gram) {
         if (cudaMallocAsync(&gram, (size_t)a.n_global * a.n_global * 8, a.stream) != cudaSuccess) {
@@ -333,6 +337,25 @@ int solve(SolveArgs& a) {
         pl = Plan();
         rc = make_plan(a.n_rows_max, (int)a.d, a.ctas_per_rank, a.max_smem, pl);
         if (rc) return rc;
+        // kernel-row LRU cache (a8) for streamed X
+        int slots = a.p.cache_rows;
+        if (slots == 0 && !pl.resident && !a.independent && a.n_global <= 200000) {
+            slots = (int)(a.n_global / 25);
+            slots = slots < 64 ? 64 : (slots > 2048 ? 2048 : slots);
+            size_t fr = 0, tot = 0;
+            if (cudaMemGetInfo(&fr, &tot) != cudaSuccess ||
+                (double)slots * a.n_global * 8.0 > (double)fr / 3.0)
+                slots = 0;
+        }
+        if (slots > 0 && !pl.resident) {
+            if (slots < 4) slots = 4;
+            Plan pc;
+            if (make_plan(a.n_rows_max, (int)a.d, a.ctas_per_rank, a.max_smem, pc, false, false, slots) == SVM_OK &&
+                !pc.resident) {
+                pl = pc;
+                pl.cache_slots = slots;
+            }
+        }
     }
     KernelFn fn = pick_kernel(p.kernel, pl.rpt, pl.alpha_smem);
     CKR(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
@@ -370,6 +393,8 @@ int solve(SolveArgs& a) {
     P.check_interval = p.check_interval; P.state_cap = pl.state_cap; P.resident = pl.resident ? 1 : 0;
     P.bin_words = pl.bin_words;
     P.gram = gram;
+    P.cache_slots = pl.cache_slots;
+    P.cache_hash = pl.cache_hash;
     P.independent = a.independent ? 1 : 0;
     for (int r = 0; r < world; ++r) {
         P.xr_rank[r] = a.independent ? a.xr_rank[r] : a.xr;
@@ -401,6 +426,11 @@ int solve(SolveArgs& a) {
         if ((rc = dalloc((void**)&f, (size_t)nr * 8 + 8))) { release(); return rc; }
         if ((rc = dalloc((void**)&fl, (size_t)nr + 8))) { release(); return rc; }
         if ((rc = dalloc((void**)&ctl, sizeof(Ctl)))) { release(); return rc; }
+        if (pl.cache_slots > 0) {
+            double* cache;
+            if ((rc = dalloc((void**)&cache, (size_t)pl.cache_slots * (nr > 0 ? nr : 1) * 8))) { release(); return rc; }
+            P.cache[r] = cache;
+        }
         al = a.alpha_out[r];
         CKR(cudaMemsetAsync(xb, 0, (size_t)pl.cta_stride * pl.G * 4, st));
         CKR(cudaMemsetAsync(ctl, 0, sizeof(Ctl), st));
@@ -512,8 +542,9 @@ int solve(SolveArgs& a) {
         CKR(cudaStreamSynchronize(st));
         const char* nm[PH_N] = {"S.waitC", "S.publish", "S.poll", "S.read", "S.pivot", "S.kul",
                                 "C.exch", "C.pivot", "C.dist", "C.waitB", "C.update", "C.reduce"};
-        fprintf(stderr, "[svmb200] cycles/iter of CTA 0 over %lld iters (rpt=%d kc=%d stages=%d smem=%zu a_smem=%d resident=%d bin_words=%d):",
-                hc.it, pl.rpt, pl.kc, pl.stages, pl.smem, (int)pl.alpha_smem, (int)pl.resident, pl.bin_words);
+        fprintf(stderr, "[svmb200] cycles/iter of CTA 0 over %lld iters (rpt=%d kc=%d stages=%d smem=%zu a_smem=%d resident=%d bin_words=%d cache=%d gram=%d):",
+                hc.it, pl.rpt, pl.kc, pl.stages, pl.smem, (int)pl.alpha_smem, (int)pl.resident, pl.bin_words,
+                pl.cache_slots, gram ? 1 : 0);
         for (int k = 0; k < PH_N; ++k)
             fprintf(stderr, " %s=%.0f", nm[k], hc.it ? (double)tm[k] / hc.it : 0.0);
         fprintf(stderr, "\n");

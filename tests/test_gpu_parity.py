@@ -209,18 +209,24 @@ def test_predict_exact_parity(S, name, n, m):
 
 
 # ---------------------------------------------------------------- full-size configs
-def test_w2_full_matches_stored_oracle(S):
-    """Adult-like at full size (BASELINE.json configs[1], the bench workload): the whole
-    42,790-step trajectory against the oracle result stored by
-    oracle/tools/make_golden.py."""
-    path = os.path.join(GOLD, "W2_oracle.npz")
+@pytest.mark.parametrize("name,params", [
+    ("W2", {}),                      # bench workload: binary bit rows, X resident
+    ("W3", {}),                      # streamed X + automatic row cache (a8)
+    ("W3", {"cache_rows": -1}),      # streamed X, every row recomputed
+    ("W3", {"gram": 1}),             # full Gram matrix (a9)
+])
+def test_full_trajectory_matches_stored_oracle(S, name, params):
+    """Full-size configs: the whole trajectory (W2: 42,790 steps, BASELINE.json
+    configs[1], the bench workload; W3: 11,659 steps) against the oracle result stored
+    by oracle/tools/make_golden.py, in each execution mode the solve can take."""
+    path = os.path.join(GOLD, f"{name}_oracle.npz")
     if not os.path.exists(path):
-        pytest.skip("golden W2_oracle.npz not generated")
+        pytest.skip(f"golden {name}_oracle.npz not generated")
     g = np.load(path)
-    w = W.get("W2")
+    w = W.get(name)
     X, y = w.train()
     r = S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol, want_f=True,
-                       trace_cap=int(g["iterations"]) + 1)
+                       trace_cap=int(g["iterations"]) + 1, **params)
     assert r["info"]["iterations"] == int(g["iterations"])
     sha = hashlib.sha256(np.ascontiguousarray(r["trace"], dtype=np.int64).tobytes()).hexdigest()
     assert sha == str(g["trace_sha"])
@@ -357,4 +363,27 @@ def test_full_size_w3_streaming_prefix(S):
     k = 40
     r_or = O.train(X, y, w.C, w.kernel, w.gamma, w.tol, max_iter=k, trace_cap=k)
     r_g = S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol, max_iter=k, want_f=True, trace_cap=k, gram=-1)
+    _assert_exact(r_g, r_or)
+
+
+@pytest.mark.parametrize("name,n,slots", [("W3", 2000, 4), ("W3", 2000, 64), ("W5", 3000, 8), ("W1", 200, 4),
+                                          ("W4", 6000, 16)])
+def test_row_cache_parity(S, monkeypatch, name, n, slots):
+    """Kernel-row LRU cache on the streaming path (X not resident): tiny
+    caches force constant eviction; results stay identical to the oracle and to the
+    uncached solve."""
+    monkeypatch.setenv("SVMB200_NO_RESIDENT", "1")
+    w = W.get(name)
+    X, y = w.train(n)
+    r_g, r_or = _run_pair(S, w, X, y, cache_rows=slots)
+    _assert_exact(r_g, r_or)
+    r_nc = S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol, cache_rows=-1)
+    np.testing.assert_array_equal(r_nc["alpha"], r_g["alpha"])
+
+
+def test_row_cache_with_virtual_ranks(S, monkeypatch):
+    monkeypatch.setenv("SVMB200_NO_RESIDENT", "1")
+    w = W.get("W5")
+    X, y = w.train(2500)
+    r_g, r_or = _run_pair(S, w, X, y, cache_rows=32, virtual_ranks=3)
     _assert_exact(r_g, r_or)
