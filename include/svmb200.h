@@ -76,13 +76,21 @@ typedef struct {
     int32_t gram;           /* full-Gram path: 1 force (one rank), otherwise off.
                                K is precomputed once with the same arithmetic (R13/R14), so
                                results are identical either way. */
-    int32_t cache_rows;     /* kernel-row LRU cache: > 0 slots, -1 off, 0 auto
-                               (X streamed from HBM and n <= 200,000: max(64, n/25) slots, at most
+    int32_t cache_rows;     /* kernel-row cache: > 0 slots, -1 off, 0 auto (X
+                               streamed from HBM and n <= 200,000: max(64, n/25) slots, at most
                                2048).  A slot holds the kernel row K(i, .) restricted to each CTA's
-                               own rows, so it never crosses CTAs; every CTA runs the same LRU
-                               directory on the same pair sequence.  An iteration whose two rows
-                               are both cached reads them instead of streaming X.  Cached values
-                               are the computed ones, so results are identical either way. */
+                               own rows; every CTA runs the same directory (hash lookup, FIFO
+                               replacement) on the same pair sequence.  An iteration whose two
+                               rows are both cached reads them (and K_ul) instead of streaming X.
+                               Cached values are the computed ones, so results are identical. */
+    int32_t cluster;        /* candidate exchange among a rank's CTAs: 0 auto, -1 global-memory
+                               mailboxes, 1..16 force one thread-block cluster of that many CTAs
+                               per rank exchanging through distributed shared memory (one rank
+                               or batched problems; the rank's rows must fit resident in the
+                               cluster's shared memory).  Auto picks a cluster when the rows fit
+                               (<= 2048 rows per CTA, or <= 8192 with 16 CTAs).  The exchange
+                               computes the same lexicographic winner, so results are identical. */
+    int32_t reserved0;      /* 0 */
 } svm_params;
 
 typedef struct {

@@ -40,7 +40,8 @@ class Params(ctypes.Structure):
                 ("max_iter", ctypes.c_int64), ("check_interval", ctypes.c_int32),
                 ("kernel", ctypes.c_int32), ("sv_epsilon", ctypes.c_double),
                 ("virtual_ranks", ctypes.c_int32), ("ctas", ctypes.c_int32),
-                ("iters_per_launch", ctypes.c_int64), ("gram", ctypes.c_int32), ("cache_rows", ctypes.c_int32)]
+                ("iters_per_launch", ctypes.c_int64), ("gram", ctypes.c_int32), ("cache_rows", ctypes.c_int32),
+                ("cluster", ctypes.c_int32), ("reserved0", ctypes.c_int32)]
 
 
 class Info(ctypes.Structure):

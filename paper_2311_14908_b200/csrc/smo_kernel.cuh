@@ -48,32 +48,33 @@ constexpr int PRODUCER_WARP = NWC + 1;
 constexpr int NTHREADS = NT + 64;  // + scalar warp + producer warp
 constexpr int NSYNC = NT + 32;     // participants of the named barriers
 constexpr int MAX_STAGES = 16;
-enum { BAR_A = 1, BAR_B = 2, BAR_C = 3, BAR_D = 4, BAR_E = 5, BAR_F = 6 };
+enum { BAR_A = 1, BAR_B = 2, BAR_C = 3, BAR_D = 4 };
 
 enum { ST_RUNNING = 0, ST_CONVERGED = 1, ST_MAXITER = 2, ST_LIMIT = 3, ST_TIMEOUT = -8 };
 enum { FL_POS = 1, FL_UP = 2, FL_LOW = 4 };
 
-// One CTA's candidate record in "LL" form: twelve 8-byte words, each = (32-bit flag << 32)
-// | 32-bit payload, flag = exchange sequence number.  Aligned 8-byte stores are single-copy
-// atomic, so a record whose twelve flags all read `seq` is complete: no release fence is
-// needed on the writer's side.  Payload words: 0-1 f_up, 2-3 f_low, 4-5 a_up, 6-7 a_low
-// (lo, hi halves), 8 i_up, 9 i_low (global row, -1 = empty set), 10 y_up | y_low << 16.
-constexpr int REC_ROW_WORDS = 8;   // binary rows up to 256 features travel in the record
-constexpr int NREP = 8;            // max replicas of every record (spreads the all-to-all reads)
-struct __align__(16) Record {
-    unsigned long long w[12 + 2 * REC_ROW_WORDS];   // base words, then the two candidate bit rows
-};
-
+// One CTA's candidate record: four 16-byte words, each {seq:16 | chk:16, payload[3]},
+// written by one vector store and read by one vector load.  A word whose sequence number
+// (low 16 bits of the exchange number; the stale content of a slot is exchange seq - 2)
+// and checksum of its payload both match is taken as written by exchange seq, so a reader
+// needs no fence, counter or flag ordering (the checksum also rejects a word observed
+// half-written, should a 16-byte access ever be split).  Payloads:
+//   w0 = (i_up, f_up lo, f_up hi)    w1 = (i_low, f_low lo, f_low hi)
+//   w2 = (y_up | y_low << 16, a_up lo, a_up hi)    w3 = (0, a_low lo, a_low hi)
+// (i = global row, 0xffffffff = empty set).  The mailbox stores the words transposed,
+// word[parity][h][g], so one warp load of word h covers 32 consecutive records; the
+// selection polls w0/w1 only and fetches w2/w3 of the two winning records afterwards.
 struct __align__(128) Mailbox {
-    unsigned long long count;      // monotonic arrivals (relaxed: a hint that all records landed)
-    unsigned long long pad[15];
+    unsigned long long pad[16];
 };
-// records follow the header: Record recs[NREP][2][g_total] (replica, exchange parity)
-__host__ __device__ inline Record* mbox_parts(Mailbox* m, int rep, int parity, int g_total) {
-    return reinterpret_cast<Record*>(m + 1) + ((size_t)rep * 2 + parity) * g_total;
+__host__ __device__ inline uint4* mbox_words(Mailbox* m, int parity, int h, int g_total) {
+    return reinterpret_cast<uint4*>(m + 1) + ((size_t)parity * 4 + h) * g_total;
+}
+__host__ __device__ inline const uint4* mbox_words(const Mailbox* m, int parity, int h, int g_total) {
+    return reinterpret_cast<const uint4*>(m + 1) + ((size_t)parity * 4 + h) * g_total;
 }
 __host__ __device__ inline size_t mbox_bytes(int cpr, int world) {
-    return sizeof(Mailbox) + (size_t)NREP * 2 * cpr * world * sizeof(Record);
+    return sizeof(Mailbox) + (size_t)2 * 4 * cpr * world * sizeof(uint4);
 }
 
 struct Ctl {                       // per rank solver control, persists across launches
@@ -113,9 +114,6 @@ struct Params {
                                    // encoding); distances are popcounts -- exact, so identical to
                                    // the fp64 recurrence R13
     const uint32_t* xrbits;        // bit rows [n_global][bin_words] (pivot gather)
-    int rec_rows;                  // 1: candidate bit rows travel in the records (bin_words <= 8)
-    int nrep;                      // record replicas written (1..NREP); readers pick cta % nrep
-    int direct_poll_ns;            // >= 0: skip the counter, poll the records directly with this backoff
     const double* gram;            // full-Gram path (a9): K [n_global][n_global], rows read per
                                    // iteration instead of streaming X (one rank only)
     double* cache[MAXR];           // row cache (a8): [cache_slots][n_rows[r]] per rank, or null
@@ -127,6 +125,11 @@ struct Params {
     long long max_iter_rank[MAXR]; // independent mode: max_iter of problem r
     long long timeout_ns;
     int sys_scope;                 // 1 when mailboxes live on other GPUs (system scope)
+    int cluster;                   // 1: the ctas_per_rank CTAs of a rank form one thread-block
+                                   // cluster and exchange through distributed shared memory
+    int crow;                      // cluster mode: 32-bit words of a candidate row carried in
+                                   // its record (binary: bin_words, else d), 0 = rows gathered
+    int crw;                       // cluster mode: 16-byte words per record (4 + 2 ceil(crow/3))
     unsigned long long* timers;    // optional [8] per-phase cycle totals of CTA 0
 };
 
@@ -213,6 +216,26 @@ __device__ __forceinline__ void named_arrive(int id) {
     asm volatile("bar.arrive %0, %1;" :: "r"(id), "n"(NSYNC) : "memory");
 }
 
+// ---- thread-block cluster (distributed shared memory) helpers
+__device__ __forceinline__ uint32_t cluster_map(const void* p, int cta) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(cta));
+    return r;
+}
+__device__ __forceinline__ void st_cluster_v4(uint32_t addr, uint4 v) {
+    asm volatile("st.shared::cluster.v4.u32 [%0], {%1, %2, %3, %4};"
+                 :: "r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ uint4 ld_volatile_shared_v4(const uint4* p) {
+    uint4 v;
+    asm volatile("ld.volatile.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(smem_u32(p)) : "memory");
+    return v;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // Lexicographic "better" for the two selections: smaller f wins for I_up,
 // larger f for I_low, and the lower index wins a tie.  Empty = index INT_MAX.
 __device__ __forceinline__ bool better_up(double f1, int i1, double f2, int i2) {
@@ -240,17 +263,10 @@ struct Shared {
     double cu, cl;                 // written by the scalar warp before barrier B
     double red_f[2][NWC];          // per consumer warp candidates (local row index)
     int red_i[2][NWC];
-    double wf[2], wa[2];           // the global winner of this iteration
-    int wi[2], wy[2];
-    int c_slot_u, c_slot_l;        // row cache: slot holding K(u,.) / K(l,.) (hit) ...
-    int c_fill_u, c_fill_l;        // ... or the slot this iteration fills (miss), else -1
-    int c_stream;                  // 1: X must be streamed this iteration
+    int c_hit, c_su, c_sl;         // row cache: both rows cached / their slots
+    int c_fill_u, c_fill_l;        // row cache: the slot this iteration fills (miss), else -1
     int c_fifo;                    // next FIFO victim slot
     int kul_cnt;                   // compacted terms of K(x_u, x_l) (cache mode)
-    double cf[2][NWC + 1];         // per warp combine results (global row index)
-    int ci[2][NWC + 1];
-    double ca[2][NWC + 1];
-    int cy[2][NWC + 1];
     int timeout;
     unsigned long long bars[2 * MAX_STAGES];
     double exp_tab[svmexp::EXP_TABLE_DOUBLES];
@@ -283,61 +299,44 @@ __device__ __forceinline__ void cand_merge(Cand& a, const Cand& b) {
     if (b.iu != INT_MAX && better_up(b.fu, b.iu, a.fu, a.iu)) { a.fu = b.fu; a.iu = b.iu; a.au = b.au; a.yu = b.yu; }
     if (b.il != INT_MAX && better_low(b.fl, b.il, a.fl, a.il)) { a.fl = b.fl; a.il = b.il; a.al = b.al; a.yl = b.yl; }
 }
-__device__ __forceinline__ void cand_warp_merge(Cand& c) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        Cand b;
-        b.fu = __shfl_xor_sync(0xffffffffu, c.fu, o); b.iu = __shfl_xor_sync(0xffffffffu, c.iu, o);
-        b.au = __shfl_xor_sync(0xffffffffu, c.au, o); b.yu = __shfl_xor_sync(0xffffffffu, c.yu, o);
-        b.fl = __shfl_xor_sync(0xffffffffu, c.fl, o); b.il = __shfl_xor_sync(0xffffffffu, c.il, o);
-        b.al = __shfl_xor_sync(0xffffffffu, c.al, o); b.yl = __shfl_xor_sync(0xffffffffu, c.yl, o);
-        cand_merge(c, b);
-    }
+__device__ __forceinline__ uint32_t rec_chk(uint32_t a, uint32_t b, uint32_t c) {
+    // high half of a multiplicative hash: any change of one payload word changes it with
+    // probability ~1 - 2^-16
+    return (a * 0x9E3779B1u + b * 0x85EBCA77u + c * 0xC2B2AE3Du) >> 16;
 }
-__device__ __forceinline__ void ll_store(Record* rec, uint32_t fg, const Cand& c) {
-    unsigned long long* w = rec->w;
-    const unsigned long long bu = (unsigned long long)__double_as_longlong(c.fu);
-    const unsigned long long bl = (unsigned long long)__double_as_longlong(c.fl);
-    const unsigned long long au = (unsigned long long)__double_as_longlong(c.au);
-    const unsigned long long al = (unsigned long long)__double_as_longlong(c.al);
-    const uint32_t iu = c.iu == INT_MAX ? 0xffffffffu : (uint32_t)c.iu;
-    const uint32_t il = c.il == INT_MAX ? 0xffffffffu : (uint32_t)c.il;
-    const uint32_t yy = (uint32_t)((c.yu & 0xffff) | (c.yl << 16));
-    st_volatile_v2(w + 0, ll_word(fg, (uint32_t)bu), ll_word(fg, (uint32_t)(bu >> 32)));
-    st_volatile_v2(w + 2, ll_word(fg, (uint32_t)bl), ll_word(fg, (uint32_t)(bl >> 32)));
-    st_volatile_v2(w + 4, ll_word(fg, (uint32_t)au), ll_word(fg, (uint32_t)(au >> 32)));
-    st_volatile_v2(w + 6, ll_word(fg, (uint32_t)al), ll_word(fg, (uint32_t)(al >> 32)));
-    st_volatile_v2(w + 8, ll_word(fg, iu), ll_word(fg, il));
-    st_volatile_v2(w + 10, ll_word(fg, yy), ll_word(fg, 0u));
+__device__ __forceinline__ uint4 rec_pack(uint32_t sq, uint32_t a, unsigned long long v) {
+    const uint32_t lo = (uint32_t)v, hi = (uint32_t)(v >> 32);
+    return make_uint4((sq << 16) | rec_chk(a, lo, hi), a, lo, hi);
 }
-// the two candidate bit rows (W words each) after the 12 base words
-__device__ __forceinline__ void ll_store_rows(Record* rec, uint32_t fg, const uint32_t* ru, const uint32_t* rl, int W) {
-    unsigned long long* w = rec->w + 12;
-    for (int h = 0; h < W; h += 2) {
-        st_volatile_v2(w + h, ll_word(fg, ru[h]), ll_word(fg, h + 1 < W ? ru[h + 1] : 0u));
-        st_volatile_v2(w + REC_ROW_WORDS + h, ll_word(fg, rl[h]), ll_word(fg, h + 1 < W ? rl[h + 1] : 0u));
-    }
+// word h (0..3) of the record of candidate c for exchange sq
+__device__ __forceinline__ uint4 rec_word(const Cand& c, int h, uint32_t sq) {
+    if (h == 0) return rec_pack(sq, c.iu == INT_MAX ? 0xffffffffu : (uint32_t)c.iu, (unsigned long long)__double_as_longlong(c.fu));
+    if (h == 1) return rec_pack(sq, c.il == INT_MAX ? 0xffffffffu : (uint32_t)c.il, (unsigned long long)__double_as_longlong(c.fl));
+    if (h == 2) return rec_pack(sq, (uint32_t)((c.yu & 0xffff) | (c.yl << 16)), (unsigned long long)__double_as_longlong(c.au));
+    return rec_pack(sq, 0u, (unsigned long long)__double_as_longlong(c.al));
 }
-// One attempt: true (and c filled) when every word carries flag fg.
-__device__ __forceinline__ bool ll_try_load(const Record* rec, uint32_t fg, Cand& c) {
-    unsigned long long v[12];
-#pragma unroll
-    for (int h = 0; h < 6; ++h) ld_volatile_v2(rec->w + 2 * h, v[2 * h], v[2 * h + 1]);
-    bool ok = true;
-#pragma unroll
-    for (int h = 0; h < 12; ++h) ok = ok && (uint32_t)(v[h] >> 32) == fg;
-    if (!ok) return false;
-    c.fu = __longlong_as_double((long long)((v[0] & 0xffffffffull) | (v[1] << 32)));
-    c.fl = __longlong_as_double((long long)((v[2] & 0xffffffffull) | (v[3] << 32)));
-    c.au = __longlong_as_double((long long)((v[4] & 0xffffffffull) | (v[5] << 32)));
-    c.al = __longlong_as_double((long long)((v[6] & 0xffffffffull) | (v[7] << 32)));
-    const int iu = (int)(uint32_t)v[8], il = (int)(uint32_t)v[9];
-    c.iu = iu < 0 ? INT_MAX : iu;
-    c.il = il < 0 ? INT_MAX : il;
-    const uint32_t py = (uint32_t)v[10];
-    c.yu = (int)(int16_t)(py & 0xffff);
-    c.yl = (int)(int16_t)(py >> 16);
-    return true;
+__device__ __forceinline__ bool rec_ok(const uint4& v, uint32_t sq) {
+    return v.x == ((sq << 16) | rec_chk(v.y, v.z, v.w));
+}
+__device__ __forceinline__ double rec_f64(const uint4& v) {
+    return __longlong_as_double((long long)(((unsigned long long)v.w << 32) | v.z));
+}
+__device__ __forceinline__ int rec_idx(const uint4& v) {
+    return v.y == 0xffffffffu ? INT_MAX : (int)v.y;
+}
+__device__ __forceinline__ void rec_store(uint4* p, uint4 v, int sys) {
+    if (sys)
+        asm volatile("st.relaxed.sys.global.v4.u32 [%0], {%1, %2, %3, %4};" :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+    else
+        asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %4};" :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ uint4 rec_load(const uint4* p, int sys) {
+    uint4 v;
+    if (sys)
+        asm volatile("ld.relaxed.sys.global.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+    else
+        asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+    return v;
 }
 __device__ __forceinline__ void red_relaxed_gpu(unsigned long long* p) {
     asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" :: "l"(p) : "memory");
@@ -367,6 +366,78 @@ __device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long
     } while (0)
 
 // ------------------------------------------------------------------ the kernel
+// The scalar warp's record poll: lane L reads words 0 and 1 (the up and low candidates)
+// of records L, L + 32, ... (PB records in flight), re-reading the ones not yet written by
+// exchange sq, and keeps the lexicographically best up / low candidate it saw with the
+// record it came from (gu, gl).  Returns true (warp-uniform) on timeout.
+struct Sel {
+    double fu, fl;
+    int iu, il, gu, gl;
+};
+template <int PB>
+__device__ __forceinline__ bool poll_records(const uint4* w0, const uint4* w1, int g_total, uint32_t sq,
+                                             int sys, long long timeout_ns, int lane, Sel& b,
+                                             unsigned int& rounds) {
+    b.fu = __longlong_as_double(0x7ff0000000000000ll); b.fl = -b.fu;
+    b.iu = INT_MAX; b.il = INT_MAX; b.gu = 0; b.gl = 0;
+    bool tmo = false;
+    long long t0 = 0;
+    unsigned int spins = 0;
+    for (int g0 = 0; g0 < g_total && !tmo; g0 += 32 * PB) {
+        uint4 v[PB][2];
+        unsigned pend = 0;
+#pragma unroll
+        for (int q = 0; q < PB; ++q) if (g0 + 32 * q + lane < g_total) pend |= 1u << q;
+        const unsigned mine = pend;
+        while (pend) {
+            ++rounds;
+#pragma unroll
+            for (int q = 0; q < PB; ++q)
+                if (pend & (1u << q)) {
+                    const int g = g0 + 32 * q + lane;
+                    v[q][0] = rec_load(w0 + g, sys);
+                    v[q][1] = rec_load(w1 + g, sys);
+                }
+#pragma unroll
+            for (int q = 0; q < PB; ++q)
+                if ((pend & (1u << q)) && rec_ok(v[q][0], sq) && rec_ok(v[q][1], sq)) pend &= ~(1u << q);
+            if (pend && (++spins & 255u) == 0) {
+                const long long now = globaltimer();
+                if (t0 == 0) t0 = now;
+                else if (now - t0 > timeout_ns) { tmo = true; break; }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < PB; ++q)
+            if (mine & (1u << q)) {
+                const int g = g0 + 32 * q + lane;
+                const int iu = rec_idx(v[q][0]), il = rec_idx(v[q][1]);
+                const double fu = rec_f64(v[q][0]), fl = rec_f64(v[q][1]);
+                if (iu != INT_MAX && better_up(fu, iu, b.fu, b.iu)) { b.fu = fu; b.iu = iu; b.gu = g; }
+                if (il != INT_MAX && better_low(fl, il, b.fl, b.il)) { b.fl = fl; b.il = il; b.gl = g; }
+            }
+        tmo = __any_sync(0xffffffffu, tmo);
+    }
+    return tmo;
+}
+
+// Row cache (a8): rank owning global row g (ranks 0..world-1 hold consecutive blocks).
+__device__ __forceinline__ int cache_owner(const Params& P, long long g) {
+    int r = 0;
+    while (r + 1 < P.world && g >= P.row_off[r + 1]) ++r;
+    return r;
+}
+// K_ul can be read from a cached row when the columns it needs live on this GPU.
+__device__ __forceinline__ bool kul_cache_ok(const Params& P, int u, int l) {
+    if (P.independent) return false;
+    return P.cache[cache_owner(P, l)] != nullptr && P.cache[cache_owner(P, u)] != nullptr;
+}
+// Column g of the cached kernel row in slot s.
+__device__ __forceinline__ double kcache_at(const Params& P, int s, long long g) {
+    const int r = cache_owner(P, g);
+    return __ldcg(P.cache[r] + (long long)s * P.n_rows[r] + (g - P.row_off[r]));
+}
+
 template <int KERNEL, int RPT, bool A_SMEM>
 __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -391,6 +462,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
     off = (off + 15) & ~size_t(15);
     double2* kul_t = reinterpret_cast<double2*>(smem_raw + off);
     if (P.cache_slots > 0) off += (size_t)P.d_pad * 16;
+    // cluster mode: records of the rank's CTAs, cmb[parity][cta][crw] (written remotely)
+    uint4* cmb = reinterpret_cast<uint4*>(smem_raw + off);
+    if (P.cluster) off += (size_t)2 * P.ctas_per_rank * P.crw * 16;
     off = (off + 127) & ~size_t(127);
     float* ring = reinterpret_cast<float*>(smem_raw + off);
     const int stage_floats = P.kc * P.rt;
@@ -407,6 +481,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
     const int R = r1 - r0;                                   // rows owned by this CTA
     const long long gbase = P.row_off[rank] + r0;            // global index of local row 0
     const int n_tiles = (R + P.rt - 1) / P.rt;
+    const int rt_log2 = __ffs(P.rt) - 1;                     // rt = 256 RPT: a power of two
     const float* xcta = P.xblk[rank] + (long long)cta * P.cta_stride;
     double* alpha_g = P.alpha[rank] + r0;                    // this CTA's alpha (global)
     const double C = P.C;
@@ -419,6 +494,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
     for (int e = t; e < svmexp::EXP_TABLE_DOUBLES; e += NTHREADS) sh.exp_tab[e] = svmexp::table_entry(e);
     for (int e = t; e < P.cache_slots; e += NTHREADS) dir_owner[e] = -1;
     for (int e = t; e < P.cache_hash; e += NTHREADS) dir_hash[e] = make_int2(-1, -1);
+    if (P.cluster)
+        for (int e = t; e < 2 * P.ctas_per_rank * P.crw; e += NTHREADS) cmb[e] = make_uint4(0u, 0u, 0u, 0u);
     if (t == 0) sh.c_fifo = 0;
     for (int j = t; j < R; j += NTHREADS) {
         f_s[j] = P.f[rank][r0 + j];
@@ -432,10 +509,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
         __syncthreads();
     }
 
+    // every CTA of the cluster has zeroed its mailbox before any record is stored into it
+    if (P.cluster) cluster_sync_all();
+
     // ============================================================ producer warp
     if (warp == PRODUCER_WARP) {
+        // (cluster mode: the producer waits in the final cluster barrier, so no CTA exits
+        // while a peer may still address its shared memory)
         if (P.gram) {
             if (lane == 0) { sh.issued = 0; __threadfence_block(); sh.producer_done = 1; }
+            if (P.cluster) cluster_sync_all();
             return;
         }
         if (P.resident) {
@@ -447,6 +530,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                 bulk_g2s(ring, xcta, bytes, &full[0]);
             }
             if (lane == 0) { sh.issued = 0; __threadfence_block(); sh.producer_done = 1; }
+            if (P.cluster) cluster_sync_all();
             return;
         }
         if (lane == 0 && n_tiles > 0) {
@@ -473,6 +557,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
             }
         }
         if (lane == 0) { __threadfence_block(); sh.producer_done = 1; }
+        __syncwarp();
+        if (P.cluster) cluster_sync_all();
         return;
     }
 
@@ -515,29 +601,36 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
     for (;;) {
         named_sync(BAR_C);                  // consumer candidates are in sh.red_*
         SVM_PHASE(timing, is_scalar ? PH_S_WAITC : PH_C_REDUCE);
-        // ---- exchange seq + 1 (a6).  The scalar warp stores the CTA record (LL form)
-        // into every rank's mailbox -- peer pointers when the ranks are GPUs -- and bumps
-        // each rank's arrival counter with a relaxed reduction (no fence: the records
-        // validate themselves).  One thread polls the local counter; then every thread of
-        // the CTA reads its share of the records (re-reading any whose flags are not yet
-        // current) and the CTA reduces them lexicographically -- identical in every CTA of
-        // every rank.  Chosen by measurement (tools/exchange_bench.cu).
         ++seq;
-        const int g_total = xworld * P.ctas_per_rank;
-        const int par = (int)(seq & 1);
-        const uint32_t fg = (uint32_t)seq;
-        if (is_scalar) {
-            double fu = lane < NWC ? sh.red_f[0][lane] : INF;
-            int ju = lane < NWC ? sh.red_i[0][lane] : INT_MAX;
-            double fl = lane < NWC ? sh.red_f[1][lane] : -INF;
-            int jl = lane < NWC ? sh.red_i[1][lane] : INT_MAX;
-            warp_reduce_fi<true>(fu, ju, NWC);
-            warp_reduce_fi<false>(fl, jl, NWC);
-            // lanes 0-7 hold the CTA result; every lane writes some replica -> broadcast
-            fu = __shfl_sync(0xffffffffu, fu, 0); ju = __shfl_sync(0xffffffffu, ju, 0);
-            fl = __shfl_sync(0xffffffffu, fl, 0); jl = __shfl_sync(0xffffffffu, jl, 0);
+        if (!is_scalar) {
+            // consumers: the scalar warp runs the exchange, the selection, the stopping test,
+            // the row-cache directory and the pivot gather, then releases barrier A
+            named_sync(BAR_A);
+            SVM_PHASE(timing, PH_C_EXCH);
+            const int dec = sh.decision;
+            if (dec != ST_RUNNING) { final_state = dec; break; }
+        } else {
+            // ---- exchange seq (a6).  The scalar warp stores this CTA's record (four 16-byte
+            // words, each carrying the sequence number and a checksum of its payload) into
+            // every rank's mailbox -- peer pointers when the ranks are GPUs -- and polls all
+            // g_total records of its own mailbox, every lane keeping up to PB loads in flight.
+            // No fences or counters: a record word whose sequence number and checksum match
+            // is complete.  Measured against counter- and tree-based exchanges in
+            // tools/xch2_bench.cu.
+            const int g_total = xworld * P.ctas_per_rank;
+            const int par = (int)(seq & 1);
+            const uint32_t sq = (uint32_t)seq & 0xffffu;
+            Cand c;
+            int ju, jl;                                   // this CTA's candidates (local rows)
             {
-                Cand c;
+                double fu = lane < NWC ? sh.red_f[0][lane] : INF;
+                ju = lane < NWC ? sh.red_i[0][lane] : INT_MAX;
+                double fl = lane < NWC ? sh.red_f[1][lane] : -INF;
+                jl = lane < NWC ? sh.red_i[1][lane] : INT_MAX;
+                warp_reduce_fi<true>(fu, ju, NWC);
+                warp_reduce_fi<false>(fl, jl, NWC);
+                fu = __shfl_sync(0xffffffffu, fu, 0); ju = __shfl_sync(0xffffffffu, ju, 0);
+                fl = __shfl_sync(0xffffffffu, fl, 0); jl = __shfl_sync(0xffffffffu, jl, 0);
                 c.fu = fu; c.fl = fl;
                 c.iu = (ju == INT_MAX) ? INT_MAX : (int)(gbase + ju);
                 c.il = (jl == INT_MAX) ? INT_MAX : (int)(gbase + jl);
@@ -545,224 +638,258 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                 c.al = (jl == INT_MAX) ? 0.0 : (A_SMEM ? a_s[jl] : alpha_g[jl]);
                 c.yu = (ju == INT_MAX) ? 0 : ((fl_s[ju] & FL_POS) ? 1 : -1);
                 c.yl = (jl == INT_MAX) ? 0 : ((fl_s[jl] & FL_POS) ? 1 : -1);
-                uint32_t ru[REC_ROW_WORDS], rl[REC_ROW_WORDS];
-                if (P.rec_rows) {
-                    // the candidates' bit rows, from the resident block [tile][word][row]
-                    const uint32_t* xbits = reinterpret_cast<const uint32_t*>(ring);
-                    const int W = P.bin_words;
-#pragma unroll
-                    for (int h = 0; h < REC_ROW_WORDS; ++h) {
-                        ru[h] = 0u; rl[h] = 0u;
-                        if (h < W && ju != INT_MAX) {
-                            const int tl = ju / P.rt, rin = ju - tl * P.rt, rows_t = min(P.rt, R - tl * P.rt);
-                            ru[h] = xbits[(size_t)tl * W * P.rt + (size_t)h * ((rows_t + 3) & ~3) + rin];
-                        }
-                        if (h < W && jl != INT_MAX) {
-                            const int tl = jl / P.rt, rin = jl - tl * P.rt, rows_t = min(P.rt, R - tl * P.rt);
-                            rl[h] = xbits[(size_t)tl * W * P.rt + (size_t)h * ((rows_t + 3) & ~3) + rin];
-                        }
-                    }
-                }
-                const int gcta = (rank - xbase) * P.ctas_per_rank + cta;
-                for (int q = lane; q < xworld * P.nrep; q += 32) {
-                    Record* rec = mbox_parts(P.mbox[xbase + q / P.nrep], q % P.nrep, par, g_total) + gcta;
-                    ll_store(rec, fg, c);
-                    if (P.rec_rows) ll_store_rows(rec, fg, ru, rl, P.bin_words);
-                }
-                __syncwarp();
-                if (lane < xworld && P.direct_poll_ns < 0) {
-                    if (P.sys_scope) red_relaxed_sys(&P.mbox[xbase + lane]->count);
-                    else red_relaxed_gpu(&P.mbox[xbase + lane]->count);
-                }
             }
-            SVM_PHASE(timing, PH_S_PUBLISH);
-            if (lane == 0 && P.direct_poll_ns < 0) {
-                const unsigned long long target = (unsigned long long)seq * g_total;
-                long long t0 = 0;
-                unsigned int spins = 0;
-                while ((P.sys_scope ? ld_relaxed_sys(&my_mb->count) : ld_relaxed_gpu(&my_mb->count)) < target) {
-                    if ((++spins & 1023u) == 0) {
-                        const long long now = globaltimer();
-                        if (t0 == 0) t0 = now;
-                        else if (now - t0 > P.timeout_ns) { sh.timeout = 1; break; }
-                    }
-                }
-            }
-            SVM_PHASE(timing, PH_S_POLL);
-        }
-        named_sync(BAR_E);                  // records published (direct mode) / landed (counter mode)
-        uint32_t myrow_u[REC_ROW_WORDS], myrow_l[REC_ROW_WORDS];  // bit rows of my best candidates
-        int my_iu = INT_MAX, my_il = INT_MAX;
-        {
-            Cand c;
-            cand_init(c);
-            if (!sh.timeout) {
-                const Record* recs = mbox_parts(my_mb, cta % P.nrep, par, g_total);
-                long long t0 = 0;
-                unsigned int spins = 0;
-                for (int g = t; g < g_total; g += NSYNC) {
-                    Cand r;
-                    bool ok;
-                    uint32_t wu[REC_ROW_WORDS], wl[REC_ROW_WORDS];
-                    for (;;) {
-                        ok = ll_try_load(recs + g, fg, r);
-                        if (ok && P.rec_rows) {
-                            const unsigned long long* w = recs[g].w + 12;
-#pragma unroll
-                            for (int h = 0; h < REC_ROW_WORDS; h += 2) {
-                                unsigned long long a0, a1, b0, b1;
-                                if (h < P.bin_words) {
-                                    ld_volatile_v2(w + h, a0, a1);
-                                    ld_volatile_v2(w + REC_ROW_WORDS + h, b0, b1);
-                                    ok = ok && (uint32_t)(a0 >> 32) == fg && (uint32_t)(a1 >> 32) == fg &&
-                                         (uint32_t)(b0 >> 32) == fg && (uint32_t)(b1 >> 32) == fg;
-                                    wu[h] = (uint32_t)a0; wu[h + 1] = (uint32_t)a1;
-                                    wl[h] = (uint32_t)b0; wl[h + 1] = (uint32_t)b1;
-                                } else {
-                                    wu[h] = wu[h + 1] = wl[h] = wl[h + 1] = 0u;
-                                }
+            Sel best;
+            bool tmo;
+            if (P.cluster) {
+                // ---- cluster exchange: store the record (4 words + the candidates' rows)
+                // into every CTA's shared-memory mailbox of this rank's cluster, then poll the
+                // local mailbox (lane j reads the record of CTA j)
+                const int G = P.ctas_per_rank, RW = P.crw, rw = (P.crow + 2) / 3;
+                // lane h < RW builds word h of the record and stores it into every CTA
+                if (lane < RW) {
+                    uint4 wv;
+                    if (lane < 4) {
+                        wv = rec_word(c, lane, sq);
+                    } else {
+                        const bool is_u = (lane - 4) < rw;
+                        const int k0 = 3 * ((lane - 4) - (is_u ? 0 : rw));
+                        const int jr = is_u ? ju : jl;
+                        uint32_t e[3] = {0u, 0u, 0u};
+                        if (jr != INT_MAX) {
+                            const uint32_t* base;
+                            int stride;
+                            if (P.bin_words) {
+                                const int tl = jr >> rt_log2, rin = jr & (P.rt - 1), rows_t = min(P.rt, R - (tl << rt_log2));
+                                base = reinterpret_cast<const uint32_t*>(ring) + (size_t)tl * P.bin_words * P.rt + rin;
+                                stride = (rows_t + 3) & ~3;
+                            } else {
+                                base = reinterpret_cast<const uint32_t*>(ring) + jr;
+                                stride = (R + 3) & ~3;
                             }
+#pragma unroll
+                            for (int m = 0; m < 3; ++m)
+                                if (k0 + m < P.crow) e[m] = base[(size_t)(k0 + m) * stride];
                         }
-                        if (ok) break;
-                        if (P.direct_poll_ns > 0) __nanosleep(P.direct_poll_ns);
+                        wv = rec_pack(sq, e[0], (unsigned long long)e[1] | ((unsigned long long)e[2] << 32));
+                    }
+                    const uint32_t src = smem_u32(cmb + ((size_t)par * G + cta) * RW + lane);
+                    for (int j = 0; j < G; ++j) {
+                        uint32_t ra;
+                        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(src), "r"(j));
+                        st_cluster_v4(ra, wv);
+                    }
+                }
+                SVM_PHASE(timing, PH_S_PUBLISH);
+                // lane j < G polls words 0/1 (the candidates) of CTA j's record
+                best.fu = INF; best.fl = -INF; best.iu = INT_MAX; best.il = INT_MAX; best.gu = 0; best.gl = 0;
+                bool to = false;
+                if (lane < G) {
+                    const uint4* r = cmb + ((size_t)par * G + lane) * RW;
+                    long long t0 = 0;
+                    unsigned int spins = 0;
+                    uint4 w0, w1;
+                    for (;;) {
+                        w0 = ld_volatile_shared_v4(r);
+                        w1 = ld_volatile_shared_v4(r + 1);
+                        if (rec_ok(w0, sq) && rec_ok(w1, sq)) break;
                         if ((++spins & 255u) == 0) {
                             const long long now = globaltimer();
                             if (t0 == 0) t0 = now;
-                            else if (now - t0 > P.timeout_ns) { sh.timeout = 1; break; }
+                            else if (now - t0 > P.timeout_ns) { to = true; break; }
                         }
                     }
-                    if (!ok) break;
-                    if (r.iu != INT_MAX && better_up(r.fu, r.iu, c.fu, c.iu)) {
-                        c.fu = r.fu; c.iu = r.iu; c.au = r.au; c.yu = r.yu;
-                        my_iu = r.iu;
-#pragma unroll
-                        for (int h = 0; h < REC_ROW_WORDS; ++h) myrow_u[h] = wu[h];
-                    }
-                    if (r.il != INT_MAX && better_low(r.fl, r.il, c.fl, c.il)) {
-                        c.fl = r.fl; c.il = r.il; c.al = r.al; c.yl = r.yl;
-                        my_il = r.il;
-#pragma unroll
-                        for (int h = 0; h < REC_ROW_WORDS; ++h) myrow_l[h] = wl[h];
-                    }
+                    best.iu = rec_idx(w0); best.fu = best.iu == INT_MAX ? INF : rec_f64(w0); best.gu = lane;
+                    best.il = rec_idx(w1); best.fl = best.il == INT_MAX ? -INF : rec_f64(w1); best.gl = lane;
                 }
+                tmo = __any_sync(0xffffffffu, to) || sh.timeout != 0;
+            } else {
+                const int gcta = (rank - xbase) * P.ctas_per_rank + cta;
+                if (lane < 4 * xworld)
+                    rec_store(mbox_words(P.mbox[xbase + (lane >> 2)], par, lane & 3, g_total) + gcta,
+                              rec_word(c, lane & 3, sq), P.sys_scope);
+                SVM_PHASE(timing, PH_S_PUBLISH);
+                constexpr int PB = 5;                            // records in flight per lane
+                unsigned int rounds = 0;
+                tmo = poll_records<PB>(mbox_words(my_mb, par, 0, g_total), mbox_words(my_mb, par, 1, g_total),
+                                       g_total, sq, P.sys_scope, P.timeout_ns, lane, best, rounds) ||
+                      sh.timeout != 0;
+                if (timing) ph_acc[PH_C_PIVOT] += rounds;     // (timers only) poll rounds of lane 0
             }
-            cand_warp_merge(c);
-            if (lane == 0 && P.bin_words && !P.rec_rows && c.iu != INT_MAX && c.il != INT_MAX) {
-                // the winner is one of the 9 warp results: pull their bit rows into this
-                // SM's L1 now, so the pivot gather after barrier F hits L1
-                asm volatile("prefetch.global.L1 [%0];" :: "l"(P.xrbits + (long long)c.iu * P.bin_words));
-                asm volatile("prefetch.global.L1 [%0];" :: "l"(P.xrbits + (long long)c.il * P.bin_words));
-            }
-            if (lane == 0) {
-                sh.cf[0][warp] = c.fu; sh.ci[0][warp] = c.iu; sh.ca[0][warp] = c.au; sh.cy[0][warp] = c.yu;
-                sh.cf[1][warp] = c.fl; sh.ci[1][warp] = c.il; sh.ca[1][warp] = c.al; sh.cy[1][warp] = c.yl;
-            }
-        }
-        named_sync(BAR_F);
-        SVM_PHASE(timing, is_scalar ? PH_S_READ : PH_C_EXCH);
-        // every thread reduces the 9 warp results in the same order -> same winners
-        double fu = sh.cf[0][0], fl = sh.cf[1][0], au = sh.ca[0][0], al = sh.ca[1][0];
-        int iu = sh.ci[0][0], il = sh.ci[1][0], yu = sh.cy[0][0], yl = sh.cy[1][0];
-#pragma unroll
-        for (int w = 1; w < NWC + 1; ++w) {
-            if (better_up(sh.cf[0][w], sh.ci[0][w], fu, iu)) { fu = sh.cf[0][w]; iu = sh.ci[0][w]; au = sh.ca[0][w]; yu = sh.cy[0][w]; }
-            if (better_low(sh.cf[1][w], sh.ci[1][w], fl, il)) { fl = sh.cf[1][w]; il = sh.ci[1][w]; al = sh.ca[1][w]; yl = sh.cy[1][w]; }
-        }
-        int dec = ST_RUNNING;
-        if (sh.timeout) dec = ST_TIMEOUT;
-        else if (iu == INT_MAX || il == INT_MAX) dec = ST_CONVERGED;
-        else if (fl - fu <= 2.0 * P.tol) dec = ST_CONVERGED;
-        else if (it == max_iter) dec = ST_MAXITER;
-        else if (P.iter_limit > 0 && it - it_start == P.iter_limit) dec = ST_LIMIT;
-        if (dec != ST_RUNNING) {
-            final_state = dec;
-            if (t == 0) { sh.u = iu; sh.l = il; sh.f_up = fu; sh.f_low = fl; }
-            break;
-        }
-        // ---- row cache (a8): thread 0 of every CTA runs the same directory operations on
-        // the same pair sequence (hash lookup, FIFO replacement), so every CTA agrees
-        if (P.cache_slots > 0 && t == 0) {
-            const int hm = P.cache_hash - 1;
-            auto hslot = [&](int key) { return (int)(((unsigned)key * 2654435761u) >> 7) & hm; };
-            auto find = [&](int key) {
-                for (int h = hslot(key);; h = (h + 1) & hm) {
-                    const int2 e = dir_hash[h];
-                    if (e.x == key) return e.y;
-                    if (e.x < 0) return -1;
+            SVM_PHASE(timing, PH_S_POLL);
+            // the warp's winners and the records they came from
+            double fu = best.fu, fl = best.fl;
+            int iu = best.iu, il = best.il;
+            warp_reduce_fi<true>(fu, iu);
+            warp_reduce_fi<false>(fl, il);
+            const unsigned mu = __ballot_sync(0xffffffffu, best.iu == iu);
+            const unsigned ml = __ballot_sync(0xffffffffu, best.il == il);
+            const int rec_u = __shfl_sync(0xffffffffu, best.gu, mu ? __ffs(mu) - 1 : 0);
+            const int rec_l = __shfl_sync(0xffffffffu, best.gl, ml ? __ffs(ml) - 1 : 0);
+            int dec = ST_RUNNING;
+            if (tmo) dec = ST_TIMEOUT;
+            else if (iu == INT_MAX || il == INT_MAX) dec = ST_CONVERGED;
+            else if (fl - fu <= 2.0 * P.tol) dec = ST_CONVERGED;
+            else if (it == max_iter) dec = ST_MAXITER;
+            else if (P.iter_limit > 0 && it - it_start == P.iter_limit) dec = ST_LIMIT;
+            if (dec != ST_RUNNING) {
+                final_state = dec;
+                if (lane == 0) {
+                    if (tmo) sh.timeout = 1;
+                    sh.decision = dec; sh.u = iu; sh.l = il; sh.f_up = fu; sh.f_low = fl;
                 }
-            };
-            auto insert = [&](int key, int slot) {
-                int h = hslot(key);
-                while (dir_hash[h].x >= 0) h = (h + 1) & hm;
-                dir_hash[h] = make_int2(key, slot);
-            };
-            auto erase = [&](int key) {                   // linear probing, backward shift
-                int h = hslot(key);
-                while (dir_hash[h].x != key) h = (h + 1) & hm;
-                int j = h;
-                for (;;) {
-                    j = (j + 1) & hm;
-                    const int2 e = dir_hash[j];
-                    if (e.x < 0) break;
-                    const int k = hslot(e.x);
-                    // move e back to h if its home k is not cyclically in (h, j]
-                    const bool in_range = (h <= j) ? (h < k && k <= j) : (h < k || k <= j);
-                    if (!in_range) { dir_hash[h] = e; h = j; }
-                }
-                dir_hash[h] = make_int2(-1, -1);
-            };
-            const int su = find(iu), sl = find(il);
-            int fu_ = -1, fl_ = -1;
-            auto victim = [&](int avoid) {
-                int v = sh.c_fifo;
-                if (v == avoid) v = (v + 1) % P.cache_slots;
-                sh.c_fifo = (v + 1) % P.cache_slots;
-                if (dir_owner[v] >= 0) erase(dir_owner[v]);
-                return v;
-            };
-            if (su < 0) { fu_ = victim(sl); dir_owner[fu_] = iu; insert(iu, fu_); }
-            if (sl < 0) { fl_ = victim(su >= 0 ? su : fu_); dir_owner[fl_] = il; insert(il, fl_); }
-            sh.c_slot_u = su; sh.c_slot_l = sl; sh.c_fill_u = fu_; sh.c_fill_l = fl_;
-            sh.c_stream = (su < 0 || sl < 0) ? 1 : 0;
-        }
-        // ---- pivot rows x_up, x_low (fp64 in shared memory, or bit rows), all threads
-        if (P.gram) {
-            // rows of K are read directly; no pivot rows needed
-        } else if (P.rec_rows) {
-            uint32_t* pw = reinterpret_cast<uint32_t*>(piv);
-            if (my_iu == iu)
-                for (int h = 0; h < P.bin_words; ++h) pw[h] = myrow_u[h];
-            if (my_il == il)
-                for (int h = 0; h < P.bin_words; ++h) pw[P.bin_words + h] = myrow_l[h];
-        } else if (P.bin_words) {
-            uint32_t* pw = reinterpret_cast<uint32_t*>(piv);
-            if (t < 2 * P.bin_words) {
-                const int w = t % P.bin_words;
-                pw[t] = __ldg(&P.xrbits[(long long)(t < P.bin_words ? iu : il) * P.bin_words + w]);
+                __syncwarp();
+                named_arrive(BAR_A);
+                break;
             }
-        } else {
-            const float* xu_g = xr + (long long)iu * P.d;
-            const float* xl_g = xr + (long long)il * P.d;
-            for (int k0 = 0; k0 < P.d_pad; k0 += NSYNC * 4) {
-                float vu[4], vl[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int k = k0 + q * NSYNC + t;
-                    vu[q] = (k < P.d) ? __ldg(&xu_g[k]) : 0.0f;
-                    vl[q] = (k < P.d) ? __ldg(&xl_g[k]) : 0.0f;
-                }
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int k = k0 + q * NSYNC + t;
-                    if (k < P.d_pad) piv[k] = make_double2((double)vu[q], (double)vl[q]);
-                }
-            }
-        }
-        named_sync(BAR_A);
-        SVM_PHASE(timing, is_scalar ? PH_S_PIVOT : PH_C_PIVOT);
-        const int u = iu, l = il;
-        if (is_scalar) {
+            // ---- row cache (a8): every CTA runs the same directory operations on the same
+            // pair sequence (hash lookup, FIFO replacement), so every CTA agrees
+            int c_hit = 0, su = -1, sl = -1;
             if (P.cache_slots > 0) {
+                if (lane == 0) {
+                    const int hm = P.cache_hash - 1;
+                    auto hslot = [&](int key) { return (int)(((unsigned)key * 2654435761u) >> 7) & hm; };
+                    auto find = [&](int key) {
+                        for (int h = hslot(key);; h = (h + 1) & hm) {
+                            const int2 e = dir_hash[h];
+                            if (e.x == key) return e.y;
+                            if (e.x < 0) return -1;
+                        }
+                    };
+                    auto insert = [&](int key, int slot) {
+                        int h = hslot(key);
+                        while (dir_hash[h].x >= 0) h = (h + 1) & hm;
+                        dir_hash[h] = make_int2(key, slot);
+                    };
+                    auto erase = [&](int key) {                   // linear probing, backward shift
+                        int h = hslot(key);
+                        while (dir_hash[h].x != key) h = (h + 1) & hm;
+                        int j = h;
+                        for (;;) {
+                            j = (j + 1) & hm;
+                            const int2 e = dir_hash[j];
+                            if (e.x < 0) break;
+                            const int k = hslot(e.x);
+                            // move e back to h if its home k is not cyclically in (h, j]
+                            const bool in_range = (h <= j) ? (h < k && k <= j) : (h < k || k <= j);
+                            if (!in_range) { dir_hash[h] = e; h = j; }
+                        }
+                        dir_hash[h] = make_int2(-1, -1);
+                    };
+                    auto victim = [&](int avoid) {
+                        int v = sh.c_fifo;
+                        if (v == avoid) v = (v + 1) % P.cache_slots;
+                        sh.c_fifo = (v + 1) % P.cache_slots;
+                        if (dir_owner[v] >= 0) erase(dir_owner[v]);
+                        return v;
+                    };
+                    su = find(iu); sl = find(il);
+                    c_hit = (su >= 0 && sl >= 0) ? 1 : 0;
+                    int fu_ = -1, fl_ = -1;
+                    if (su < 0) { fu_ = victim(sl); dir_owner[fu_] = iu; insert(iu, fu_); }
+                    if (sl < 0) { fl_ = victim(su >= 0 ? su : fu_); dir_owner[fl_] = il; insert(il, fl_); }
+                    sh.c_hit = c_hit; sh.c_su = su; sh.c_sl = sl; sh.c_fill_u = fu_; sh.c_fill_l = fl_;
+                }
+                c_hit = __shfl_sync(0xffffffffu, c_hit, 0);
+                su = __shfl_sync(0xffffffffu, su, 0);
+                sl = __shfl_sync(0xffffffffu, sl, 0);
+            }
+            SVM_PHASE(timing, PH_S_READ);
+            // alpha and label of the two winners: words 2 / 3 of their records, in flight
+            // while the pivot rows load (lane 0: w2 of u's record, 1: w2 of l's, 2: w3 of l's)
+            // cluster mode: lane 0: word 2 of u's record, 1/2: words 2/3 of l's record,
+            // 3.. 3+rw-1: u's row words, 3+rw .. 3+2rw-1: l's row words (validated: they may
+            // trail the candidate words)
+            const int rwc = (P.crow + 2) / 3;
+            const uint4* wp;
+            if (P.cluster) {
+                int rr, hh;
+                if (lane < 3) { rr = lane == 0 ? rec_u : rec_l; hh = lane == 2 ? 3 : 2; }
+                else if (lane < 3 + rwc) { rr = rec_u; hh = 4 + (lane - 3); }
+                else { rr = rec_l; hh = 4 + rwc + (lane - 3 - rwc); }
+                wp = cmb + ((size_t)par * P.ctas_per_rank + rr) * P.crw + (hh < P.crw ? hh : 0);
+            } else {
+                wp = mbox_words(my_mb, par, lane == 2 ? 3 : 2, g_total) + (lane == 0 ? rec_u : rec_l);
+            }
+            uint4 wa = make_uint4(0u, 0u, 0u, 0u);
+            if (P.cluster) {
+                if (lane < 3 + (P.gram || c_hit ? 0 : 2 * rwc)) {
+                    wa = ld_volatile_shared_v4(wp);
+                    unsigned int spins = 0;
+                    while (!rec_ok(wa, sq)) {
+                        wa = ld_volatile_shared_v4(wp);
+                        if (++spins > (1u << 24)) { sh.timeout = 1; break; }
+                    }
+                }
+            } else if (lane < 3) {
+                wa = rec_load(wp, P.sys_scope);
+            }
+            // ---- pivot rows x_up, x_low into shared memory (fp64, or bit rows)
+            if (P.gram || c_hit) {
+                // rows of K are read directly (Gram or cached rows; K_ul from the cached row
+                // of u); no pivot rows needed
+            } else if (P.cluster && P.crow) {
+                // the winners' rows travelled in their records (lanes 3.. hold the words)
+                const int nu = P.bin_words ? P.bin_words : P.d;
+                for (int k0 = 0; k0 < (P.bin_words ? 32 : P.d_pad); k0 += 32) {
+                    const int k = k0 + lane;
+                    const int kk = k < nu ? k : 0;
+                    const int src_u = 3 + kk / 3, src_l = 3 + rwc + kk / 3, m = kk % 3;
+                    const uint32_t vu_y = __shfl_sync(0xffffffffu, wa.y, src_u), vu_z = __shfl_sync(0xffffffffu, wa.z, src_u),
+                                   vu_w = __shfl_sync(0xffffffffu, wa.w, src_u);
+                    const uint32_t vl_y = __shfl_sync(0xffffffffu, wa.y, src_l), vl_z = __shfl_sync(0xffffffffu, wa.z, src_l),
+                                   vl_w = __shfl_sync(0xffffffffu, wa.w, src_l);
+                    const uint32_t xu = m == 0 ? vu_y : (m == 1 ? vu_z : vu_w);
+                    const uint32_t xl = m == 0 ? vl_y : (m == 1 ? vl_z : vl_w);
+                    if (P.bin_words) {
+                        uint32_t* pw = reinterpret_cast<uint32_t*>(piv);
+                        if (k < nu) { pw[k] = xu; pw[P.bin_words + k] = xl; }
+                    } else if (k < P.d_pad) {
+                        piv[k] = k < nu ? make_double2((double)__uint_as_float(xu), (double)__uint_as_float(xl))
+                                        : make_double2(0.0, 0.0);
+                    }
+                }
+            } else if (P.bin_words) {
+                uint32_t* pw = reinterpret_cast<uint32_t*>(piv);
+                if (lane < 2 * P.bin_words) {
+                    const int w = lane % P.bin_words;
+                    pw[lane] = __ldg(&P.xrbits[(long long)(lane < P.bin_words ? iu : il) * P.bin_words + w]);
+                }
+            } else {
+                const float* xu_g = xr + (long long)iu * P.d;
+                const float* xl_g = xr + (long long)il * P.d;
+                for (int k0 = 0; k0 < P.d_pad; k0 += 32 * 8) {
+                    float vu[8], vl[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int k = k0 + 32 * q + lane;
+                        vu[q] = (k < P.d) ? __ldg(&xu_g[k]) : 0.0f;
+                        vl[q] = (k < P.d) ? __ldg(&xl_g[k]) : 0.0f;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int k = k0 + 32 * q + lane;
+                        if (k < P.d_pad) piv[k] = make_double2((double)vu[q], (double)vl[q]);
+                    }
+                }
+            }
+            if (lane == 0) { sh.decision = ST_RUNNING; sh.u = iu; sh.l = il; }
+            __syncwarp();
+            named_arrive(BAR_A);
+            if (lane < 3 && !P.cluster) {
+                unsigned int spins = 0;
+                while (!rec_ok(wa, sq)) {            // written with w0/w1: (almost) never taken
+                    wa = rec_load(wp, P.sys_scope);
+                    if (++spins > (1u << 24)) { sh.timeout = 1; break; }
+                }
+            }
+            const int yu = (int)(int16_t)(__shfl_sync(0xffffffffu, wa.y, 0) & 0xffffu);
+            const double au = __hiloint2double((int)__shfl_sync(0xffffffffu, wa.w, 0), (int)__shfl_sync(0xffffffffu, wa.z, 0));
+            const int yl = (int)(int16_t)(__shfl_sync(0xffffffffu, wa.y, 1) >> 16);
+            const double al = __hiloint2double((int)__shfl_sync(0xffffffffu, wa.w, 2), (int)__shfl_sync(0xffffffffu, wa.z, 2));
+            SVM_PHASE(timing, PH_S_PIVOT);
+            const int u = iu, l = il;
+            if (P.cache_slots > 0 && !c_hit) {
                 // compact the non-zero terms of K(x_u, x_l) (RBF: x_u - x_l; linear: pairs
                 // with x_u or x_l non-zero) in ascending k
                 int cnt = 0;
@@ -782,7 +909,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                 if (lane == 0) sh.kul_cnt = cnt;
                 __syncwarp();
             }
-            // ---- pair update (a2): eta, clipped step, snapped alphas (lane 0)
+        // ---- pair update (a2): eta, clipped step, snapped alphas (lane 0)
             if (lane == 0) {
                 double Kuu, Kll, Kul;
                 if (P.gram) {
@@ -803,6 +930,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                     } else {
                         Kuu = (double)cuu; Kll = (double)cll; Kul = (double)cul;
                     }
+                } else if (c_hit && kul_cache_ok(P, u, l)) {
+                    // both rows cached: K_ul is column l of the cached row of u (computed by
+                    // l's owner CTA with the row-pass arithmetic, made visible by its fence);
+                    // K(x, x) is column u of u's row / column l of l's row
+                    Kul = kcache_at(P, su, l);
+                    if (KERNEL == 1) { Kuu = 1.0; Kll = 1.0; }
+                    else { Kuu = kcache_at(P, su, u); Kll = kcache_at(P, sl, l); }
                 } else if (P.cache_slots > 0) {
                     // only k with a non-zero term change the sums (fma(0, x, acc) == acc), so
                     // the serial chains run over the compacted non-zero terms (ascending k)
@@ -872,6 +1006,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
             continue;
         }
         // ================= consumers: row pass (a3-a5)
+        const int u = sh.u, l = sh.l;
+        const bool c_hit = P.cache_slots > 0 && sh.c_hit;
+        const int su = sh.c_su, sl = sh.c_sl;
         bool rows_ready = P.gram != nullptr;
         const double* krow_u = nullptr;
         const double* krow_l = nullptr;
@@ -883,19 +1020,89 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
         } else if (P.cache_slots > 0) {
             double* cb = P.cache[rank] + r0;                  // this CTA's columns of every slot
             const long long stride = P.n_rows[rank];
-            if (!sh.c_stream) {
+            if (c_hit) {
                 rows_ready = true;
-                krow_u = cb + sh.c_slot_u * stride;
-                krow_l = cb + sh.c_slot_l * stride;
-            } else {
-                if (sh.c_fill_u >= 0) fill_u = cb + sh.c_fill_u * stride;
-                if (sh.c_fill_l >= 0) fill_l = cb + sh.c_fill_l * stride;
+                krow_u = cb + su * stride;
+                krow_l = cb + sl * stride;
             }
         }
         double cu = 0.0, cl = 0.0;
         double bfu = INF, bfl = -INF;
         int bju = INT_MAX, bjl = INT_MAX;
         if (n_tiles == 0) named_sync(BAR_B);
+        if (P.bin_words && !rows_ready && n_tiles > 0) {
+            // binary bit rows resident ([tile][word][row]); thread t owns row t of every tile.
+            // The popcounts of BT tiles are independent chains computed together, then the
+            // rows are updated after barrier B.
+            constexpr int BT = 8;
+            const int lu_loc = (u >= gbase && u < gbase + R) ? (int)(u - gbase) : -1;
+            const int ll_loc = (l >= gbase && l < gbase + R) ? (int)(l - gbase) : -1;
+            const uint32_t* pw = reinterpret_cast<const uint32_t*>(piv);
+            const uint32_t* xb0 = reinterpret_cast<const uint32_t*>(ring);
+            const int W = P.bin_words;
+            for (int tb = 0; tb < n_tiles; tb += BT) {
+                // all loads of a batch are unconditional (clamped to a valid row), so they
+                // issue back to back; rows past the end are computed and discarded
+                const uint32_t* xq[BT];
+                int rq[BT];
+#pragma unroll
+                for (int q = 0; q < BT; ++q) {
+                    const int tile = min(tb + q, n_tiles - 1);
+                    const int rows_t = min(P.rt, R - tile * P.rt);
+                    rq[q] = (rows_t + 3) & ~3;
+                    xq[q] = xb0 + (size_t)tile * W * P.rt + min(t, rows_t - 1);
+                }
+                int cu_[BT], cl_[BT];
+#pragma unroll
+                for (int q = 0; q < BT; ++q) { cu_[q] = 0; cl_[q] = 0; }
+                for (int w = 0; w < W; ++w) {
+                    const uint32_t pu = pw[w], pl = pw[W + w];
+                    uint32_t xv[BT];
+#pragma unroll
+                    for (int q = 0; q < BT; ++q) xv[q] = xq[q][(size_t)w * rq[q]];
+#pragma unroll
+                    for (int q = 0; q < BT; ++q) {
+                        if (KERNEL == 1) { cu_[q] += __popc(xv[q] ^ pu); cl_[q] += __popc(xv[q] ^ pl); }
+                        else { cu_[q] += __popc(xv[q] & pu); cl_[q] += __popc(xv[q] & pl); }
+                    }
+                }
+                if (tb == 0) {
+                    SVM_PHASE(timing, PH_C_DIST);
+                    named_sync(BAR_B);          // c_u, c_l and the owner's flags are ready
+                    SVM_PHASE(timing, PH_C_WAITB);
+                    cu = sh.cu; cl = sh.cl;
+                }
+                double ku[BT], kl[BT], fo[BT];
+                uint8_t gq[BT];
+#pragma unroll
+                for (int q = 0; q < BT; ++q) {
+                    const int j = min((tb + q) * P.rt + t, R - 1);
+                    if (KERNEL == 1) {
+                        ku[q] = ktab[cu_[q]];
+                        kl[q] = ktab[cl_[q]];
+                    } else {
+                        ku[q] = (double)cu_[q]; kl[q] = (double)cl_[q];
+                    }
+                    fo[q] = f_s[j];
+                    gq[q] = fl_s[j];
+                }
+#pragma unroll
+                for (int q = 0; q < BT; ++q) {
+                    const int j = (tb + q) * P.rt + t;
+                    if (tb + q < n_tiles && j < R) {
+                        if (KERNEL == 1) {
+                            if (j == lu_loc) ku[q] = 1.0;
+                            if (j == ll_loc) kl[q] = 1.0;
+                        }
+                        const double fj = fma(cl, kl[q], fma(cu, ku[q], fo[q]));
+                        f_s[j] = fj;
+                        // this thread visits its rows in increasing j: a tie keeps the earlier
+                        if ((gq[q] & FL_UP) && fj < bfu) { bfu = fj; bju = j; }
+                        if ((gq[q] & FL_LOW) && fj > bfl) { bfl = fj; bjl = j; }
+                    }
+                }
+            }
+        } else
         for (int tile = 0; tile < n_tiles; ++tile) {
             const int rows_t = min(P.rt, R - tile * P.rt);
             const int rp = (rows_t + 3) & ~3;
@@ -995,9 +1202,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
             }
             if (tile == 0) {
                 SVM_PHASE(timing, PH_C_DIST);
-                named_sync(BAR_B);          // c_u, c_l and the owner's flags are ready
+                named_sync(BAR_B);          // c_u, c_l, the owner's flags and the fill slots are ready
                 SVM_PHASE(timing, PH_C_WAITB);
                 cu = sh.cu; cl = sh.cl;
+                if (P.cache_slots > 0 && !c_hit) {
+                    double* cb = P.cache[rank] + r0;
+                    const long long stride = P.n_rows[rank];
+                    if (sh.c_fill_u >= 0) fill_u = cb + sh.c_fill_u * stride;
+                    if (sh.c_fill_l >= 0) fill_l = cb + sh.c_fill_l * stride;
+                }
             }
             if (active) {
 #pragma unroll
@@ -1028,6 +1241,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                 }
             }
         }
+        // filled cache columns are read by other CTAs' scalar warps (K_ul) in later
+        // iterations: order them before this CTA's next record
+        if (fill_u || fill_l) __threadfence();
         SVM_PHASE(timing, PH_C_UPDATE);
         warp_reduce_fi<true>(bfu, bju);
         warp_reduce_fi<false>(bfl, bjl);
@@ -1074,6 +1290,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
         ctl->i_up = sh.u == INT_MAX ? -1 : sh.u;
         ctl->i_low = sh.l == INT_MAX ? -1 : sh.l;
     }
+    __syncwarp();
+    if (P.cluster) cluster_sync_all();
 }
 
 }  // namespace svmk

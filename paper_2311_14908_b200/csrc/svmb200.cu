@@ -24,6 +24,7 @@
 using namespace svmk;
 
 namespace svmint {
+static_assert(sizeof(svm_params) == 80, "svm_params layout (binding and tests assume 80 bytes)");
 
 thread_local std::string g_err;
 thread_local long long g_launches = 0;
@@ -173,13 +174,17 @@ struct Plan {
     int bin_words = 0;
     int cache_slots = 0;
     int cache_hash = 0;
+    int cluster = 0;  // > 0: cluster mode with G CTAs per cluster (one cluster per rank)
+    int crow = 0, crw = 0;
     long long cta_stride = 0;
     size_t smem = 0;
 };
 
 int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl, bool binary = false,
-              bool gram = false, int cache_slots = 0) {
+              bool gram = false, int cache_slots = 0, int cl_words = 0) {
     pl.G = G;
+    // cluster mode: the shared-memory mailbox cmb[2][G][cl_words] of 16-byte words
+    const size_t cl_bytes = cl_words > 0 ? (size_t)2 * G * cl_words * 16 + 16 : 0;
     if (gram) {
         // rows of K are read from HBM: state and control only, no X stages
         pl.state_cap = (int)((n_r_max + G - 1) / G);
@@ -209,6 +214,7 @@ int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl, bool bina
         size_t fixed = (sizeof(Shared) + 127) & ~size_t(127);
         fixed += 2 * (size_t)pl.d_pad * 8 + (size_t)pl.state_cap * (pl.alpha_smem ? 17 : 9);
         fixed = ((fixed + 7) & ~size_t(7)) + (size_t)(32 * pl.bin_words + 1) * 8;   // K table
+        fixed += cl_bytes;
         fixed = (fixed + 127) & ~size_t(127);
         const size_t bytes = (size_t)pl.cta_stride * 4;
         pl.resident = true;
@@ -243,6 +249,7 @@ int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl, bool bina
     fixed = ((fixed + 7) & ~size_t(7)) + (size_t)cache_slots * 4;                       // cache directory
     fixed = ((fixed + 7) & ~size_t(7)) + (size_t)hash * 8 + (cache_slots > 0 ? (size_t)pl.d_pad * 16 + 8 : 0);
     pl.cache_hash = hash;
+    fixed += cl_bytes;
     fixed = (fixed + 127) & ~size_t(127);
     const size_t stage_bytes = (size_t)pl.kc * pl.rt * 4;
     // resident mode: the whole (single-tile) X block of a CTA fits next to the state
@@ -357,8 +364,59 @@ int solve(SolveArgs& a) {
             }
         }
     }
+    // ---- cluster mode: when a rank's rows fit resident in the shared memory of <= 16 CTAs,
+    // those CTAs form one thread-block cluster and exchange candidates through distributed
+    // shared memory (~0.2 us) instead of global-memory mailboxes (~2.5 us); the candidates'
+    // rows travel in the records.  Auto: the smallest power-of-two cluster with <= 2048 rows
+    // per CTA (else 16 CTAs if <= 8192 rows each), when it is resident.
+    const bool cl_allowed = gram == nullptr && pl.cache_slots == 0 && a.p.cluster != -1 &&
+                            a.world == a.nranks_here && (a.world == 1 || a.independent) &&
+                            (a.p.ctas <= 0 || a.p.cluster > 0) && getenv("SVMB200_NO_CLUSTER") == nullptr;
+    if (a.p.cluster > 16 || a.p.cluster < -1) return fail(SVM_EINVAL, "cluster must be -1, 0 or 1..16");
+    if (a.p.cluster > 0 && !cl_allowed)
+        return fail(SVM_EINVAL, "cluster mode needs one rank (or batched problems) and no Gram/cache path");
+    if (cl_allowed) {
+        const int crow = binary ? (pl.bin_words <= 12 ? pl.bin_words : 0) : (a.d <= 12 ? (int)a.d : 0);
+        const int crw = 4 + 2 * ((crow + 2) / 3);
+        for (int gc = 1; gc <= 16; gc *= 2) {
+            if (a.p.cluster > 0 && gc != a.p.cluster) continue;
+            const long long rows = (a.n_rows_max + gc - 1) / gc;
+            if (a.p.cluster == 0) {
+                if (rows > 8192) continue;
+                if (rows > 2048 && gc < 16) continue;
+            }
+            if ((long long)gc * a.nranks_here > a.n_sm) break;
+            Plan pc;
+            if (make_plan(a.n_rows_max, (int)a.d, gc, a.max_smem, pc, binary, false, 0, crw) != SVM_OK) {
+                cudaGetLastError();
+                continue;
+            }
+            if (!pc.resident) continue;
+            KernelFn f2 = pick_kernel(p.kernel, pc.rpt, pc.alpha_smem);
+            CKR(cudaFuncSetAttribute((const void*)f2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pc.smem));
+            if (gc > 8) CKR(cudaFuncSetAttribute((const void*)f2, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            cudaLaunchConfig_t cfg = {};
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = gc; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+            cfg.gridDim = dim3(gc * a.nranks_here); cfg.blockDim = dim3(NTHREADS);
+            cfg.dynamicSmemBytes = pc.smem; cfg.attrs = at; cfg.numAttrs = 1;
+            int ncl = 0;
+            if (cudaOccupancyMaxActiveClusters(&ncl, (const void*)f2, &cfg) != cudaSuccess || ncl < 1) {
+                cudaGetLastError();
+                continue;
+            }
+            pl = pc;
+            pl.cluster = gc; pl.crow = crow; pl.crw = crw;
+            a.ctas_per_rank = gc;
+            break;
+        }
+        if (a.p.cluster > 0 && pl.cluster == 0)
+            return fail(SVM_EINVAL, "cluster mode needs every rank's rows resident in the cluster's shared memory");
+    }
     KernelFn fn = pick_kernel(p.kernel, pl.rpt, pl.alpha_smem);
     CKR(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+    if (pl.cluster > 8) CKR(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     int per_sm = 0;
     CKR(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, NTHREADS, pl.smem));
     const int grid = a.ctas_per_rank * a.nranks_here;
@@ -395,25 +453,14 @@ int solve(SolveArgs& a) {
     P.gram = gram;
     P.cache_slots = pl.cache_slots;
     P.cache_hash = pl.cache_hash;
+    P.cluster = pl.cluster > 0 ? 1 : 0;
+    P.crow = pl.crow;
+    P.crw = pl.crw;
     P.independent = a.independent ? 1 : 0;
     for (int r = 0; r < world; ++r) {
         P.xr_rank[r] = a.independent ? a.xr_rank[r] : a.xr;
         P.max_iter_rank[r] = a.independent ? a.max_iter_rank[r] : p.max_iter;
     }
-    // Candidate bit rows inside the records (saves the pivot round trip) measured slower on
-    // W2 (larger records, row extraction on the publish path): off unless requested.
-    P.rec_rows = 0;
-    if (const char* e = getenv("SVMB200_RECROWS"))
-        P.rec_rows = (pl.bin_words > 0 && pl.bin_words <= REC_ROW_WORDS && atoi(e) != 0) ? 1 : 0;
-    P.nrep = 4;                                            // 4 replicas: measured best on W2
-    if (const char* e = getenv("SVMB200_NREP")) { const int v = atoi(e); if (v >= 1 && v <= NREP) P.nrep = v; }
-    // Record reads: direct LL polling right after the publish barrier is fastest when the
-    // solve is latency-bound (X resident in shared memory: W2 4.8 vs 5.5 us/iteration);
-    // when X streams from HBM the CTAs arrive spread out and 288 pollers per CTA slow the
-    // stragglers (W3/W4/W5 +10-15%), so there one thread polls the arrival counter first.
-    P.direct_poll_ns = (pl.resident && !a.independent && a.mbox_local_alloc) ? 0 : -1;
-    if (const char* e = getenv("SVMB200_DIRECTPOLL")) P.direct_poll_ns = atoi(e);
-    if (const char* e = getenv("SVMB200_NREP")) { const int v = atoi(e); if (v >= 1 && v <= NREP) P.nrep = v; }
     P.timeout_ns = a.timeout_ns;
     P.sys_scope = a.mbox_local_alloc ? 0 : 1;
     const bool want_timers = getenv("SVMB200_PHASE_TIMERS") != nullptr;
@@ -501,7 +548,19 @@ int solve(SolveArgs& a) {
     long long launches = 0;
     for (;;) {
         void* args[] = {(void*)&P};
-        cudaError_t e = cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(NTHREADS), args, pl.smem, st);
+        cudaError_t e;
+        if (pl.cluster) {
+            // clusters are independent (no exchange between them): a plain cluster launch
+            cudaLaunchConfig_t cfg = {};
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = pl.cluster; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+            cfg.gridDim = dim3(grid); cfg.blockDim = dim3(NTHREADS);
+            cfg.dynamicSmemBytes = pl.smem; cfg.stream = st; cfg.attrs = at; cfg.numAttrs = 1;
+            e = cudaLaunchKernelExC(&cfg, (const void*)fn, args);
+        } else {
+            e = cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(NTHREADS), args, pl.smem, st);
+        }
         if (e != cudaSuccess) { release(); return fail(SVM_ECUDA, std::string("cooperative launch: ") + cudaGetErrorString(e)); }
         ++launches;
         counted();
@@ -540,11 +599,11 @@ int solve(SolveArgs& a) {
         unsigned long long tm[PH_N];
         CKR(cudaMemcpyAsync(tm, P.timers, sizeof(tm), cudaMemcpyDeviceToHost, st));
         CKR(cudaStreamSynchronize(st));
-        const char* nm[PH_N] = {"S.waitC", "S.publish", "S.poll", "S.read", "S.pivot", "S.kul",
-                                "C.exch", "C.pivot", "C.dist", "C.waitB", "C.update", "C.reduce"};
-        fprintf(stderr, "[svmb200] cycles/iter of CTA 0 over %lld iters (rpt=%d kc=%d stages=%d smem=%zu a_smem=%d resident=%d bin_words=%d cache=%d gram=%d):",
+        const char* nm[PH_N] = {"S.waitC", "S.publish", "S.poll", "S.select", "S.pivot", "S.kul",
+                                "C.waitA", "S.pollrounds", "C.dist", "C.waitB", "C.update", "C.reduce"};
+        fprintf(stderr, "[svmb200] cycles/iter of CTA 0 over %lld iters (rpt=%d kc=%d stages=%d smem=%zu a_smem=%d resident=%d bin_words=%d cache=%d gram=%d cluster=%d):",
                 hc.it, pl.rpt, pl.kc, pl.stages, pl.smem, (int)pl.alpha_smem, (int)pl.resident, pl.bin_words,
-                pl.cache_slots, gram ? 1 : 0);
+                pl.cache_slots, gram ? 1 : 0, pl.cluster);
         for (int k = 0; k < PH_N; ++k)
             fprintf(stderr, " %s=%.0f", nm[k], hc.it ? (double)tm[k] / hc.it : 0.0);
         fprintf(stderr, "\n");

@@ -52,8 +52,8 @@ def test_library_is_sm100a(S):
 
 
 def test_struct_layouts_match_header(S):
-    # svm_params: 3 doubles, int64, int32, int32, double, int32, int32, int64, int32, int32 = 72 bytes
-    assert ctypes.sizeof(S.Params) == 72
+    # svm_params: 3 doubles, int64, int32, int32, double, int32, int32, int64, 4 x int32 = 80 bytes
+    assert ctypes.sizeof(S.Params) == 80
     assert ctypes.sizeof(S.Info) == 72
     assert S.version().startswith("svmb200")
 

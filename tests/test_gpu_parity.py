@@ -7,6 +7,7 @@ relative, decision values 1e-4 absolute, identical labels, identical SV sets wit
 within 1e-6 C) the tests also require the identical pair trajectory and bit-equal alpha.
 """
 import hashlib
+import types
 import os
 
 import numpy as np
@@ -125,6 +126,45 @@ def test_partition_independence(S, vr, ctas):
     X, y = w.train(2500)
     r_g, r_or = _run_pair(S, w, X, y, virtual_ranks=vr, ctas=ctas)
     _assert_exact(r_g, r_or)
+
+
+def _cluster_cases():
+    rng = np.random.default_rng(31)
+    cases = []
+    w1 = W.get("W1")
+    cases.append(("W1 d=2 (rows in records)", w1, *w1.train()))
+    w2 = W.get("W2")
+    X2, y2 = w2.train()
+    cases.append(("W2 4000 rows, bit rows in records", w2, X2[:4000], y2[:4000]))
+    for n, d in ((900, 10), (600, 40)):                  # d > 12: rows gathered from HBM
+        X = rng.normal(size=(n, d)).astype(np.float32)
+        y = np.where(X[:, 0] + 0.7 * rng.normal(size=n) > 0, 1, -1).astype(np.int8)
+        w = types.SimpleNamespace(C=1.0, kernel=1, gamma=0.1, tol=1e-3)
+        cases.append((f"dense n={n} d={d}", w, X, y))
+    return cases
+
+
+@pytest.mark.parametrize("cluster", [-1, 1, 2, 4, 8, 16])
+def test_cluster_exchange_parity(S, cluster):
+    """Cluster mode -- the rank's CTAs form one thread-block cluster and exchange their
+    candidates through distributed shared memory, the candidates' rows travelling in the
+    records when they are short -- gives the oracle's trajectory bit for bit, as does the
+    global-mailbox exchange (cluster=-1), for every cluster size."""
+    for label, w, X, y in _cluster_cases():
+        r_g, r_or = _run_pair(S, w, X, y, cluster=cluster)
+        _assert_exact(r_g, r_or)
+
+
+def test_cluster_mode_errors(S):
+    w = W.get("W1")
+    X, y = w.train()
+    with pytest.raises(S.SvmError, match="cluster"):
+        S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol, cluster=17)
+    with pytest.raises(S.SvmError, match="cluster"):
+        S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol, cluster=2, virtual_ranks=2)
+    X5, y5 = W.get("W5").train(20000)                    # 20,000 x 256 floats: not resident
+    with pytest.raises(S.SvmError, match="cluster"):
+        S.svm_train_ex(X5, y5, 1.0, 1, 1.0 / 256, 1e-3, cluster=2, max_iter=5)
 
 
 def test_ragged_and_tiny(S):

@@ -221,6 +221,68 @@ __global__ void s4(Rec* recs, unsigned long long* cnt, int iters, double* out) {
     if (t == 0) out[blockIdx.x] = acc;
 }
 
+
+// Shared helpers for S5/S6: every thread t < G polls record t (direct polling, as the SMO
+// kernel does when X is resident), then warp shuffles + one barrier + a 9-way reduce.
+__device__ __forceinline__ void ldv4(const void* p, unsigned& s, unsigned& i, unsigned long long& f) {
+    unsigned a, b, c, d;
+    asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "l"(p) : "memory");
+    s = a; i = b; f = ((unsigned long long)d << 32) | c;
+}
+__device__ __forceinline__ void stv4(void* p, unsigned s, unsigned i, unsigned long long f) {
+    asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" :: "l"(p), "r"(s), "r"(i), "r"((unsigned)f), "r"((unsigned)(f >> 32)) : "memory");
+}
+template <int NREP>
+__global__ void s5(uint4* recs, int iters, double* out, int rec16) {
+    // rec16 = 16-byte words per record: 2 (compact: up + low) or 6 (96-byte LL-style size)
+    __shared__ double wf[2][10]; __shared__ int wi[2][10];
+    const int t = threadIdx.x, G = gridDim.x, lane = t & 31, warp = t >> 5;
+    double acc = 0;
+    for (int it = 0; it < iters; ++it) {
+        const int par = it & 1;
+        const unsigned fg = it + 1;
+        if (warp == 8) {
+            const double f = my_f(blockIdx.x, it);
+            for (int q = lane; q < NREP * rec16; q += 32) {
+                const int rep = q / rec16, w = q % rec16;
+                uint4* r = recs + ((size_t)(rep * 2 + par) * G + blockIdx.x) * rec16 + w;
+                stv4(r, fg, blockIdx.x, __double_as_longlong(f + w));
+            }
+        }
+        __syncthreads();
+        double bu = 1e300, bl = -1e300; int iu = 1 << 30, il = 1 << 30;
+        if (t < G) {
+            const uint4* r = recs + ((size_t)((blockIdx.x % NREP) * 2 + par) * G + t) * rec16;
+            unsigned s0, i0; unsigned long long f0;
+            unsigned s1, i1; unsigned long long f1;
+            for (;;) {
+                bool ok = true;
+                ldv4(r, s0, i0, f0); ok = s0 == fg;
+                ldv4(r + 1, s1, i1, f1); ok = ok && s1 == fg;
+                for (int w = 2; w < rec16; ++w) { unsigned sx, ix; unsigned long long fx; ldv4(r + w, sx, ix, fx); ok = ok && sx == fg; }
+                if (ok) break;
+            }
+            bu = __longlong_as_double(f0); iu = i0; bl = __longlong_as_double(f1); il = i1;
+        }
+        for (int o = 16; o; o >>= 1) {
+            const double f2 = __shfl_xor_sync(~0u, bu, o); const int i2 = __shfl_xor_sync(~0u, iu, o);
+            if (f2 < bu || (f2 == bu && i2 < iu)) { bu = f2; iu = i2; }
+            const double f3 = __shfl_xor_sync(~0u, bl, o); const int i3 = __shfl_xor_sync(~0u, il, o);
+            if (f3 > bl || (f3 == bl && i3 < il)) { bl = f3; il = i3; }
+        }
+        if (lane == 0) { wf[0][warp] = bu; wi[0][warp] = iu; wf[1][warp] = bl; wi[1][warp] = il; }
+        __syncthreads();
+        bu = wf[0][0]; iu = wi[0][0]; bl = wf[1][0]; il = wi[1][0];
+        for (int w = 1; w < NTH / 32; ++w) {
+            if (wf[0][w] < bu || (wf[0][w] == bu && wi[0][w] < iu)) { bu = wf[0][w]; iu = wi[0][w]; }
+            if (wf[1][w] > bl || (wf[1][w] == bl && wi[1][w] < il)) { bl = wf[1][w]; il = wi[1][w]; }
+        }
+        acc += bu + iu + bl + il;
+        __syncthreads();
+    }
+    if (t == 0) out[blockIdx.x] = acc;
+}
+
 int main() {
     int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
     Rec* recs; LL* ll; LL* bc; unsigned long long* cnt; double* out;
@@ -239,5 +301,12 @@ int main() {
     time("S2 LL all-to-all, warp polls all records", [&] { s2<<<nsm, NTH>>>(ll, iters, out); });
     time("S3 LL aggregator + 8 broadcast replicas", [&] { s3<<<nsm, NTH>>>(ll, bc, iters, out); });
     time("S4 counter red.release, warp reads unrolled", [&] { s4<<<nsm, NTH>>>(recs, cnt, iters, out); });
+    uint4* r5; cudaMalloc(&r5, (size_t)16 * nsm * 6 * 16);
+    auto z5 = [&] { cudaMemset(r5, 0, (size_t)16 * nsm * 6 * 16); cudaDeviceSynchronize(); };
+    z5(); time("S5 compact 32B, direct, NREP=1", [&] { s5<1><<<nsm, NTH>>>(r5, iters, out, 2); });
+    z5(); time("S5 compact 32B, direct, NREP=4", [&] { s5<4><<<nsm, NTH>>>(r5, iters, out, 2); });
+    z5(); time("S5 compact 32B, direct, NREP=8", [&] { s5<8><<<nsm, NTH>>>(r5, iters, out, 2); });
+    z5(); time("S6 96B (6x16B), direct, NREP=1", [&] { s5<1><<<nsm, NTH>>>(r5, iters, out, 6); });
+    z5(); time("S6 96B (6x16B), direct, NREP=4", [&] { s5<4><<<nsm, NTH>>>(r5, iters, out, 6); });
     return 0;
 }

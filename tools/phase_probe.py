@@ -7,7 +7,10 @@ import sys
 import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-os.environ.setdefault("SVMB200_PHASE_TIMERS", "1")
+if os.environ.get("SVMB200_PHASE_TIMERS", "1") != "0":
+    os.environ["SVMB200_PHASE_TIMERS"] = "1"
+else:
+    del os.environ["SVMB200_PHASE_TIMERS"]
 
 import torch  # noqa: E402
 
