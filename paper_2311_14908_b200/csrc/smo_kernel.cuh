@@ -136,7 +136,8 @@ struct Params {
 // phase timers (cycles, CTA 0): scalar warp lane 0 ...
 enum { PH_S_WAITC = 0, PH_S_PUBLISH, PH_S_POLL, PH_S_READ, PH_S_PIVOT, PH_S_KUL,
        // ... and consumer thread 0
-       PH_C_EXCH, PH_C_PIVOT, PH_C_DIST, PH_C_WAITB, PH_C_UPDATE, PH_C_REDUCE, PH_N };
+       PH_C_EXCH, PH_C_PIVOT, PH_C_DIST, PH_C_WAITB, PH_C_UPDATE, PH_C_REDUCE,
+       PH_S_CAND, PH_S_BUILD, PH_N };
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -284,6 +285,28 @@ __device__ __forceinline__ void warp_reduce_fi(double& f, int& i, int width = 32
     }
 }
 
+// Order-preserving 64-bit key of a double (no NaNs; -0 is keyed as +0, since the
+// selections compare f values with ==, under which -0 == +0).
+__device__ __forceinline__ unsigned long long fkey(double f) {
+    unsigned long long b = (unsigned long long)__double_as_longlong(f);
+    if (b == 0x8000000000000000ull) b = 0ull;
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double fkey_inv(unsigned long long k) {
+    return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k));
+}
+// Lexicographic minimum of (key, idx) over the lanes of `mask` (every lane of the mask
+// calls it with the same mask): three warp reductions on 32-bit halves.  The winner's
+// key and index are returned to every lane of the mask.
+__device__ __forceinline__ void argmin_redux(unsigned mask, unsigned long long key, unsigned idx,
+                                             unsigned long long& kmin, unsigned& imin) {
+    const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+    const unsigned mh = __reduce_min_sync(mask, hi);
+    const unsigned ml = __reduce_min_sync(mask, hi == mh ? lo : 0xffffffffu);
+    imin = __reduce_min_sync(mask, (hi == mh && lo == ml) ? idx : 0xffffffffu);
+    kmin = ((unsigned long long)mh << 32) | ml;
+}
+
 // (the volatile shared load forces a deferred-blocking bar.sync to resolve before
 // the clock is read)
 // A (candidate up, candidate low) pair with the alpha and label of each.
@@ -421,6 +444,11 @@ __device__ __forceinline__ bool poll_records(const uint4* w0, const uint4* w1, i
     return tmo;
 }
 
+// Word k of local row j in a CTA's resident binary block (row j at words [j Wp, j Wp + Wp)).
+__device__ __forceinline__ uint32_t bin_row_word(const float* ring, int j, int k, int W) {
+    return reinterpret_cast<const uint32_t*>(ring)[(size_t)j * ((W + 3) & ~3) + k];
+}
+
 // Row cache (a8): rank owning global row g (ranks 0..world-1 hold consecutive blocks).
 __device__ __forceinline__ int cache_owner(const Params& P, long long g) {
     int r = 0;
@@ -438,8 +466,17 @@ __device__ __forceinline__ double kcache_at(const Params& P, int s, long long g)
     return __ldcg(P.cache[r] + (long long)s * P.n_rows[r] + (g - P.row_off[r]));
 }
 
-template <int KERNEL, int RPT, bool A_SMEM>
+// BINCL: the kernel specialised for binary rows resident in a thread-block cluster (the
+// latency-bound small-problem path): the other modes compile out, so the per-iteration code
+// is short (instruction-cache resident).
+template <int KERNEL, int RPT, bool A_SMEM, bool BINCL>
 __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
+    // mode switches: compile-time constants in the BINCL specialisation
+    const bool m_cluster = BINCL || P.cluster != 0;
+    const bool m_isbin = BINCL || P.bin_words > 0;
+    const double* const m_gram = BINCL ? nullptr : P.gram;
+    const int m_cache = BINCL ? 0 : P.cache_slots;
+    const bool m_resident = BINCL || P.resident != 0;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Shared& sh = *reinterpret_cast<Shared*>(smem_raw);
     size_t off = (sizeof(Shared) + 127) & ~size_t(127);
@@ -451,20 +488,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
     off = (off + 7) & ~size_t(7);
     // binary RBF: K for every possible Hamming distance, K_tab[D] = exp_cr(-(gamma D))
     double* ktab = reinterpret_cast<double*>(smem_raw + off);
-    if (P.bin_words) off += (size_t)(32 * P.bin_words + 1) * 8;
+    if (m_isbin) off += (size_t)(32 * P.bin_words + 1) * 8;
     off = (off + 7) & ~size_t(7);
     // row-cache directory: owner (global row) of every slot + an open-addressing hash
     // row -> slot (cache_hash entries, a power of two >= 2 slots), FIFO replacement
-    int* dir_owner = reinterpret_cast<int*>(smem_raw + off); off += (size_t)P.cache_slots * 4;
+    int* dir_owner = reinterpret_cast<int*>(smem_raw + off); off += (size_t)m_cache * 4;
     off = (off + 7) & ~size_t(7);
     int2* dir_hash = reinterpret_cast<int2*>(smem_raw + off); off += (size_t)P.cache_hash * 8;
     // cache mode: the scalar warp compacts the k with a non-zero term of K(x_u, x_l) here
     off = (off + 15) & ~size_t(15);
     double2* kul_t = reinterpret_cast<double2*>(smem_raw + off);
-    if (P.cache_slots > 0) off += (size_t)P.d_pad * 16;
+    if (m_cache > 0) off += (size_t)P.d_pad * 16;
     // cluster mode: records of the rank's CTAs, cmb[parity][cta][crw] (written remotely)
     uint4* cmb = reinterpret_cast<uint4*>(smem_raw + off);
-    if (P.cluster) off += (size_t)2 * P.ctas_per_rank * P.crw * 16;
+    if (m_cluster) off += (size_t)2 * P.ctas_per_rank * P.crw * 16;
     off = (off + 127) & ~size_t(127);
     float* ring = reinterpret_cast<float*>(smem_raw + off);
     const int stage_floats = P.kc * P.rt;
@@ -492,9 +529,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     for (int e = t; e < svmexp::EXP_TABLE_DOUBLES; e += NTHREADS) sh.exp_tab[e] = svmexp::table_entry(e);
-    for (int e = t; e < P.cache_slots; e += NTHREADS) dir_owner[e] = -1;
+    for (int e = t; e < m_cache; e += NTHREADS) dir_owner[e] = -1;
     for (int e = t; e < P.cache_hash; e += NTHREADS) dir_hash[e] = make_int2(-1, -1);
-    if (P.cluster)
+    if (m_cluster)
         for (int e = t; e < 2 * P.ctas_per_rank * P.crw; e += NTHREADS) cmb[e] = make_uint4(0u, 0u, 0u, 0u);
     if (t == 0) sh.c_fifo = 0;
     for (int j = t; j < R; j += NTHREADS) {
@@ -504,33 +541,33 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
     }
     __syncthreads();
     const svmexp::PtrTab tab{sh.exp_tab};
-    if (KERNEL == 1 && P.bin_words) {
+    if (KERNEL == 1 && m_isbin) {
         for (int e = t; e <= 32 * P.bin_words; e += NTHREADS) ktab[e] = svmexp::exp_cr_t(-(P.gamma * (double)e), tab);
         __syncthreads();
     }
 
     // every CTA of the cluster has zeroed its mailbox before any record is stored into it
-    if (P.cluster) cluster_sync_all();
+    if (m_cluster) cluster_sync_all();
 
     // ============================================================ producer warp
     if (warp == PRODUCER_WARP) {
         // (cluster mode: the producer waits in the final cluster barrier, so no CTA exits
         // while a peer may still address its shared memory)
-        if (P.gram) {
+        if (m_gram) {
             if (lane == 0) { sh.issued = 0; __threadfence_block(); sh.producer_done = 1; }
-            if (P.cluster) cluster_sync_all();
+            if (m_cluster) cluster_sync_all();
             return;
         }
-        if (P.resident) {
+        if (m_resident) {
             if (lane == 0 && n_tiles > 0) {
                 const int rp = (R + 3) & ~3;
-                const uint32_t bytes = P.bin_words ? (uint32_t)(n_tiles * P.bin_words * P.rt * 4)
+                const uint32_t bytes = m_isbin ? (uint32_t)(n_tiles * ((P.bin_words + 3) & ~3) * P.rt * 4)
                                                    : (uint32_t)P.d_pad * rp * 4u;
                 mbar_arrive_tx(&full[0], bytes);
                 bulk_g2s(ring, xcta, bytes, &full[0]);
             }
             if (lane == 0) { sh.issued = 0; __threadfence_block(); sh.producer_done = 1; }
-            if (P.cluster) cluster_sync_all();
+            if (m_cluster) cluster_sync_all();
             return;
         }
         if (lane == 0 && n_tiles > 0) {
@@ -558,7 +595,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
         }
         if (lane == 0) { __threadfence_block(); sh.producer_done = 1; }
         __syncwarp();
-        if (P.cluster) cluster_sync_all();
+        if (m_cluster) cluster_sync_all();
         return;
     }
 
@@ -579,7 +616,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
     unsigned int cslot = 0, cpar = 0, consumed = 0;
     const double INF = __longlong_as_double(0x7ff0000000000000ll);
 
-    if (P.resident && !P.gram && n_tiles > 0 && !is_scalar) mbar_wait(&full[0], 0);
+    if (m_resident && !m_gram && n_tiles > 0 && !is_scalar) mbar_wait(&full[0], 0);
     // ---- initial selection from the current state (no update)
     if (!is_scalar) {
         double fu = INF, fl = -INF;
@@ -620,90 +657,137 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
             const int g_total = xworld * P.ctas_per_rank;
             const int par = (int)(seq & 1);
             const uint32_t sq = (uint32_t)seq & 0xffffu;
-            Cand c;
-            int ju, jl;                                   // this CTA's candidates (local rows)
-            {
-                double fu = lane < NWC ? sh.red_f[0][lane] : INF;
-                ju = lane < NWC ? sh.red_i[0][lane] : INT_MAX;
-                double fl = lane < NWC ? sh.red_f[1][lane] : -INF;
-                jl = lane < NWC ? sh.red_i[1][lane] : INT_MAX;
-                warp_reduce_fi<true>(fu, ju, NWC);
-                warp_reduce_fi<false>(fl, jl, NWC);
-                fu = __shfl_sync(0xffffffffu, fu, 0); ju = __shfl_sync(0xffffffffu, ju, 0);
-                fl = __shfl_sync(0xffffffffu, fl, 0); jl = __shfl_sync(0xffffffffu, jl, 0);
-                c.fu = fu; c.fl = fl;
-                c.iu = (ju == INT_MAX) ? INT_MAX : (int)(gbase + ju);
-                c.il = (jl == INT_MAX) ? INT_MAX : (int)(gbase + jl);
-                c.au = (ju == INT_MAX) ? 0.0 : (A_SMEM ? a_s[ju] : alpha_g[ju]);
-                c.al = (jl == INT_MAX) ? 0.0 : (A_SMEM ? a_s[jl] : alpha_g[jl]);
-                c.yu = (ju == INT_MAX) ? 0 : ((fl_s[ju] & FL_POS) ? 1 : -1);
-                c.yl = (jl == INT_MAX) ? 0 : ((fl_s[jl] & FL_POS) ? 1 : -1);
-            }
-            Sel best;
+            double fu, fl;
+            int iu, il, rec_u, rec_l;
             bool tmo;
-            if (P.cluster) {
-                // ---- cluster exchange: store the record (4 words + the candidates' rows)
-                // into every CTA's shared-memory mailbox of this rank's cluster, then poll the
-                // local mailbox (lane j reads the record of CTA j)
+            if (m_cluster) {
+                // ======== cluster exchange (distributed shared memory).  The two selections
+                // run side by side: lanes 0-15 handle I_up, lanes 16-31 I_low.
+                const bool lowh = lane >= 16;
+                const int hl = lane & 15;
                 const int G = P.ctas_per_rank, RW = P.crw, rw = (P.crow + 2) / 3;
-                // lane h < RW builds word h of the record and stores it into every CTA
-                if (lane < RW) {
-                    uint4 wv;
-                    if (lane < 4) {
-                        wv = rec_word(c, lane, sq);
+                // CTA candidate: reduce the 8 consumer-warp candidates of this half
+                // (low half: max f = min of the complemented key)
+                const unsigned hmask = lowh ? 0xffff0000u : 0x0000ffffu;
+                unsigned long long kv = 0xffffffffffffffffull;
+                unsigned jv = 0xffffffffu;
+                if (hl < NWC) {
+                    const unsigned long long k = fkey(sh.red_f[lowh ? 1 : 0][hl]);
+                    kv = lowh ? ~k : k;
+                    jv = (unsigned)sh.red_i[lowh ? 1 : 0][hl];
+                }
+                unsigned long long kmin;
+                unsigned jmin;
+                argmin_redux(hmask, kv, jv, kmin, jmin);
+                const unsigned long long ku_ = __shfl_sync(0xffffffffu, kmin, 0), kl_ = __shfl_sync(0xffffffffu, kmin, 16);
+                const int ju = (int)__shfl_sync(0xffffffffu, jmin, 0), jl = (int)__shfl_sync(0xffffffffu, jmin, 16);
+                const double c_fu = ju == INT_MAX ? INF : fkey_inv(ku_);
+                const double c_fl = jl == INT_MAX ? -INF : fkey_inv(~kl_);
+                SVM_PHASE(timing, PH_S_CAND);
+                // lanes h and 16 + h (h < RW) build word h of the record (branch-free)
+                if (hl < RW) {
+                    uint32_t a;
+                    unsigned long long v;
+                    if (hl < 4) {
+                        const int jj = (hl == 0 || hl == 2) ? ju : jl;
+                        const bool empty = jj == INT_MAX;
+                        const int jc = empty ? 0 : jj;
+                        const double av = A_SMEM ? a_s[jc] : alpha_g[jc];
+                        if (hl == 0) { a = empty ? 0xffffffffu : (uint32_t)(gbase + ju); v = __double_as_longlong(c_fu); }
+                        else if (hl == 1) { a = empty ? 0xffffffffu : (uint32_t)(gbase + jl); v = __double_as_longlong(c_fl); }
+                        else if (hl == 2) {
+                            const int yu_ = ju == INT_MAX ? 0 : ((fl_s[ju] & FL_POS) ? 1 : -1);
+                            const int yl_ = jl == INT_MAX ? 0 : ((fl_s[jl] & FL_POS) ? 1 : -1);
+                            a = (uint32_t)((yu_ & 0xffff) | (yl_ << 16));
+                            v = __double_as_longlong(empty ? 0.0 : av);
+                        } else { a = 0u; v = __double_as_longlong(empty ? 0.0 : av); }
                     } else {
-                        const bool is_u = (lane - 4) < rw;
-                        const int k0 = 3 * ((lane - 4) - (is_u ? 0 : rw));
+                        const bool is_u = (hl - 4) < rw;
+                        const int k0 = 3 * ((hl - 4) - (is_u ? 0 : rw));
                         const int jr = is_u ? ju : jl;
                         uint32_t e[3] = {0u, 0u, 0u};
                         if (jr != INT_MAX) {
-                            const uint32_t* base;
-                            int stride;
-                            if (P.bin_words) {
-                                const int tl = jr >> rt_log2, rin = jr & (P.rt - 1), rows_t = min(P.rt, R - (tl << rt_log2));
-                                base = reinterpret_cast<const uint32_t*>(ring) + (size_t)tl * P.bin_words * P.rt + rin;
-                                stride = (rows_t + 3) & ~3;
-                            } else {
-                                base = reinterpret_cast<const uint32_t*>(ring) + jr;
-                                stride = (R + 3) & ~3;
-                            }
 #pragma unroll
                             for (int m = 0; m < 3; ++m)
-                                if (k0 + m < P.crow) e[m] = base[(size_t)(k0 + m) * stride];
+                                if (k0 + m < P.crow) e[m] = m_isbin ? bin_row_word(ring, jr, k0 + m, P.bin_words)
+                                                                        : __float_as_uint(ring[(size_t)(k0 + m) * ((R + 3) & ~3) + jr]);
                         }
-                        wv = rec_pack(sq, e[0], (unsigned long long)e[1] | ((unsigned long long)e[2] << 32));
+                        a = e[0];
+                        v = (unsigned long long)e[1] | ((unsigned long long)e[2] << 32);
                     }
-                    const uint32_t src = smem_u32(cmb + ((size_t)par * G + cta) * RW + lane);
-                    for (int j = 0; j < G; ++j) {
+                    const uint4 wv = rec_pack(sq, a, v);
+                    if (lane == 0) SVM_PHASE(timing, PH_S_BUILD);
+                    const uint32_t src = smem_u32(cmb + ((size_t)par * G + cta) * RW + hl);
+                    const int half = (G + 1) >> 1;
+                    const int j0 = lowh ? half : 0, j1 = lowh ? G : half;
+                    for (int j = j0; j < j1; ++j) {
                         uint32_t ra;
                         asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(src), "r"(j));
                         st_cluster_v4(ra, wv);
                     }
                 }
                 SVM_PHASE(timing, PH_S_PUBLISH);
-                // lane j < G polls words 0/1 (the candidates) of CTA j's record
-                best.fu = INF; best.fl = -INF; best.iu = INT_MAX; best.il = INT_MAX; best.gu = 0; best.gl = 0;
+                // lane hl < G polls word 0 (lanes 0-15) or word 1 (lanes 16-31) of CTA hl's record
+                double pf = lowh ? -INF : INF;
+                int pi = INT_MAX;
                 bool to = false;
-                if (lane < G) {
-                    const uint4* r = cmb + ((size_t)par * G + lane) * RW;
+                if (hl < G) {
+                    const uint4* r = cmb + ((size_t)par * G + hl) * RW + (lowh ? 1 : 0);
                     long long t0 = 0;
                     unsigned int spins = 0;
-                    uint4 w0, w1;
+                    uint4 w;
                     for (;;) {
-                        w0 = ld_volatile_shared_v4(r);
-                        w1 = ld_volatile_shared_v4(r + 1);
-                        if (rec_ok(w0, sq) && rec_ok(w1, sq)) break;
+                        w = ld_volatile_shared_v4(r);
+                        if (rec_ok(w, sq)) break;
                         if ((++spins & 255u) == 0) {
                             const long long now = globaltimer();
                             if (t0 == 0) t0 = now;
                             else if (now - t0 > P.timeout_ns) { to = true; break; }
                         }
                     }
-                    best.iu = rec_idx(w0); best.fu = best.iu == INT_MAX ? INF : rec_f64(w0); best.gu = lane;
-                    best.il = rec_idx(w1); best.fl = best.il == INT_MAX ? -INF : rec_f64(w1); best.gl = lane;
+                    pi = rec_idx(w);
+                    if (pi != INT_MAX) pf = rec_f64(w);
                 }
                 tmo = __any_sync(0xffffffffu, to) || sh.timeout != 0;
+                SVM_PHASE(timing, PH_S_POLL);
+                {
+                    const unsigned long long k0 = fkey(pf);
+                    const unsigned long long kk = lowh ? ~k0 : k0;
+                    unsigned long long kw;
+                    unsigned iw;
+                    argmin_redux(hmask, kk, (unsigned)pi, kw, iw);
+                    // the record each winner came from: the lane of its half holding it
+                    const unsigned hit = __ballot_sync(0xffffffffu, (unsigned)pi == iw && kk == kw);
+                    const unsigned hu = hit & 0xffffu, hlw = hit >> 16;
+                    iu = (int)__shfl_sync(0xffffffffu, iw, 0);
+                    il = (int)__shfl_sync(0xffffffffu, iw, 16);
+                    const unsigned long long kwu = __shfl_sync(0xffffffffu, kw, 0), kwl = __shfl_sync(0xffffffffu, kw, 16);
+                    fu = iu == INT_MAX ? INF : fkey_inv(kwu);
+                    fl = il == INT_MAX ? -INF : fkey_inv(~kwl);
+                    rec_u = hu ? __ffs(hu) - 1 : 0;
+                    rec_l = hlw ? __ffs(hlw) - 1 : 0;
+                }
             } else {
+                Cand c;
+                int ju, jl;                                   // this CTA's candidates (local rows)
+                {
+                    double fu = lane < NWC ? sh.red_f[0][lane] : INF;
+                    ju = lane < NWC ? sh.red_i[0][lane] : INT_MAX;
+                    double fl = lane < NWC ? sh.red_f[1][lane] : -INF;
+                    jl = lane < NWC ? sh.red_i[1][lane] : INT_MAX;
+                    warp_reduce_fi<true>(fu, ju, NWC);
+                    warp_reduce_fi<false>(fl, jl, NWC);
+                    fu = __shfl_sync(0xffffffffu, fu, 0); ju = __shfl_sync(0xffffffffu, ju, 0);
+                    fl = __shfl_sync(0xffffffffu, fl, 0); jl = __shfl_sync(0xffffffffu, jl, 0);
+                    c.fu = fu; c.fl = fl;
+                    c.iu = (ju == INT_MAX) ? INT_MAX : (int)(gbase + ju);
+                    c.il = (jl == INT_MAX) ? INT_MAX : (int)(gbase + jl);
+                    c.au = (ju == INT_MAX) ? 0.0 : (A_SMEM ? a_s[ju] : alpha_g[ju]);
+                    c.al = (jl == INT_MAX) ? 0.0 : (A_SMEM ? a_s[jl] : alpha_g[jl]);
+                    c.yu = (ju == INT_MAX) ? 0 : ((fl_s[ju] & FL_POS) ? 1 : -1);
+                    c.yl = (jl == INT_MAX) ? 0 : ((fl_s[jl] & FL_POS) ? 1 : -1);
+                }
+                Sel best;
                 const int gcta = (rank - xbase) * P.ctas_per_rank + cta;
                 if (lane < 4 * xworld)
                     rec_store(mbox_words(P.mbox[xbase + (lane >> 2)], par, lane & 3, g_total) + gcta,
@@ -715,17 +799,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                                        g_total, sq, P.sys_scope, P.timeout_ns, lane, best, rounds) ||
                       sh.timeout != 0;
                 if (timing) ph_acc[PH_C_PIVOT] += rounds;     // (timers only) poll rounds of lane 0
+                SVM_PHASE(timing, PH_S_POLL);
+                // the warp's winners and the records they came from
+                fu = best.fu; fl = best.fl;
+                iu = best.iu; il = best.il;
+                warp_reduce_fi<true>(fu, iu);
+                warp_reduce_fi<false>(fl, il);
+                const unsigned mu = __ballot_sync(0xffffffffu, best.iu == iu);
+                const unsigned ml = __ballot_sync(0xffffffffu, best.il == il);
+                rec_u = __shfl_sync(0xffffffffu, best.gu, mu ? __ffs(mu) - 1 : 0);
+                rec_l = __shfl_sync(0xffffffffu, best.gl, ml ? __ffs(ml) - 1 : 0);
             }
-            SVM_PHASE(timing, PH_S_POLL);
-            // the warp's winners and the records they came from
-            double fu = best.fu, fl = best.fl;
-            int iu = best.iu, il = best.il;
-            warp_reduce_fi<true>(fu, iu);
-            warp_reduce_fi<false>(fl, il);
-            const unsigned mu = __ballot_sync(0xffffffffu, best.iu == iu);
-            const unsigned ml = __ballot_sync(0xffffffffu, best.il == il);
-            const int rec_u = __shfl_sync(0xffffffffu, best.gu, mu ? __ffs(mu) - 1 : 0);
-            const int rec_l = __shfl_sync(0xffffffffu, best.gl, ml ? __ffs(ml) - 1 : 0);
             int dec = ST_RUNNING;
             if (tmo) dec = ST_TIMEOUT;
             else if (iu == INT_MAX || il == INT_MAX) dec = ST_CONVERGED;
@@ -745,7 +829,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
             // ---- row cache (a8): every CTA runs the same directory operations on the same
             // pair sequence (hash lookup, FIFO replacement), so every CTA agrees
             int c_hit = 0, su = -1, sl = -1;
-            if (P.cache_slots > 0) {
+            if (m_cache > 0) {
                 if (lane == 0) {
                     const int hm = P.cache_hash - 1;
                     auto hslot = [&](int key) { return (int)(((unsigned)key * 2654435761u) >> 7) & hm; };
@@ -778,8 +862,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                     };
                     auto victim = [&](int avoid) {
                         int v = sh.c_fifo;
-                        if (v == avoid) v = (v + 1) % P.cache_slots;
-                        sh.c_fifo = (v + 1) % P.cache_slots;
+                        if (v == avoid) v = (v + 1) % m_cache;
+                        sh.c_fifo = (v + 1) % m_cache;
                         if (dir_owner[v] >= 0) erase(dir_owner[v]);
                         return v;
                     };
@@ -802,7 +886,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
             // trail the candidate words)
             const int rwc = (P.crow + 2) / 3;
             const uint4* wp;
-            if (P.cluster) {
+            if (m_cluster) {
                 int rr, hh;
                 if (lane < 3) { rr = lane == 0 ? rec_u : rec_l; hh = lane == 2 ? 3 : 2; }
                 else if (lane < 3 + rwc) { rr = rec_u; hh = 4 + (lane - 3); }
@@ -812,8 +896,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                 wp = mbox_words(my_mb, par, lane == 2 ? 3 : 2, g_total) + (lane == 0 ? rec_u : rec_l);
             }
             uint4 wa = make_uint4(0u, 0u, 0u, 0u);
-            if (P.cluster) {
-                if (lane < 3 + (P.gram || c_hit ? 0 : 2 * rwc)) {
+            if (m_cluster) {
+                if (lane < 3 + (m_gram || c_hit ? 0 : 2 * rwc)) {
                     wa = ld_volatile_shared_v4(wp);
                     unsigned int spins = 0;
                     while (!rec_ok(wa, sq)) {
@@ -825,13 +909,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                 wa = rec_load(wp, P.sys_scope);
             }
             // ---- pivot rows x_up, x_low into shared memory (fp64, or bit rows)
-            if (P.gram || c_hit) {
+            if (m_gram || c_hit) {
                 // rows of K are read directly (Gram or cached rows; K_ul from the cached row
                 // of u); no pivot rows needed
-            } else if (P.cluster && P.crow) {
+            } else if (m_cluster && P.crow) {
                 // the winners' rows travelled in their records (lanes 3.. hold the words)
-                const int nu = P.bin_words ? P.bin_words : P.d;
-                for (int k0 = 0; k0 < (P.bin_words ? 32 : P.d_pad); k0 += 32) {
+                const int nu = m_isbin ? P.bin_words : P.d;
+                for (int k0 = 0; k0 < (m_isbin ? 32 : P.d_pad); k0 += 32) {
                     const int k = k0 + lane;
                     const int kk = k < nu ? k : 0;
                     const int src_u = 3 + kk / 3, src_l = 3 + rwc + kk / 3, m = kk % 3;
@@ -841,19 +925,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                                    vl_w = __shfl_sync(0xffffffffu, wa.w, src_l);
                     const uint32_t xu = m == 0 ? vu_y : (m == 1 ? vu_z : vu_w);
                     const uint32_t xl = m == 0 ? vl_y : (m == 1 ? vl_z : vl_w);
-                    if (P.bin_words) {
+                    if (m_isbin) {
                         uint32_t* pw = reinterpret_cast<uint32_t*>(piv);
-                        if (k < nu) { pw[k] = xu; pw[P.bin_words + k] = xl; }
+                        const int Wp = (P.bin_words + 3) & ~3;
+                        if (k < Wp) { pw[k] = k < nu ? xu : 0u; pw[Wp + k] = k < nu ? xl : 0u; }
                     } else if (k < P.d_pad) {
                         piv[k] = k < nu ? make_double2((double)__uint_as_float(xu), (double)__uint_as_float(xl))
                                         : make_double2(0.0, 0.0);
                     }
                 }
-            } else if (P.bin_words) {
+            } else if (m_isbin) {
                 uint32_t* pw = reinterpret_cast<uint32_t*>(piv);
-                if (lane < 2 * P.bin_words) {
-                    const int w = lane % P.bin_words;
-                    pw[lane] = __ldg(&P.xrbits[(long long)(lane < P.bin_words ? iu : il) * P.bin_words + w]);
+                const int Wp = (P.bin_words + 3) & ~3;
+                if (lane < 2 * Wp) {
+                    const int w = lane < Wp ? lane : lane - Wp;
+                    pw[lane] = w < P.bin_words ? __ldg(&P.xrbits[(long long)(lane < Wp ? iu : il) * P.bin_words + w]) : 0u;
                 }
             } else {
                 const float* xu_g = xr + (long long)iu * P.d;
@@ -876,7 +962,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
             if (lane == 0) { sh.decision = ST_RUNNING; sh.u = iu; sh.l = il; }
             __syncwarp();
             named_arrive(BAR_A);
-            if (lane < 3 && !P.cluster) {
+            if (lane < 3 && !m_cluster) {
                 unsigned int spins = 0;
                 while (!rec_ok(wa, sq)) {            // written with w0/w1: (almost) never taken
                     wa = rec_load(wp, P.sys_scope);
@@ -889,7 +975,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
             const double al = __hiloint2double((int)__shfl_sync(0xffffffffu, wa.w, 2), (int)__shfl_sync(0xffffffffu, wa.z, 2));
             SVM_PHASE(timing, PH_S_PIVOT);
             const int u = iu, l = il;
-            if (P.cache_slots > 0 && !c_hit) {
+            if (m_cache > 0 && !c_hit) {
                 // compact the non-zero terms of K(x_u, x_l) (RBF: x_u - x_l; linear: pairs
                 // with x_u or x_l non-zero) in ascending k
                 int cnt = 0;
@@ -912,16 +998,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
         // ---- pair update (a2): eta, clipped step, snapped alphas (lane 0)
             if (lane == 0) {
                 double Kuu, Kll, Kul;
-                if (P.gram) {
+                if (m_gram) {
                     const long long n = P.n_global;
-                    Kuu = __ldg(&P.gram[(long long)u * n + u]);
-                    Kll = __ldg(&P.gram[(long long)l * n + l]);
-                    Kul = __ldg(&P.gram[(long long)u * n + l]);
-                } else if (P.bin_words) {
+                    Kuu = __ldg(&m_gram[(long long)u * n + u]);
+                    Kll = __ldg(&m_gram[(long long)l * n + l]);
+                    Kul = __ldg(&m_gram[(long long)u * n + l]);
+                } else if (m_isbin) {
                     const uint32_t* pw = reinterpret_cast<const uint32_t*>(piv);
                     int cuu = 0, cll = 0, cul = 0, cx = 0;
+                    const int Wp = (P.bin_words + 3) & ~3;
                     for (int w = 0; w < P.bin_words; ++w) {
-                        const uint32_t a = pw[w], bb = pw[P.bin_words + w];
+                        const uint32_t a = pw[w], bb = pw[Wp + w];
                         cuu += __popc(a); cll += __popc(bb); cul += __popc(a & bb); cx += __popc(a ^ bb);
                     }
                     if (KERNEL == 1) {
@@ -937,7 +1024,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                     Kul = kcache_at(P, su, l);
                     if (KERNEL == 1) { Kuu = 1.0; Kll = 1.0; }
                     else { Kuu = kcache_at(P, su, u); Kll = kcache_at(P, sl, l); }
-                } else if (P.cache_slots > 0) {
+                } else if (m_cache > 0) {
                     // only k with a non-zero term change the sums (fma(0, x, acc) == acc), so
                     // the serial chains run over the compacted non-zero terms (ascending k)
                     const int cnt = sh.kul_cnt;
@@ -1007,17 +1094,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
         }
         // ================= consumers: row pass (a3-a5)
         const int u = sh.u, l = sh.l;
-        const bool c_hit = P.cache_slots > 0 && sh.c_hit;
+        const bool c_hit = m_cache > 0 && sh.c_hit;
         const int su = sh.c_su, sl = sh.c_sl;
-        bool rows_ready = P.gram != nullptr;
+        bool rows_ready = m_gram != nullptr;
         const double* krow_u = nullptr;
         const double* krow_l = nullptr;
         double* fill_u = nullptr;
         double* fill_l = nullptr;
-        if (P.gram) {
-            krow_u = P.gram + (long long)u * P.n_global + gbase;
-            krow_l = P.gram + (long long)l * P.n_global + gbase;
-        } else if (P.cache_slots > 0) {
+        if (m_gram) {
+            krow_u = m_gram + (long long)u * P.n_global + gbase;
+            krow_l = m_gram + (long long)l * P.n_global + gbase;
+        } else if (m_cache > 0) {
             double* cb = P.cache[rank] + r0;                  // this CTA's columns of every slot
             const long long stride = P.n_rows[rank];
             if (c_hit) {
@@ -1030,40 +1117,40 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
         double bfu = INF, bfl = -INF;
         int bju = INT_MAX, bjl = INT_MAX;
         if (n_tiles == 0) named_sync(BAR_B);
-        if (P.bin_words && !rows_ready && n_tiles > 0) {
-            // binary bit rows resident ([tile][word][row]); thread t owns row t of every tile.
-            // The popcounts of BT tiles are independent chains computed together, then the
-            // rows are updated after barrier B.
+        if (m_isbin && !rows_ready && n_tiles > 0) {
+            // binary bit rows resident (row j at words [j Wp, j Wp + Wp), Wp = W rounded up to 4);
+            // thread t owns row t of every tile.  The popcounts of BT tiles are independent
+            // chains computed together (16-byte loads), then the rows are updated after
+            // barrier B.
             constexpr int BT = 8;
-            const int lu_loc = (u >= gbase && u < gbase + R) ? (int)(u - gbase) : -1;
-            const int ll_loc = (l >= gbase && l < gbase + R) ? (int)(l - gbase) : -1;
             const uint32_t* pw = reinterpret_cast<const uint32_t*>(piv);
-            const uint32_t* xb0 = reinterpret_cast<const uint32_t*>(ring);
             const int W = P.bin_words;
+            const int Wq = (W + 3) >> 2;                  // 16-byte groups per row
+            const uint4* x4 = reinterpret_cast<const uint4*>(ring);
+            const uint4* p4 = reinterpret_cast<const uint4*>(pw);
             for (int tb = 0; tb < n_tiles; tb += BT) {
                 // all loads of a batch are unconditional (clamped to a valid row), so they
                 // issue back to back; rows past the end are computed and discarded
-                const uint32_t* xq[BT];
-                int rq[BT];
+                int jq[BT];
 #pragma unroll
-                for (int q = 0; q < BT; ++q) {
-                    const int tile = min(tb + q, n_tiles - 1);
-                    const int rows_t = min(P.rt, R - tile * P.rt);
-                    rq[q] = (rows_t + 3) & ~3;
-                    xq[q] = xb0 + (size_t)tile * W * P.rt + min(t, rows_t - 1);
-                }
+                for (int q = 0; q < BT; ++q) jq[q] = min((tb + q) * P.rt + t, R - 1);
                 int cu_[BT], cl_[BT];
 #pragma unroll
                 for (int q = 0; q < BT; ++q) { cu_[q] = 0; cl_[q] = 0; }
-                for (int w = 0; w < W; ++w) {
-                    const uint32_t pu = pw[w], pl = pw[W + w];
-                    uint32_t xv[BT];
+                for (int w4 = 0; w4 < Wq; ++w4) {
+                    const uint4 pu = p4[w4], pl = p4[Wq + w4];
+                    uint4 xv[BT];
 #pragma unroll
-                    for (int q = 0; q < BT; ++q) xv[q] = xq[q][(size_t)w * rq[q]];
+                    for (int q = 0; q < BT; ++q) xv[q] = x4[jq[q] * Wq + w4];
 #pragma unroll
                     for (int q = 0; q < BT; ++q) {
-                        if (KERNEL == 1) { cu_[q] += __popc(xv[q] ^ pu); cl_[q] += __popc(xv[q] ^ pl); }
-                        else { cu_[q] += __popc(xv[q] & pu); cl_[q] += __popc(xv[q] & pl); }
+                        if (KERNEL == 1) {
+                            cu_[q] += __popc(xv[q].x ^ pu.x) + __popc(xv[q].y ^ pu.y) + __popc(xv[q].z ^ pu.z) + __popc(xv[q].w ^ pu.w);
+                            cl_[q] += __popc(xv[q].x ^ pl.x) + __popc(xv[q].y ^ pl.y) + __popc(xv[q].z ^ pl.z) + __popc(xv[q].w ^ pl.w);
+                        } else {
+                            cu_[q] += __popc(xv[q].x & pu.x) + __popc(xv[q].y & pu.y) + __popc(xv[q].z & pu.z) + __popc(xv[q].w & pu.w);
+                            cl_[q] += __popc(xv[q].x & pl.x) + __popc(xv[q].y & pl.y) + __popc(xv[q].z & pl.z) + __popc(xv[q].w & pl.w);
+                        }
                     }
                 }
                 if (tb == 0) {
@@ -1086,21 +1173,31 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                     fo[q] = f_s[j];
                     gq[q] = fl_s[j];
                 }
+                // (RBF: K(x_j, x_j) = ktab[0] = 1 already, R16)
+                double cfu[BT], cfl[BT];
+                int cju[BT], cjl[BT];
 #pragma unroll
                 for (int q = 0; q < BT; ++q) {
                     const int j = (tb + q) * P.rt + t;
+                    cfu[q] = INF; cfl[q] = -INF; cju[q] = j; cjl[q] = j;
                     if (tb + q < n_tiles && j < R) {
-                        if (KERNEL == 1) {
-                            if (j == lu_loc) ku[q] = 1.0;
-                            if (j == ll_loc) kl[q] = 1.0;
-                        }
                         const double fj = fma(cl, kl[q], fma(cu, ku[q], fo[q]));
                         f_s[j] = fj;
-                        // this thread visits its rows in increasing j: a tie keeps the earlier
-                        if ((gq[q] & FL_UP) && fj < bfu) { bfu = fj; bju = j; }
-                        if ((gq[q] & FL_LOW) && fj > bfl) { bfl = fj; bjl = j; }
+                        if (gq[q] & FL_UP) cfu[q] = fj;
+                        if (gq[q] & FL_LOW) cfl[q] = fj;
                     }
                 }
+                // tree over the batch (rows increase with q: on equal f the lower q wins),
+                // then against the running best (earlier rows: a tie keeps it)
+#pragma unroll
+                for (int s2 = 1; s2 < BT; s2 <<= 1)
+#pragma unroll
+                    for (int q = 0; q + s2 < BT; q += 2 * s2) {
+                        if (cfu[q + s2] < cfu[q]) { cfu[q] = cfu[q + s2]; cju[q] = cju[q + s2]; }
+                        if (cfl[q + s2] > cfl[q]) { cfl[q] = cfl[q + s2]; cjl[q] = cjl[q + s2]; }
+                    }
+                if (cfu[0] < bfu) { bfu = cfu[0]; bju = cju[0]; }
+                if (cfl[0] > bfl) { bfl = cfl[0]; bjl = cjl[0]; }
             }
         } else
         for (int tile = 0; tile < n_tiles; ++tile) {
@@ -1120,23 +1217,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                         if (tile * P.rt + t * RPT + q < R) { du[q] = __ldcg(&ku_row[q]); dl[q] = __ldcg(&kl_row[q]); }
                     }
                 }
-            } else if (P.bin_words) {
-                if (active) {
-                    // bit rows resident in shared memory: [tile][word][row], popcounts
-                    const uint32_t* xb = reinterpret_cast<const uint32_t*>(ring) + (size_t)tile * P.bin_words * P.rt + t;
-                    const uint32_t* pw = reinterpret_cast<const uint32_t*>(piv);
-                    int cu_ = 0, cl_ = 0;
-                    for (int w = 0; w < P.bin_words; ++w) {
-                        const uint32_t xv = xb[(size_t)w * rp];
-                        if (KERNEL == 1) { cu_ += __popc(xv ^ pw[w]); cl_ += __popc(xv ^ pw[P.bin_words + w]); }
-                        else { cu_ += __popc(xv & pw[w]); cl_ += __popc(xv & pw[P.bin_words + w]); }
-                    }
-                    du[0] = (double)cu_; dl[0] = (double)cl_;
-                }
             }
-            for (int ch = 0; ch < ((P.bin_words || rows_ready) ? 0 : P.n_chunks); ++ch) {
-                if (!P.resident) mbar_wait(&full[cslot], cpar);
-                const float* st = P.resident ? ring + (size_t)ch * P.kc * rp : ring + (size_t)cslot * stage_floats;
+            for (int ch = 0; ch < ((m_isbin || rows_ready) ? 0 : P.n_chunks); ++ch) {
+                if (!m_resident) mbar_wait(&full[cslot], cpar);
+                const float* st = m_resident ? ring + (size_t)ch * P.kc * rp : ring + (size_t)cslot * stage_floats;
                 const int k0 = ch * P.kc;
                 if (active) {
                     if (RPT == 4) {
@@ -1194,7 +1278,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                     }
                 }
                 __syncwarp();
-                if (!P.resident) {
+                if (!m_resident) {
                     if (lane == 0) mbar_arrive(&empty[cslot]);
                     ++consumed;
                     if (++cslot == (unsigned)P.stages) { cslot = 0; cpar ^= 1u; }
@@ -1205,7 +1289,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                 named_sync(BAR_B);          // c_u, c_l, the owner's flags and the fill slots are ready
                 SVM_PHASE(timing, PH_C_WAITB);
                 cu = sh.cu; cl = sh.cl;
-                if (P.cache_slots > 0 && !c_hit) {
+                if (m_cache > 0 && !c_hit) {
                     double* cb = P.cache[rank] + r0;
                     const long long stride = P.n_rows[rank];
                     if (sh.c_fill_u >= 0) fill_u = cb + sh.c_fill_u * stride;
@@ -1221,9 +1305,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                         double ku, kl;
                         if (rows_ready) {
                             ku = du[q]; kl = dl[q];
-                        } else if (KERNEL == 1 && P.bin_words) {
-                            ku = (jg == u) ? 1.0 : ktab[(int)du[q]];
-                            kl = (jg == l) ? 1.0 : ktab[(int)dl[q]];
                         } else if (KERNEL == 1) {
                             ku = (jg == u) ? 1.0 : svmexp::exp_cr_t(-(P.gamma * du[q]), tab);
                             kl = (jg == l) ? 1.0 : svmexp::exp_cr_t(-(P.gamma * dl[q]), tab);
@@ -1245,8 +1326,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
         // iterations: order them before this CTA's next record
         if (fill_u || fill_l) __threadfence();
         SVM_PHASE(timing, PH_C_UPDATE);
-        warp_reduce_fi<true>(bfu, bju);
-        warp_reduce_fi<false>(bfl, bjl);
+        {
+            unsigned long long kw;
+            unsigned iw;
+            argmin_redux(0xffffffffu, fkey(bfu), (unsigned)bju, kw, iw);
+            bju = (int)iw;
+            bfu = bju == INT_MAX ? INF : fkey_inv(kw);
+            argmin_redux(0xffffffffu, ~fkey(bfl), (unsigned)bjl, kw, iw);
+            bjl = (int)iw;
+            bfl = bjl == INT_MAX ? -INF : fkey_inv(~kw);
+        }
         if (lane == 0) {
             sh.red_f[0][warp] = bfu; sh.red_i[0][warp] = bju;
             sh.red_f[1][warp] = bfl; sh.red_i[1][warp] = bjl;
@@ -1291,7 +1380,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
         ctl->i_low = sh.l == INT_MAX ? -1 : sh.l;
     }
     __syncwarp();
-    if (P.cluster) cluster_sync_all();
+    if (m_cluster) cluster_sync_all();
 }
 
 }  // namespace svmk

@@ -79,19 +79,17 @@ __global__ void k_pack_bits(const float* __restrict__ X, long long n, int d, int
     }
 }
 
-// CTA-blocked bit layout of one rank's rows: xb[c*cta_stride + tile*W*rt + w*rp + rin]
-__global__ void k_build_xbits(const uint32_t* __restrict__ bits, long long n_r, int W, int G, int rt,
+// CTA-blocked bit layout of one rank's rows: row j of CTA c at xb[c*cta_stride + j*Wp ..],
+// Wp = W rounded up to 4 (zero padded), so a consumer thread reads a row with 16-byte loads
+__global__ void k_build_xbits(const uint32_t* __restrict__ bits, long long n_r, int W, int Wp, int G,
                               long long cta_stride, uint32_t* __restrict__ xb) {
     const int c = blockIdx.y;
     const long long r0 = (n_r * c) / G, r1 = (n_r * (c + 1)) / G;
     const long long R = r1 - r0;
-    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < R * W; e += (long long)gridDim.x * blockDim.x) {
-        const long long j = e / W;
-        const int w = (int)(e - j * W);
-        const long long tile = j / rt, rin = j - tile * rt;
-        const long long rows_t = (R - tile * rt) < rt ? (R - tile * rt) : rt;
-        const long long rp = (rows_t + 3) & ~3ll;
-        xb[(long long)c * cta_stride + tile * (long long)W * rt + w * rp + rin] = bits[(r0 + j) * W + w];
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < R * Wp; e += (long long)gridDim.x * blockDim.x) {
+        const long long j = e / Wp;
+        const int w = (int)(e - j * Wp);
+        xb[(long long)c * cta_stride + e] = w < W ? bits[(r0 + j) * W + w] : 0u;
     }
 }
 
@@ -209,7 +207,7 @@ int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl, bool bina
         pl.d_pad = pl.bin_words * 32;                      // pivot region sizing only
         pl.n_chunks = 0;
         const int n_tiles = (pl.state_cap + pl.rt - 1) / pl.rt;
-        pl.cta_stride = (long long)n_tiles * pl.bin_words * pl.rt;
+        pl.cta_stride = (long long)n_tiles * ((pl.bin_words + 3) & ~3) * pl.rt;
         pl.alpha_smem = pl.state_cap <= 2048;
         size_t fixed = (sizeof(Shared) + 127) & ~size_t(127);
         fixed += 2 * (size_t)pl.d_pad * 8 + (size_t)pl.state_cap * (pl.alpha_smem ? 17 : 9);
@@ -273,11 +271,16 @@ typedef void (*KernelFn)(const Params);
 
 template <int K>
 KernelFn pick_rpt(int rpt, bool a_smem) {
-    if (a_smem) return rpt == 4 ? smo_persistent<K, 4, true> : rpt == 2 ? smo_persistent<K, 2, true> : smo_persistent<K, 1, true>;
-    return rpt == 4 ? smo_persistent<K, 4, false> : rpt == 2 ? smo_persistent<K, 2, false> : smo_persistent<K, 1, false>;
+    if (a_smem) return rpt == 4 ? smo_persistent<K, 4, true, false> : rpt == 2 ? smo_persistent<K, 2, true, false> : smo_persistent<K, 1, true, false>;
+    return rpt == 4 ? smo_persistent<K, 4, false, false> : rpt == 2 ? smo_persistent<K, 2, false, false> : smo_persistent<K, 1, false, false>;
 }
 
-KernelFn pick_kernel(int kernel, int rpt, bool a_smem) {
+// bincl: binary rows resident in a cluster (the specialised kernel; rpt is 1 there)
+KernelFn pick_kernel(int kernel, int rpt, bool a_smem, bool bincl = false) {
+    if (bincl && getenv("SVMB200_NO_SPECIALISE") == nullptr) {
+        if (kernel == SVM_RBF) return a_smem ? smo_persistent<1, 1, true, true> : smo_persistent<1, 1, false, true>;
+        return a_smem ? smo_persistent<0, 1, true, true> : smo_persistent<0, 1, false, true>;
+    }
     return kernel == SVM_RBF ? pick_rpt<1>(rpt, a_smem) : pick_rpt<0>(rpt, a_smem);
 }
 
@@ -392,7 +395,7 @@ int solve(SolveArgs& a) {
                 continue;
             }
             if (!pc.resident) continue;
-            KernelFn f2 = pick_kernel(p.kernel, pc.rpt, pc.alpha_smem);
+            KernelFn f2 = pick_kernel(p.kernel, pc.rpt, pc.alpha_smem, binary);
             CKR(cudaFuncSetAttribute((const void*)f2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pc.smem));
             if (gc > 8) CKR(cudaFuncSetAttribute((const void*)f2, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
             cudaLaunchConfig_t cfg = {};
@@ -414,7 +417,7 @@ int solve(SolveArgs& a) {
         if (a.p.cluster > 0 && pl.cluster == 0)
             return fail(SVM_EINVAL, "cluster mode needs every rank's rows resident in the cluster's shared memory");
     }
-    KernelFn fn = pick_kernel(p.kernel, pl.rpt, pl.alpha_smem);
+    KernelFn fn = pick_kernel(p.kernel, pl.rpt, pl.alpha_smem, pl.cluster > 0 && pl.bin_words > 0);
     CKR(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
     if (pl.cluster > 8) CKR(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     int per_sm = 0;
@@ -493,8 +496,9 @@ int solve(SolveArgs& a) {
                 P.xrbits = xrb;
             }
             counted(2);   // build + init_state below
-            k_build_xbits<<<bg, 256, 0, st>>>(P.xrbits + a.row_off[r] * pl.bin_words, nr, pl.bin_words, pl.G,
-                                               pl.rt, pl.cta_stride, reinterpret_cast<uint32_t*>(xb));
+            k_build_xbits<<<bg, 256, 0, st>>>(P.xrbits + a.row_off[r] * pl.bin_words, nr, pl.bin_words,
+                                               (pl.bin_words + 3) & ~3, pl.G, pl.cta_stride,
+                                               reinterpret_cast<uint32_t*>(xb));
         } else {
             counted(2);   // build + init_state below
             k_build_xblk<<<bg, 256, 0, st>>>(a.x_rank[r], nr, (int)a.d, pl.d_pad, pl.G, pl.rt, pl.cta_stride, xb);
@@ -600,7 +604,8 @@ int solve(SolveArgs& a) {
         CKR(cudaMemcpyAsync(tm, P.timers, sizeof(tm), cudaMemcpyDeviceToHost, st));
         CKR(cudaStreamSynchronize(st));
         const char* nm[PH_N] = {"S.waitC", "S.publish", "S.poll", "S.select", "S.pivot", "S.kul",
-                                "C.waitA", "S.pollrounds", "C.dist", "C.waitB", "C.update", "C.reduce"};
+                                "C.waitA", "S.pollrounds", "C.dist", "C.waitB", "C.update", "C.reduce",
+                                "S.cand", "S.build"};
         fprintf(stderr, "[svmb200] cycles/iter of CTA 0 over %lld iters (rpt=%d kc=%d stages=%d smem=%zu a_smem=%d resident=%d bin_words=%d cache=%d gram=%d cluster=%d):",
                 hc.it, pl.rpt, pl.kc, pl.stages, pl.smem, (int)pl.alpha_smem, (int)pl.resident, pl.bin_words,
                 pl.cache_slots, gram ? 1 : 0, pl.cluster);
