@@ -18,7 +18,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libsvmb200.so")
 SOURCES = ["svmb200.cu", "predict.cu", "comm.cu", "gram.cu"]
-HEADERS = ["smo_kernel.cuh", "svm_exp.cuh", "exp_table.inc", "svm_internal.h", "predict_tc.cuh"]
+HEADERS = ["smo_kernel.cuh", "smo_bincl.cuh", "svm_exp.cuh", "exp_table.inc", "svm_internal.h", "predict_tc.cuh"]
 
 
 def _nccl_paths():

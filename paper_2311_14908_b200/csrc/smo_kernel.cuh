@@ -131,6 +131,7 @@ struct Params {
                                    // its record (binary: bin_words, else d), 0 = rows gathered
     int crw;                       // cluster mode: 16-byte words per record (4 + 2 ceil(crow/3))
     unsigned long long* timers;    // optional [8] per-phase cycle totals of CTA 0
+    int poll_ns;                   // > 0: back-off between mailbox polls (tuning)
 };
 
 // phase timers (cycles, CTA 0): scalar warp lane 0 ...

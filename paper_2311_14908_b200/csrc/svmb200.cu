@@ -19,6 +19,7 @@
 
 #include "../../include/svmb200.h"
 #include "smo_kernel.cuh"
+#include "smo_bincl.cuh"
 #include "svm_internal.h"
 
 using namespace svmk;
@@ -173,6 +174,7 @@ struct Plan {
     int cache_slots = 0;
     int cache_hash = 0;
     int cluster = 0;  // > 0: cluster mode with G CTAs per cluster (one cluster per rank)
+    bool bincl = false;  // cluster mode on binary rows: the smo_bincl kernel (NTB threads)
     int crow = 0, crw = 0;
     long long cta_stride = 0;
     size_t smem = 0;
@@ -274,6 +276,8 @@ KernelFn pick_rpt(int rpt, bool a_smem) {
     if (a_smem) return rpt == 4 ? smo_persistent<K, 4, true, false> : rpt == 2 ? smo_persistent<K, 2, true, false> : smo_persistent<K, 1, true, false>;
     return rpt == 4 ? smo_persistent<K, 4, false, false> : rpt == 2 ? smo_persistent<K, 2, false, false> : smo_persistent<K, 1, false, false>;
 }
+
+KernelFn pick_bincl(int kernel) { return kernel == SVM_RBF ? smo_bincl<1> : smo_bincl<0>; }
 
 // bincl: binary rows resident in a cluster (the specialised kernel; rpt is 1 there)
 KernelFn pick_kernel(int kernel, int rpt, bool a_smem, bool bincl = false) {
@@ -395,14 +399,20 @@ int solve(SolveArgs& a) {
                 continue;
             }
             if (!pc.resident) continue;
-            KernelFn f2 = pick_kernel(p.kernel, pc.rpt, pc.alpha_smem, binary);
+            // binary rows of <= 256 features: the dedicated latency-path kernel
+            if (binary && pc.bin_words <= BINCL_MAXW && getenv("SVMB200_NO_BINCL") == nullptr) {
+                pc.bincl = true;
+                pc.smem = bincl_smem_bytes(pc.state_cap, pc.bin_words, gc, crw);
+                if (pc.smem > (size_t)a.max_smem) continue;
+            }
+            KernelFn f2 = pc.bincl ? pick_bincl(p.kernel) : pick_kernel(p.kernel, pc.rpt, pc.alpha_smem, binary);
             CKR(cudaFuncSetAttribute((const void*)f2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pc.smem));
             if (gc > 8) CKR(cudaFuncSetAttribute((const void*)f2, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
             cudaLaunchConfig_t cfg = {};
             cudaLaunchAttribute at[1];
             at[0].id = cudaLaunchAttributeClusterDimension;
             at[0].val.clusterDim.x = gc; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
-            cfg.gridDim = dim3(gc * a.nranks_here); cfg.blockDim = dim3(NTHREADS);
+            cfg.gridDim = dim3(gc * a.nranks_here); cfg.blockDim = dim3(pc.bincl ? NTB : NTHREADS);
             cfg.dynamicSmemBytes = pc.smem; cfg.attrs = at; cfg.numAttrs = 1;
             int ncl = 0;
             if (cudaOccupancyMaxActiveClusters(&ncl, (const void*)f2, &cfg) != cudaSuccess || ncl < 1) {
@@ -417,11 +427,12 @@ int solve(SolveArgs& a) {
         if (a.p.cluster > 0 && pl.cluster == 0)
             return fail(SVM_EINVAL, "cluster mode needs every rank's rows resident in the cluster's shared memory");
     }
-    KernelFn fn = pick_kernel(p.kernel, pl.rpt, pl.alpha_smem, pl.cluster > 0 && pl.bin_words > 0);
+    KernelFn fn = pl.bincl ? pick_bincl(p.kernel) : pick_kernel(p.kernel, pl.rpt, pl.alpha_smem, pl.cluster > 0 && pl.bin_words > 0);
+    const int nthreads = pl.bincl ? NTB : NTHREADS;
     CKR(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
     if (pl.cluster > 8) CKR(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     int per_sm = 0;
-    CKR(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, NTHREADS, pl.smem));
+    CKR(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, nthreads, pl.smem));
     const int grid = a.ctas_per_rank * a.nranks_here;
     if (per_sm < 1 || grid > per_sm * a.n_sm)
         return fail(SVM_ECUDA, "persistent grid of " + std::to_string(grid) + " CTAs is not co-resident");
@@ -465,6 +476,7 @@ int solve(SolveArgs& a) {
         P.max_iter_rank[r] = a.independent ? a.max_iter_rank[r] : p.max_iter;
     }
     P.timeout_ns = a.timeout_ns;
+    if (const char* e = getenv("SVMB200_POLL_NS")) P.poll_ns = atoi(e);
     P.sys_scope = a.mbox_local_alloc ? 0 : 1;
     const bool want_timers = getenv("SVMB200_PHASE_TIMERS") != nullptr;
     for (int r = 0; r < world; ++r) { P.row_off[r] = a.row_off[r]; P.n_rows[r] = (int)a.n_rows[r]; P.mbox[r] = a.mbox[r]; }
@@ -559,7 +571,7 @@ int solve(SolveArgs& a) {
             cudaLaunchAttribute at[1];
             at[0].id = cudaLaunchAttributeClusterDimension;
             at[0].val.clusterDim.x = pl.cluster; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
-            cfg.gridDim = dim3(grid); cfg.blockDim = dim3(NTHREADS);
+            cfg.gridDim = dim3(grid); cfg.blockDim = dim3(nthreads);
             cfg.dynamicSmemBytes = pl.smem; cfg.stream = st; cfg.attrs = at; cfg.numAttrs = 1;
             e = cudaLaunchKernelExC(&cfg, (const void*)fn, args);
         } else {
