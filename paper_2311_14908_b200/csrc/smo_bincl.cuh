@@ -115,6 +115,8 @@ __global__ void __launch_bounds__(NTB, 1) smo_bincl(const Params P) {
     for (int k = 0; k < BINCL_MAXW; ++k) { pu[k] = 0u; pl[k] = 0u; }
     double cu = 0.0, cl = 0.0;
     const int nq = (R + NTB - 1) / NTB;  // rows per thread (upper bound)
+    const bool trace_on = P.trace != nullptr && cta == 0 && rank == 0;
+    int progress_left = 1;               // the host-visible progress word, every check_interval
 
     const bool timing = P.timers != nullptr && blockIdx.x == 0 && t == 0;
     unsigned long long ph_acc[PH_N] = {};
@@ -363,14 +365,18 @@ __global__ void __launch_bounds__(NTB, 1) smo_bincl(const Params P) {
         // the owners of rows u and l (thread j % NTB of the owning CTA) update them before
         // their next row pass
         {
-            const long long lu = (long long)iu - gbase, ll = (long long)il - gbase;
-            if (lu >= 0 && lu < R && (int)(lu % NTB) == t) { a_s[lu] = au2; fl_s[lu] = flags_of(yu, au2, C); }
-            if (ll >= 0 && ll < R && (int)(ll % NTB) == t) { a_s[ll] = al2; fl_s[ll] = flags_of(yl, al2, C); }
+            const int lu = (int)((long long)iu - gbase), ll = (int)((long long)il - gbase);   // |.| < 2^31
+            const bool own_u = (unsigned)lu < (unsigned)R && (lu & (NTB - 1)) == t;
+            const bool own_l = (unsigned)ll < (unsigned)R && (ll & (NTB - 1)) == t;
+            if (own_u) { a_s[lu] = au2; fl_s[lu] = flags_of(yu, au2, C); }
+            if (own_l) { a_s[ll] = al2; fl_s[ll] = flags_of(yl, al2, C); }
         }
-        if (t == 0 && cta == 0 && rank == 0) {
-            if (P.trace && it < P.trace_cap) { P.trace[2 * it] = iu; P.trace[2 * it + 1] = il; }
-            if (P.progress && (it % P.check_interval) == 0) *(volatile unsigned long long*)P.progress = (unsigned long long)it;
+        if (--progress_left == 0) {
+            progress_left = P.check_interval;
+            if (t == 0 && cta == 0 && rank == 0 && P.progress)
+                *(volatile unsigned long long*)P.progress = (unsigned long long)it;
         }
+        if (trace_on && t == 0 && it < P.trace_cap) { P.trace[2 * it] = iu; P.trace[2 * it + 1] = il; }
         BPHASE(PH_S_KUL);
         have_update = true;
         ++it;
