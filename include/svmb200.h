@@ -184,6 +184,11 @@ void svm_comm_destroy(void* comm);
  * (validation, staging, the persistent solver launches, prediction). */
 int64_t svm_kernel_launches(void);
 
+/* How the last solve on this thread ran (observability, not part of the arithmetic): a
+ * one-line JSON object, e.g. {"kernel": "smo_bincl<1>", "ctas_per_rank": 16, "cluster": 16,
+ * "mode": "binary-resident", "threads": 256, "smem": 73488}.  "" before the first solve. */
+const char* svm_last_plan(void);
+
 /* Message for the last non-OK status returned on this thread ("" if none). */
 const char* svm_last_error(void);
 

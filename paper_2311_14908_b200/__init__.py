@@ -86,6 +86,7 @@ def lib():
         L.svm_comm_destroy.restype = None
         L.svm_last_error.restype = ctypes.c_char_p
         L.svm_kernel_launches.restype = ctypes.c_int64
+        L.svm_last_plan.restype = ctypes.c_char_p
         L.svm_version.restype = ctypes.c_char_p
         for name in ("svm_train", "svm_train_ex", "svm_train_dev", "svm_predict", "svm_predict_dev",
                      "svm_predict_ex", "svm_predict_dev_ex", "svm_train_batch_dev",
@@ -98,6 +99,13 @@ def lib():
 def kernel_launches() -> int:
     """CUDA kernels the library launched from this thread so far."""
     return int(lib().svm_kernel_launches())
+
+
+def last_plan() -> dict:
+    """How the last solve on this thread ran (kernel, CTAs, cluster, mode) -- svm_last_plan."""
+    import json
+    txt = lib().svm_last_plan().decode()
+    return json.loads(txt) if txt else {}
 
 
 def version() -> str:

@@ -29,6 +29,7 @@ static_assert(sizeof(svm_params) == 80, "svm_params layout (binding and tests as
 
 thread_local std::string g_err;
 thread_local long long g_launches = 0;
+thread_local std::string g_plan;
 
 int fail(int code, const std::string& msg) {
     g_err = msg;
@@ -429,6 +430,19 @@ int solve(SolveArgs& a) {
     }
     KernelFn fn = pl.bincl ? pick_bincl(p.kernel) : pick_kernel(p.kernel, pl.rpt, pl.alpha_smem, pl.cluster > 0 && pl.bin_words > 0);
     const int nthreads = pl.bincl ? NTB : NTHREADS;
+    {
+        const char* mode = gram ? "gram" : pl.bin_words ? "binary-resident"
+                         : pl.resident ? "float-resident" : pl.cache_slots ? "streamed+row-cache" : "streamed";
+        char buf[320];
+        snprintf(buf, sizeof buf,
+                 "{\"kernel\": \"%s<%d%s>\", \"ctas_per_rank\": %d, \"ranks\": %d, \"cluster\": %d, "
+                 "\"mode\": \"%s\", \"threads\": %d, \"smem\": %zu, \"rows_per_cta\": %d, \"cache_slots\": %d}",
+                 pl.bincl ? "smo_bincl" : "smo_persistent", p.kernel,
+                 pl.bincl ? "" : (std::string(",") + std::to_string(pl.rpt) + (pl.alpha_smem ? ",1" : ",0") +
+                                  ((pl.cluster > 0 && pl.bin_words > 0) ? ",1" : ",0")).c_str(),
+                 a.ctas_per_rank, a.nranks_here, pl.cluster, mode, nthreads, pl.smem, pl.state_cap, pl.cache_slots);
+        g_plan = buf;
+    }
     CKR(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
     if (pl.cluster > 8) CKR(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     int per_sm = 0;
@@ -943,4 +957,5 @@ extern "C" int svm_predict(const float* X_sv, const double* coef, int64_t n_sv, 
 
 extern "C" const char* svm_last_error(void) { return g_err.c_str(); }
 extern "C" int64_t svm_kernel_launches(void) { return g_launches; }
+extern "C" const char* svm_last_plan(void) { return g_plan.c_str(); }
 extern "C" const char* svm_version(void) { return "svmb200 0.1 sm_100a"; }
