@@ -1298,27 +1298,47 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                 }
             }
             if (active) {
+                // kernel values of the thread's RPT rows: all fast exps first (independent,
+                // branch-free chains), then the rare slow phases, then the f updates
+                double ku[RPT], kl[RPT];
+                if (rows_ready || KERNEL == 0) {
+#pragma unroll
+                    for (int q = 0; q < RPT; ++q) { ku[q] = du[q]; kl[q] = dl[q]; }
+                } else {
+                    bool su[RPT], sl[RPT];
+                    bool all_safe = true;
+#pragma unroll
+                    for (int q = 0; q < RPT; ++q) {
+                        ku[q] = svmexp::exp_cr_fast(-(P.gamma * du[q]), tab, su[q]);
+                        kl[q] = svmexp::exp_cr_fast(-(P.gamma * dl[q]), tab, sl[q]);
+                        all_safe = all_safe && su[q] && sl[q];
+                    }
+                    if (!all_safe) {
+#pragma unroll
+                        for (int q = 0; q < RPT; ++q) {
+                            if (!su[q]) ku[q] = svmexp::exp_cr_slow(-(P.gamma * du[q]), tab);
+                            if (!sl[q]) kl[q] = svmexp::exp_cr_slow(-(P.gamma * dl[q]), tab);
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < RPT; ++q) {
+                        const long long jg = gbase + tile * P.rt + t * RPT + q;
+                        if (jg == u) ku[q] = 1.0;                // R16
+                        if (jg == l) kl[q] = 1.0;
+                    }
+                }
 #pragma unroll
                 for (int q = 0; q < RPT; ++q) {
                     const int j = tile * P.rt + t * RPT + q;
                     if (j < R) {
-                        const long long jg = gbase + j;
-                        double ku, kl;
-                        if (rows_ready) {
-                            ku = du[q]; kl = dl[q];
-                        } else if (KERNEL == 1) {
-                            ku = (jg == u) ? 1.0 : svmexp::exp_cr_t(-(P.gamma * du[q]), tab);
-                            kl = (jg == l) ? 1.0 : svmexp::exp_cr_t(-(P.gamma * dl[q]), tab);
-                        } else {
-                            ku = du[q]; kl = dl[q];
-                        }
-                        if (fill_u) fill_u[j] = ku;          // row cache: store the computed
-                        if (fill_l) fill_l[j] = kl;          // kernel values of a missed row
-                        const double fj = fma(cl, kl, fma(cu, ku, f_s[j]));
+                        if (fill_u) fill_u[j] = ku[q];          // row cache: store the computed
+                        if (fill_l) fill_l[j] = kl[q];          // kernel values of a missed row
+                        const double fj = fma(cl, kl[q], fma(cu, ku[q], f_s[j]));
                         f_s[j] = fj;
                         const uint8_t g = fl_s[j];
-                        if ((g & FL_UP) && better_up(fj, j, bfu, bju)) { bfu = fj; bju = j; }
-                        if ((g & FL_LOW) && better_low(fj, j, bfl, bjl)) { bfl = fj; bjl = j; }
+                        // rows are visited in increasing j: a tie keeps the earlier row
+                        if ((g & FL_UP) && fj < bfu) { bfu = fj; bju = j; }
+                        if ((g & FL_LOW) && fj > bfl) { bfl = fj; bjl = j; }
                     }
                 }
             }

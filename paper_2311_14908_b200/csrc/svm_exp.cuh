@@ -130,23 +130,26 @@ __device__ __forceinline__ double table_entry(int e) {
 #endif
 constexpr int EXP_TABLE_DOUBLES = 96;
 
+// Fast phase: returns the correctly rounded exp(x) and sets safe = true, unless the
+// double-double fast result lies too close to a rounding boundary (safe = false; the
+// caller then uses exp_cr_slow).  Branch-free apart from that flag, so a caller can
+// evaluate several exponentials side by side and take the (rare) slow path afterwards.
 template <class Tab>
-SVM_HDM double exp_cr_t(double x, const Tab& tab) {
-    if (x == 0.0) return 1.0;
-    if (x < -708.0) return 0.0;
-    double N = rint(x * SVM_EXP_INV_L32);
+SVM_HDM double exp_cr_fast(double x, const Tab& tab, bool& safe) {
+    const bool special = (x == 0.0) || (x < -708.0);
+    const double xc = special ? -1.0 : x;
+    double N = rint(xc * SVM_EXP_INV_L32);
     int Ni = (int)N;
     int j = Ni & 31;
     int k = (Ni - j) / 32;
     // r = x - N ln2/32 as double-double
-    double r1 = fma(-N, SVM_EXP_L32_1, x);                 // exact (Sterbenz, 38-bit L1)
+    double r1 = fma(-N, SVM_EXP_L32_1, xc);                // exact (Sterbenz, 38-bit L1)
     dd p2 = two_prod(N, SVM_EXP_L32_2);
     dd s = two_sum(r1, -p2.hi);
     double rlo = (s.lo - p2.lo) - N * SVM_EXP_L32_3;
     dd r = two_sum(s.hi, rlo);
     double rh = r.hi, rl = r.lo;
     double Th = tab.T_hi(j), Tl = tab.T_lo(j);
-    // fast phase
     double t = tab.IF_hi(10);
     t = fma(t, rh, tab.IF_hi(9));
     t = fma(t, rh, tab.IF_hi(8));
@@ -166,22 +169,45 @@ SVM_HDM double exp_cr_t(double x, const Tab& tab) {
     double pl = P.lo + (Th * S.lo + Tl * S.hi);
     dd R = fast_two_sum(P.hi, pl);
 #if defined(SVM_EXP_PROBE) && !defined(__CUDA_ARCH__)
-    svm_exp_probe_fast(R.hi * from_bits((uint64_t)(k + 1023) << 52),
-                       R.lo * from_bits((uint64_t)(k + 1023) << 52),
-                       !rounding_safe(R.hi, R.lo, 67));
+    if (!special)
+        svm_exp_probe_fast(R.hi * from_bits((uint64_t)(k + 1023) << 52),
+                           R.lo * from_bits((uint64_t)(k + 1023) << 52),
+                           !rounding_safe(R.hi, R.lo, 67));
 #endif
-    if (!rounding_safe(R.hi, R.lo, 67)) {
-        // slow phase: exp(r) with a degree-13 double-double Horner scheme
-        dd p; p.hi = tab.IF_hi(13); p.lo = tab.IF_lo(13);
-        for (int i = 12; i >= 0; --i) {
-            dd c; c.hi = tab.IF_hi(i); c.lo = tab.IF_lo(i);
-            p = dd_add(dd_mul(p, r), c);
-        }
-        dd T; T.hi = Th; T.lo = Tl;
-        R = dd_mul(p, T);
+    safe = special || rounding_safe(R.hi, R.lo, 67);
+    const double scale = from_bits((uint64_t)(k + 1023) << 52);  // k >= -1022: normal
+    const double v = R.hi * scale;
+    return x == 0.0 ? 1.0 : (x < -708.0 ? 0.0 : v);
+}
+
+// Slow phase (rare): exp(r) with a degree-13 double-double Horner scheme.
+template <class Tab>
+SVM_HDM double exp_cr_slow(double x, const Tab& tab) {
+    double N = rint(x * SVM_EXP_INV_L32);
+    int Ni = (int)N;
+    int j = Ni & 31;
+    int k = (Ni - j) / 32;
+    double r1 = fma(-N, SVM_EXP_L32_1, x);
+    dd p2 = two_prod(N, SVM_EXP_L32_2);
+    dd s = two_sum(r1, -p2.hi);
+    double rlo = (s.lo - p2.lo) - N * SVM_EXP_L32_3;
+    dd r = two_sum(s.hi, rlo);
+    dd p; p.hi = tab.IF_hi(13); p.lo = tab.IF_lo(13);
+    for (int i = 12; i >= 0; --i) {
+        dd c; c.hi = tab.IF_hi(i); c.lo = tab.IF_lo(i);
+        p = dd_add(dd_mul(p, r), c);
     }
-    double scale = from_bits((uint64_t)(k + 1023) << 52);  // k >= -1022: normal
+    dd T; T.hi = tab.T_hi(j); T.lo = tab.T_lo(j);
+    dd R = dd_mul(p, T);
+    double scale = from_bits((uint64_t)(k + 1023) << 52);
     return R.hi * scale;
+}
+
+template <class Tab>
+SVM_HDM double exp_cr_t(double x, const Tab& tab) {
+    bool safe;
+    const double v = exp_cr_fast(x, tab, safe);
+    return safe ? v : exp_cr_slow(x, tab);
 }
 
 SVM_HD double exp_cr(double x) {
