@@ -76,6 +76,10 @@ def test_argument_validation_before_device_work(S, kw, msg):
     assert msg in S.lib().svm_last_error().decode()
 
 
+def test_last_plan_before_any_solve(S):
+    assert isinstance(S.last_plan(), dict)
+
+
 def test_null_pointers_rejected(S):
     b = ctypes.c_double()
     assert S.lib().svm_train(None, None, 4, 2, 1.0, 0, 0.0, 1e-3, None, ctypes.byref(b)) == -1

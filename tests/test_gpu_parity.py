@@ -362,6 +362,39 @@ def test_binary_encoding_equals_fp_path(S, monkeypatch):
             _assert_exact(r_g, r_o)
 
 
+@pytest.mark.parametrize("d", [300, 500])
+def test_wide_binary_rows_kernel_variants(S, monkeypatch, d):
+    """Binary rows wider than smo_bincl's 256 features take the cluster-specialised
+    smo_persistent (d = 300: rows still travel in the records; d = 500: rows gathered
+    from HBM), and the global-exchange path (cluster = -1); all equal the oracle."""
+    rng = np.random.default_rng(d)
+    n = 1500
+    Xb = (rng.random((n, d)) < 0.05).astype(np.float32)
+    yb = np.where(Xb[:, :20].sum(1) + 0.5 * rng.normal(size=n) > 1.0, 1, -1).astype(np.int8)
+    wb = W.Workload("b", "", n, d, O.RBF, 0.05, 2.0, 1e-3, 0, 0, 0, None)
+    r_g, r_o = _run_pair(S, wb, Xb, yb)
+    _assert_exact(r_g, r_o)
+    plan = S.last_plan()
+    assert plan["mode"] == "binary-resident" and plan["kernel"].startswith("smo_persistent")
+    r_g2 = S.svm_train_ex(Xb, yb, wb.C, wb.kernel, wb.gamma, wb.tol, want_f=True, cluster=-1)
+    np.testing.assert_array_equal(r_g2["alpha"], r_o.alpha)
+
+
+def test_last_plan_reports_the_kernel(S):
+    """svm_last_plan: W2 runs on the binary-cluster kernel; a streamed problem on the
+    148-CTA persistent kernel."""
+    w = W.get("W2")
+    X, y = w.train(4000)
+    S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol, max_iter=10)
+    p = S.last_plan()
+    assert p["kernel"] == "smo_bincl<1>" and p["mode"] == "binary-resident" and p["cluster"] >= 1
+    w5 = W.get("W5")
+    X5, y5 = w5.train(200000)                            # 1352 rows of 256 floats per CTA
+    S.svm_train_ex(X5, y5, w5.C, w5.kernel, w5.gamma, w5.tol, max_iter=3)
+    p = S.last_plan()
+    assert p["kernel"].startswith("smo_persistent") and p["cluster"] == 0 and p["mode"].startswith("streamed")
+
+
 def test_train_shard_single_rank(S):
     """The one-process-per-GPU entry point (NCCL bootstrap, IPC mailbox, system-scope
     exchange) with world = 1 on one GPU reproduces the oracle."""
