@@ -52,6 +52,10 @@ def lib():
             L.oracle_svm_train.argtypes = [P, P, i64, i64, f64, i32, f64, f64, i64, P, P,
                                            P, P, P, P, P, P, P, P, i64]
             L.oracle_svm_train.restype = i32
+            L.oracle_svm_train_wss.argtypes = L.oracle_svm_train.argtypes + [i32]
+            L.oracle_svm_train_wss.restype = i32
+            L.oracle_select_second_order.argtypes = [P, P, P, P, f64, i64, i64, i32, f64, i64]
+            L.oracle_select_second_order.restype = i64
             L.oracle_decision.argtypes = [P, P, i64, i64, f64, i32, f64, P, i64, P]
             L.oracle_dual_objective.argtypes = [P, P, P, i64, i64, i32, f64]
             L.oracle_dual_objective.restype = f64
@@ -109,7 +113,9 @@ class TrainResult(dict):
 
 
 def train(X, y, C: float, kernel: int, gamma: float = 0.0, tol: float = 1e-3,
-          max_iter: int = 0, alpha0=None, f0=None, trace_cap: int = 0) -> TrainResult:
+          max_iter: int = 0, alpha0=None, f0=None, trace_cap: int = 0, wss: int = 1) -> TrainResult:
+    """The oracle SMO solve (smo_oracle.c).  wss: 1 maximal violating pair (reading R1,
+    default), 2 second-order selection of the second index (Fan et al.)."""
     X = _f32(X)
     y = np.ascontiguousarray(y, dtype=np.int8)
     n, d = X.shape
@@ -121,11 +127,11 @@ def train(X, y, C: float, kernel: int, gamma: float = 0.0, tol: float = 1e-3,
     b, it = ctypes.c_double(), ctypes.c_int64()
     conv = ctypes.c_int()
     bu, bl = ctypes.c_double(), ctypes.c_double()
-    rc = lib().oracle_svm_train(_p(X), _p(y), n, d, float(C), int(kernel), float(gamma),
-                                float(tol), int(max_iter), _p(a0), _p(g0), _p(alpha), _p(f),
-                                ctypes.byref(b), ctypes.byref(it), ctypes.byref(conv),
-                                ctypes.byref(bu), ctypes.byref(bl), _p(trace),
-                                trace_cap if trace_cap > 0 else 0)
+    rc = lib().oracle_svm_train_wss(_p(X), _p(y), n, d, float(C), int(kernel), float(gamma),
+                                    float(tol), int(max_iter), _p(a0), _p(g0), _p(alpha), _p(f),
+                                    ctypes.byref(b), ctypes.byref(it), ctypes.byref(conv),
+                                    ctypes.byref(bu), ctypes.byref(bl), _p(trace),
+                                    trace_cap if trace_cap > 0 else 0, int(wss))
     if rc != 0:
         raise ValueError(f"oracle_svm_train failed with status {rc}")
     res = TrainResult(alpha=alpha, f=f, b=b.value, iterations=it.value,

@@ -22,7 +22,8 @@
  *
  * Pins (tests/test_oracle_*.py): closed-form two/three-point duals, RBF two-point,
  * eta = 0 duplicates, separable toy with known margin, brute-force active-set QP,
- * KKT at convergence, invariants per step, mpmath-rounded exp.
+ * KKT at convergence, invariants per step, mpmath-rounded exp; the second-order working
+ * set (oracle_select_second_order, wss = 2) against scikit-learn's libsvm.
  */
 #include <math.h>
 #include <stdint.h>
@@ -184,12 +185,52 @@ int oracle_select(const double* f, const int8_t* y, const double* alpha, double 
  * pair_trace (nullable) receives (i_up, i_low) per update.
  * Returns 0 on success, -3 on a single-class problem, -1 on bad arguments.
  */
+/* Second-order working-set selection (WSS2; the method of Fan, Chen and Lin 2005 that
+ * P:L140 cites as "fan2005working").  Given the first-order u (the
+ * minimum f over I_up), choose l among t in I_low with f_t > f_u maximising the gain of
+ * the unconstrained pair step,
+ *     g_t = (f_t - f_u)^2 / a_t,   a_t = K_uu + K_tt - 2 K_ut  (a_t <= 1e-12 -> 1e-12),
+ * ties to the lowest index (reading R4).  Returns -1 when no t qualifies. */
+int64_t oracle_select_second_order(const float* X, const int8_t* y, const double* alpha,
+                                   const double* f, double C, int64_t n, int64_t d,
+                                   int kernel, double gamma, int64_t u) {
+    const float* xu = X + u * d;
+    const double Kuu = oracle_kernel(kernel, gamma, xu, xu, d, 1);
+    int64_t best = -1;
+    double best_g = 0.0;
+    for (int64_t t = 0; t < n; ++t) {
+        const int pos = y[t] == 1;
+        const int low = pos ? (alpha[t] > 0.0) : (alpha[t] < C);
+        if (!low) continue;
+        const double b = f[t] - f[u];
+        if (!(b > 0.0)) continue;
+        const float* xt = X + t * d;
+        const double Kut = oracle_kernel(kernel, gamma, xu, xt, d, t == u);
+        const double Ktt = oracle_kernel(kernel, gamma, xt, xt, d, 1);
+        double a = Kuu + Ktt - 2.0 * Kut;
+        if (!(a > 1e-12)) a = 1e-12;
+        const double g = (b * b) / a;
+        if (best < 0 || g > best_g) { best = t; best_g = g; }
+    }
+    return best;
+}
+
 int oracle_svm_train(const float* X, const int8_t* y, int64_t n, int64_t d, double C,
                      int kernel, double gamma, double tol, int64_t max_iter,
                      const double* alpha0, const double* f0,
                      double* alpha, double* f, double* b_out, int64_t* iters_out,
                      int* converged_out, double* b_up_out, double* b_low_out,
-                     int64_t* pair_trace, int64_t trace_cap) {
+                     int64_t* pair_trace, int64_t trace_cap);
+
+/* The SMO solve with working-set rule wss (1: maximal violating pair, S:L197 -- the
+ * default reading R1; 2: second-order selection of l above).  The stopping test is the
+ * first-order gap in both. */
+int oracle_svm_train_wss(const float* X, const int8_t* y, int64_t n, int64_t d, double C,
+                         int kernel, double gamma, double tol, int64_t max_iter,
+                         const double* alpha0, const double* f0,
+                         double* alpha, double* f, double* b_out, int64_t* iters_out,
+                         int* converged_out, double* b_up_out, double* b_low_out,
+                         int64_t* pair_trace, int64_t trace_cap, int wss) {
     oracle_init();
     if (n < 2 || d < 1 || !(C > 0.0) || !(tol > 0.0)) return -1;
     if (kernel == ORACLE_RBF && !(gamma > 0.0)) return -1;
@@ -212,6 +253,7 @@ int oracle_svm_train(const float* X, const int8_t* y, int64_t n, int64_t d, doub
         if (!oracle_select(f, y, alpha, C, n, &u, &l, &b_up, &b_low)) { converged = 1; break; }
         if (b_low - b_up <= 2.0 * tol) { converged = 1; break; }
         if (it == max_iter) break;
+        if (wss == 2) l = oracle_select_second_order(X, y, alpha, f, C, n, d, kernel, gamma, u);
 
         const float* xu = X + u * d;
         const float* xl = X + l * d;
@@ -219,7 +261,7 @@ int oracle_svm_train(const float* X, const int8_t* y, int64_t n, int64_t d, doub
         double Kll = oracle_kernel(kernel, gamma, xl, xl, d, 1);
         double Kul = oracle_kernel(kernel, gamma, xu, xl, d, u == l);
         double eta = Kuu + Kll - 2.0 * Kul;
-        double gap = b_low - b_up;
+        double gap = f[l] - f[u];             /* = b_low - b_up for the first-order pair */
         double yu = (double)y[u], yl = (double)y[l];
         double tu = (y[u] == 1) ? C - alpha[u] : alpha[u];
         double tl = (y[l] == 1) ? alpha[l] : C - alpha[l];
@@ -286,4 +328,15 @@ int oracle_num_threads(void) {
 #else
     return 1;
 #endif
+}
+
+int oracle_svm_train(const float* X, const int8_t* y, int64_t n, int64_t d, double C,
+                     int kernel, double gamma, double tol, int64_t max_iter,
+                     const double* alpha0, const double* f0,
+                     double* alpha, double* f, double* b_out, int64_t* iters_out,
+                     int* converged_out, double* b_up_out, double* b_low_out,
+                     int64_t* pair_trace, int64_t trace_cap) {
+    return oracle_svm_train_wss(X, y, n, d, C, kernel, gamma, tol, max_iter, alpha0, f0, alpha, f,
+                                b_out, iters_out, converged_out, b_up_out, b_low_out, pair_trace,
+                                trace_cap, 1);
 }

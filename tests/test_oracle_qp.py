@@ -10,6 +10,7 @@ import sys
 import numpy as np
 import pytest
 
+from gen import workloads as W
 from oracle import oracle as O
 
 
@@ -189,3 +190,28 @@ def test_openmp_threads_bit_identical():
         env = dict(os.environ, OMP_NUM_THREADS=t)
         outs.append(subprocess.check_output([sys.executable, "-c", code], env=env))
     assert outs[0] == outs[1]
+
+
+@pytest.mark.parametrize("name,n", [("W1", None), ("W3", 800), ("W4", 2000)])
+def test_second_order_selection_matches_libsvm(name, n):
+    """oracle wss=2 (second-order working set, the Fan et al. method P:L140 cites; SURVEY
+    §8(f) NEXT-2) against an independent implementation of the same rule -- scikit-learn's
+    libsvm (SVC, shrinking off, tolerance 2 tau = the same first-order stopping gap): the
+    same optimum (dual objective to 1e-6 relative, alpha to 1e-3 C) in an iteration count
+    of the same order (libsvm caches K in float32 and counts differently)."""
+    svm = pytest.importorskip("sklearn.svm")
+    w = W.get(name)
+    X, y = w.train(n) if n else w.train()
+    r = O.train(X, y, w.C, w.kernel, w.gamma, w.tol, wss=2)
+    assert r.converged
+    clf = svm.SVC(C=w.C, kernel="rbf" if w.kernel == O.RBF else "linear",
+                  gamma=w.gamma if w.kernel == O.RBF else "scale", tol=2 * w.tol,
+                  shrinking=False, cache_size=2000).fit(X.astype(np.float64), y)
+    a = np.zeros(len(y))
+    a[clf.support_] = np.abs(clf.dual_coef_[0])
+    w_or = O.dual_objective(X, y, r.alpha, w.kernel, w.gamma)
+    w_lib = O.dual_objective(X, y, a, w.kernel, w.gamma)
+    assert abs(w_or - w_lib) <= 1e-6 * abs(w_lib)
+    r1 = O.train(X, y, w.C, w.kernel, w.gamma, w.tol, wss=1)
+    assert abs(O.dual_objective(X, y, r1.alpha, w.kernel, w.gamma) - w_or) <= 1e-6 * abs(w_or)
+    assert 0.5 * clf.n_iter_[0] <= r.iterations <= 2.0 * clf.n_iter_[0]
