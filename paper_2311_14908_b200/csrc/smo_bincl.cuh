@@ -32,6 +32,7 @@ struct ShB {
     double exp_tab[svmexp::EXP_TABLE_DOUBLES];
     unsigned long long red_k[2][2][NTB / 32];   // [parity][up, low][warp]
     unsigned red_i[2][2][NTB / 32];
+    uint4 wrec[2][NTB / 32][16];                // [parity][warp][word]: each warp's record words
 };
 
 __host__ __device__ inline size_t bincl_align(size_t x, size_t a) { return (x + a - 1) & ~(a - 1); }
@@ -200,36 +201,20 @@ __global__ void __launch_bounds__(NTB, 1) smo_bincl(const Params P) {
         const int par = (int)(seq & 1);
         const uint32_t sq = (uint32_t)seq & 0xffffu;
         {
-            unsigned long long kw;
-            unsigned iw;
-            argmin_redux(0xffffffffu, bju == INT_MAX ? ~0ull : fkey(bfu), (unsigned)bju, kw, iw);
-            if (lane == 0) { sh.red_k[par][0][warp] = kw; sh.red_i[par][0][warp] = iw; }
-            argmin_redux(0xffffffffu, bjl == INT_MAX ? ~0ull : ~fkey(bfl), (unsigned)bjl, kw, iw);
-            if (lane == 0) { sh.red_k[par][1][warp] = kw; sh.red_i[par][1][warp] = iw; }
-        }
-        BPHASE(PH_C_REDUCE);
-        __syncthreads();                 // the one CTA barrier of the iteration
-        (void)*(volatile unsigned*)&sh.red_i[par][0][0];
-        BPHASE(PH_C_WAITB);
-
-        // ================= exchange seq (a6).  Control flow is warp-uniform throughout
-        // (divergent branches cost more than the arithmetic here): lanes compute with
-        // clamped indices and select.
-        {
-            // every warp forms the CTA candidate (local rows ju, jl) and its record; warp w
-            // stores it into the CTAs j = w, w + 8, ... (one store instruction per target:
-            // a DSMEM store instruction costs ~27 cycles per destination CTA)
-            const bool in8 = lane < NTB / 32;
-            const int l8 = lane & (NTB / 32 - 1);
-            unsigned long long kmu, kml;
-            unsigned jmu, jml;
-            argmin_redux(0xffffffffu, in8 ? sh.red_k[par][0][l8] : ~0ull, in8 ? sh.red_i[par][0][l8] : 0xffffffffu, kmu, jmu);
-            argmin_redux(0xffffffffu, in8 ? sh.red_k[par][1][l8] : ~0ull, in8 ? sh.red_i[par][1][l8] : 0xffffffffu, kml, jml);
-            const int ju = (int)jmu, jl = (int)jml;
+            unsigned long long kwu, kwl;
+            unsigned iwu, iwl;
+            argmin_redux(0xffffffffu, bju == INT_MAX ? ~0ull : fkey(bfu), (unsigned)bju, kwu, iwu);
+            argmin_redux(0xffffffffu, bjl == INT_MAX ? ~0ull : ~fkey(bfl), (unsigned)bjl, kwl, iwl);
+            if (lane == 0) {
+                sh.red_k[par][0][warp] = kwu; sh.red_i[par][0][warp] = iwu;
+                sh.red_k[par][1][warp] = kwl; sh.red_i[par][1][warp] = iwl;
+            }
+            // this warp's record words (word h = lane): 0 (i_up, f_up), 1 (i_low, f_low),
+            // 2 (y_up | y_low << 16, a_up), 3 (0, a_low), 4.. the candidates' bit rows.
+            // Built before the barrier, so after it the CTA record is a copy.
+            const int ju = (int)iwu, jl = (int)iwl;
             const bool eu = ju == INT_MAX, el = jl == INT_MAX;
             const int juc = eu ? 0 : ju, jlc = el ? 0 : jl;
-            // word h = lane: 0 (i_up, f_up), 1 (i_low, f_low), 2 (y_up | y_low << 16, a_up),
-            // 3 (0, a_low), 4.. the candidates' bit rows (3 words per record word)
             const double au_c = a_s[juc], al_c = a_s[jlc];
             const uint8_t gu_c = fl_s[juc], gl_c = fl_s[jlc];
             const int yu_ = eu ? 0 : ((gu_c & FL_POS) ? 1 : -1);
@@ -247,13 +232,44 @@ __global__ void __launch_bounds__(NTB, 1) smo_bincl(const Params P) {
                              : lane == 1 ? (el ? 0xffffffffu : (uint32_t)(gbase + jl))
                              : lane == 2 ? (uint32_t)((yu_ & 0xffff) | (yl_ << 16))
                              : lane == 3 ? 0u : r0w;
-            const double vd = lane == 0 ? (eu ? INF : fkey_inv(kmu))
-                            : lane == 1 ? (el ? -INF : fkey_inv(~kml))
+            const double vd = lane == 0 ? (eu ? INF : fkey_inv(kwu))
+                            : lane == 1 ? (el ? -INF : fkey_inv(~kwl))
                             : lane == 2 ? (eu ? 0.0 : au_c) : (el ? 0.0 : al_c);
             const unsigned long long v = lane < 4 ? (unsigned long long)__double_as_longlong(vd)
                                                   : ((unsigned long long)r1w | ((unsigned long long)r2w << 32));
-            const uint4 wv = rec_pack(sq, a, v);
-            const uint32_t src = smem_u32(cmb + ((size_t)par * G + cta) * RW + min(lane, RW - 1));
+            if (lane < RW) sh.wrec[par][warp][lane] = rec_pack(sq, a, v);
+        }
+        BPHASE(PH_C_REDUCE);
+        __syncthreads();                 // the one CTA barrier of the iteration
+        (void)*(volatile unsigned*)&sh.red_i[par][0][0];
+        BPHASE(PH_C_WAITB);
+
+        // ================= exchange seq (a6).  Control flow is warp-uniform throughout
+        // (divergent branches cost more than the arithmetic here): lanes compute with
+        // clamped indices and select.
+        {
+            // every warp forms the CTA candidate and copies its record from the winning
+            // warps' words; warp w stores it into the CTAs j = w, w + 8, ... (one store
+            // instruction per target: a DSMEM store instruction costs ~27 cycles per
+            // destination CTA)
+            const bool in8 = lane < NTB / 32;
+            const int l8 = lane & (NTB / 32 - 1);
+            unsigned long long kmu, kml;
+            unsigned jmu, jml;
+            argmin_redux(0xffffffffu, in8 ? sh.red_k[par][0][l8] : ~0ull, in8 ? sh.red_i[par][0][l8] : 0xffffffffu, kmu, jmu);
+            argmin_redux(0xffffffffu, in8 ? sh.red_k[par][1][l8] : ~0ull, in8 ? sh.red_i[par][1][l8] : 0xffffffffu, kml, jml);
+            // row j belongs to warp (j mod 256) / 32
+            const int wu = (int)jmu == INT_MAX ? 0 : (int)((jmu & (NTB - 1)) >> 5);
+            const int wl = (int)jml == INT_MAX ? 0 : (int)((jml & (NTB - 1)) >> 5);
+            const int h = min(lane, RW - 1);
+            const bool from_u = h == 0 || h == 2 || (h >= 4 && h - 4 < rw);
+            uint4 wv = sh.wrec[par][from_u ? wu : wl][h];
+            if (h == 2) {                                 // y_up from u's warp, y_low from l's
+                const uint4 w2l = sh.wrec[par][wl][2];
+                wv = rec_pack(sq, (wv.y & 0xffffu) | (w2l.y & 0xffff0000u),
+                              (unsigned long long)wv.z | ((unsigned long long)wv.w << 32));
+            }
+            const uint32_t src = smem_u32(cmb + ((size_t)par * G + cta) * RW + h);
             for (int j = warp; j < G; j += NTB / 32) {
                 uint32_t ra;
                 asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(src), "r"(j));
