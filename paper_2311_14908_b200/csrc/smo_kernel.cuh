@@ -184,33 +184,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_volatile_v2(unsigned long long* p, unsigned long long a,
-                                               unsigned long long b) {
-    asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" :: "l"(p), "l"(a), "l"(b) : "memory");
-}
-__device__ __forceinline__ void ld_volatile_v2(const unsigned long long* p, unsigned long long& a,
-                                               unsigned long long& b) {
-    asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
-}
-__device__ __forceinline__ unsigned long long ll_word(uint32_t flag, uint32_t payload) {
-    return ((unsigned long long)flag << 32) | payload;
-}
-__device__ __forceinline__ void red_release_gpu(unsigned long long* p) {
-    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" :: "l"(p) : "memory");
-}
-__device__ __forceinline__ void red_release_sys(unsigned long long* p) {
-    asm volatile("red.release.sys.global.add.u64 [%0], 1;" :: "l"(p) : "memory");
-}
 __device__ __forceinline__ void named_sync(int id) {
     asm volatile("bar.sync %0, %1;" :: "r"(id), "n"(NSYNC) : "memory");
 }
@@ -315,14 +288,6 @@ struct Cand {
     double fu, fl, au, al;
     int iu, il, yu, yl;
 };
-__device__ __forceinline__ void cand_init(Cand& c) {
-    c.fu = __longlong_as_double(0x7ff0000000000000ll); c.fl = -c.fu;
-    c.au = 0.0; c.al = 0.0; c.iu = INT_MAX; c.il = INT_MAX; c.yu = 0; c.yl = 0;
-}
-__device__ __forceinline__ void cand_merge(Cand& a, const Cand& b) {
-    if (b.iu != INT_MAX && better_up(b.fu, b.iu, a.fu, a.iu)) { a.fu = b.fu; a.iu = b.iu; a.au = b.au; a.yu = b.yu; }
-    if (b.il != INT_MAX && better_low(b.fl, b.il, a.fl, a.il)) { a.fl = b.fl; a.il = b.il; a.al = b.al; a.yl = b.yl; }
-}
 __device__ __forceinline__ uint32_t rec_chk(uint32_t a, uint32_t b, uint32_t c) {
     // high half of a multiplicative hash: any change of one payload word changes it with
     // probability ~1 - 2^-16
@@ -360,22 +325,6 @@ __device__ __forceinline__ uint4 rec_load(const uint4* p, int sys) {
         asm volatile("ld.relaxed.sys.global.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
     else
         asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void red_relaxed_gpu(unsigned long long* p) {
-    asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" :: "l"(p) : "memory");
-}
-__device__ __forceinline__ void red_relaxed_sys(unsigned long long* p) {
-    asm volatile("red.relaxed.sys.global.add.u64 [%0], 1;" :: "l"(p) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_relaxed_gpu(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
 
