@@ -132,6 +132,9 @@ struct Params {
     int crw;                       // cluster mode: 16-byte words per record (4 + 2 ceil(crow/3))
     unsigned long long* timers;    // optional [8] per-phase cycle totals of CTA 0
     int poll_ns;                   // > 0: back-off between mailbox polls (tuning)
+    int l2_keep_tiles;             // streamed X: tiles [0, l2_keep_tiles) of every CTA block are
+                                   // copied with an L2 evict_last policy, the rest evict_first, so
+                                   // that part of X stays in L2 across iterations (0 = no hints)
 };
 
 // phase timers (cycles, CTA 0): scalar warp lane 0 ...
@@ -183,6 +186,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t policy) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                 :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy) : "memory");
+}
+__device__ __forceinline__ uint64_t l2_policy(bool keep) {
+    uint64_t p;
+    if (keep) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
 }
 __device__ __forceinline__ void named_sync(int id) {
     asm volatile("bar.sync %0, %1;" :: "r"(id), "n"(NSYNC) : "memory");
@@ -523,6 +537,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
         if (lane == 0 && n_tiles > 0) {
             unsigned int s = 0, slot = 0, par = 0;
             bool wrapped = false;
+            const uint64_t pol_keep = l2_policy(true), pol_stream = l2_policy(false);
             int tile = 0, chunk = 0;
             for (;;) {
                 if (wrapped) {
@@ -536,7 +551,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                 const uint32_t bytes = (uint32_t)P.kc * rp * 4u;
                 const float* src = xcta + (long long)tile * P.d_pad * P.rt + (long long)chunk * P.kc * rp;
                 mbar_arrive_tx(&full[slot], bytes);
-                bulk_g2s(ring + (size_t)slot * stage_floats, src, bytes, &full[slot]);
+                if (P.l2_keep_tiles > 0)
+                    bulk_g2s_hint(ring + (size_t)slot * stage_floats, src, bytes, &full[slot],
+                                  tile < P.l2_keep_tiles ? pol_keep : pol_stream);
+                else
+                    bulk_g2s(ring + (size_t)slot * stage_floats, src, bytes, &full[slot]);
                 ++s;
                 sh.issued = s;
                 if (++slot == (unsigned)P.stages) { slot = 0; par ^= 1u; wrapped = true; }
@@ -742,6 +761,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                 if (lane < 4 * xworld)
                     rec_store(mbox_words(P.mbox[xbase + (lane >> 2)], par, lane & 3, g_total) + gcta,
                               rec_word(c, lane & 3, sq), P.sys_scope);
+                // warm L2 with this CTA's candidate rows: the two winners' rows are gathered
+                // from the row-major replica right after the selection (the critical path)
+                if (!m_gram && !m_isbin) {
+                    const int span = P.d * 4;
+                    const int lines = (span + 127) / 128 + 1;
+                    for (int q = lane; q < 2 * lines; q += 32) {
+                        const int jj = q < lines ? ju : jl;
+                        if (jj != INT_MAX) {
+                            const char* row = reinterpret_cast<const char*>(xr + (gbase + jj) * (long long)P.d);
+                            const int o = min((q % lines) * 128, span - 1);
+                            asm volatile("prefetch.global.L2 [%0];" :: "l"(row + o));
+                        }
+                    }
+                }
                 SVM_PHASE(timing, PH_S_PUBLISH);
                 constexpr int PB = 5;                            // records in flight per lane
                 unsigned int rounds = 0;

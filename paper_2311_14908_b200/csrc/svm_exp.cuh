@@ -9,8 +9,8 @@
 // Method (table-driven, two-phase / Ziv):
 //   x = (32 k + j) ln2/32 + r,  |r| <= ln2/64,  r in double-double (3-part ln2/32)
 //   exp(x) = 2^k * T_j * exp(r),  T_j = 2^(j/32) as double-double
-//   fast phase:  exp(r) = 1 + r + r^2/2 (double-double) + tail (double Horner,
-//                degree 3..10), relative error < 2^-72
+//   fast phase:  exp(r) - 1 = r + r^2/2 (error-free) + tail (double Horner,
+//                degree 3..8), times T in double-double; relative error < 2^-71
 //   if the fast result lies within 2^-68 (relative) of a rounding boundary,
 //   slow phase:  exp(r) by a degree-13 double-double Horner (~2^-100)
 // Arguments below -708 return 0 (reading R15); x = 0 returns 1.
@@ -134,49 +134,61 @@ constexpr int EXP_TABLE_DOUBLES = 96;
 // double-double fast result lies too close to a rounding boundary (safe = false; the
 // caller then uses exp_cr_slow).  Branch-free apart from that flag, so a caller can
 // evaluate several exponentials side by side and take the (rare) slow path afterwards.
+//
+// Error budget of R = Rh + Rl against exp(x) / 2^k (relative, |r| <= ln2/64 < 2^-6.5):
+// argument reduction 2^-80 (three-part ln2/32), truncation after r^8/8! 2^-77, the
+// double-evaluated tail r^3 (1/3! + ... + r^5/8!) ~2^-73, the omitted rl r^2/2 ~2^-74,
+// table 2^-106: < 2^-71 in all, against the 2^-67 margin of the rounding test.
 template <class Tab>
 SVM_HDM double exp_cr_fast(double x, const Tab& tab, bool& safe) {
     const bool special = (x == 0.0) || (x < -708.0);
     const double xc = special ? -1.0 : x;
-    double N = rint(xc * SVM_EXP_INV_L32);
-    int Ni = (int)N;
-    int j = Ni & 31;
-    int k = (Ni - j) / 32;
-    // r = x - N ln2/32 as double-double
-    double r1 = fma(-N, SVM_EXP_L32_1, xc);                // exact (Sterbenz, 38-bit L1)
-    dd p2 = two_prod(N, SVM_EXP_L32_2);
-    dd s = two_sum(r1, -p2.hi);
-    double rlo = (s.lo - p2.lo) - N * SVM_EXP_L32_3;
-    dd r = two_sum(s.hi, rlo);
-    double rh = r.hi, rl = r.lo;
-    double Th = tab.T_hi(j), Tl = tab.T_lo(j);
-    double t = tab.IF_hi(10);
-    t = fma(t, rh, tab.IF_hi(9));
-    t = fma(t, rh, tab.IF_hi(8));
-    t = fma(t, rh, tab.IF_hi(7));
-    t = fma(t, rh, tab.IF_hi(6));
-    t = fma(t, rh, tab.IF_hi(5));
-    t = fma(t, rh, tab.IF_hi(4));
-    t = fma(t, rh, tab.IF_hi(3));
-    double rh2 = rh * rh;
-    double tail = t * (rh2 * rh);
-    dd q = two_prod(rh, rh);
-    dd a = fast_two_sum(1.0, rh);
-    dd b = two_sum(a.hi, 0.5 * q.hi);
-    double lo = (a.lo + b.lo) + (rl + (0.5 * q.lo + (rh * rl + tail)));
-    dd S = fast_two_sum(b.hi, lo);
-    dd P = two_prod(Th, S.hi);
-    double pl = P.lo + (Th * S.lo + Tl * S.hi);
-    dd R = fast_two_sum(P.hi, pl);
+    // N = nearest integer to x 32/ln2 by the 1.5 2^52 shift (exact: |N| < 2^16); the low
+    // word of the shifted value is N as a 32-bit integer
+    const double SH = 0x1.8p52;
+    const double tN = fma(xc, SVM_EXP_INV_L32, SH);
+    const double N = tN - SH;
+    const int Ni = (int)(uint32_t)bits_of(tN);
+    const int j = Ni & 31;
+    const int k = Ni >> 5;                                 // floor(N / 32)
+    // r = x - N ln2/32 = rh + rl
+    const double r1 = fma(-N, SVM_EXP_L32_1, xc);          // exact (Sterbenz, 38-bit L1)
+    const double p2h = N * SVM_EXP_L32_2;
+    const double p2l = fma(N, SVM_EXP_L32_2, -p2h);
+    const dd s = two_sum(r1, -p2h);
+    const double rh = s.hi;
+    const double rl = fma(-N, SVM_EXP_L32_3, s.lo - p2l);
+    // exp(r) - 1 = qh + ql:  rh + rh^2/2 (error-free), + rl (1 + rh) + rh^3 P(rh)
+    constexpr double IFH[16] = {SVM_EXP_IF_HI_INIT};
+    const double sqh = rh * rh, sql = fma(rh, rh, -sqh);
+    const double h = 0.5 * sqh;
+    const double qh = rh + h;                              // fast two-sum: |rh| >= |h|
+    const double e = h - (qh - rh);
+    double P = IFH[8];
+    P = fma(P, rh, IFH[7]);
+    P = fma(P, rh, IFH[6]);
+    P = fma(P, rh, IFH[5]);
+    P = fma(P, rh, IFH[4]);
+    P = fma(P, rh, IFH[3]);
+    const double tail = (sqh * rh) * P;
+    const double ql = (e + 0.5 * sql) + (fma(rh, rl, rl) + tail);
+    // R = T (1 + q), T = Th + Tl = 2^(j/32)
+    const double Th = tab.T_hi(j), Tl = tab.T_lo(j);
+    const double ph = Th * qh, pl = fma(Th, qh, -ph);
+    const double Rh0 = Th + ph;                            // fast two-sum: Th >= 1 > |ph|
+    const double Rl0 = ph - (Rh0 - Th);
+    const double Rl1 = Rl0 + (pl + fma(Th, ql, fma(Tl, qh, Tl)));
+    const double Rh = Rh0 + Rl1;                           // normalise
+    const double Rl = Rl1 - (Rh - Rh0);
 #if defined(SVM_EXP_PROBE) && !defined(__CUDA_ARCH__)
     if (!special)
-        svm_exp_probe_fast(R.hi * from_bits((uint64_t)(k + 1023) << 52),
-                           R.lo * from_bits((uint64_t)(k + 1023) << 52),
-                           !rounding_safe(R.hi, R.lo, 67));
+        svm_exp_probe_fast(Rh * from_bits((uint64_t)(k + 1023) << 52),
+                           Rl * from_bits((uint64_t)(k + 1023) << 52),
+                           !rounding_safe(Rh, Rl, 67));
 #endif
-    safe = special || rounding_safe(R.hi, R.lo, 67);
+    safe = special || rounding_safe(Rh, Rl, 67);
     const double scale = from_bits((uint64_t)(k + 1023) << 52);  // k >= -1022: normal
-    const double v = R.hi * scale;
+    const double v = Rh * scale;
     return x == 0.0 ? 1.0 : (x < -708.0 ? 0.0 : v);
 }
 

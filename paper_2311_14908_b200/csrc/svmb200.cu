@@ -491,6 +491,15 @@ int solve(SolveArgs& a) {
     }
     P.timeout_ns = a.timeout_ns;
     if (const char* e = getenv("SVMB200_POLL_NS")) P.poll_ns = atoi(e);
+    // L2 residency of streamed X: keep the first tiles of every CTA block in L2
+    // (SVMB200_L2_KEEP_MB, per GPU; tuning)
+    if (!pl.resident && pl.bin_words == 0 && !gram) {
+        long long keep_mb = 0;
+        if (const char* e = getenv("SVMB200_L2_KEEP_MB")) keep_mb = atoll(e);
+        const long long tile_bytes = (long long)pl.d_pad * pl.rt * 4;
+        const long long ctas_here = (long long)a.ctas_per_rank * a.nranks_here;
+        if (keep_mb > 0 && tile_bytes > 0) P.l2_keep_tiles = (int)((keep_mb << 20) / (tile_bytes * ctas_here));
+    }
     P.sys_scope = a.mbox_local_alloc ? 0 : 1;
     const bool want_timers = getenv("SVMB200_PHASE_TIMERS") != nullptr;
     for (int r = 0; r < world; ++r) { P.row_off[r] = a.row_off[r]; P.n_rows[r] = (int)a.n_rows[r]; P.mbox[r] = a.mbox[r]; }
@@ -632,9 +641,9 @@ int solve(SolveArgs& a) {
         const char* nm[PH_N] = {"S.waitC", "S.publish", "S.poll", "S.select", "S.pivot", "S.kul",
                                 "C.waitA", "S.pollrounds", "C.dist", "C.waitB", "C.update", "C.reduce",
                                 "S.cand", "S.build"};
-        fprintf(stderr, "[svmb200] cycles/iter of CTA 0 over %lld iters (rpt=%d kc=%d stages=%d smem=%zu a_smem=%d resident=%d bin_words=%d cache=%d gram=%d cluster=%d):",
+        fprintf(stderr, "[svmb200] cycles/iter of CTA 0 over %lld iters (rpt=%d kc=%d stages=%d smem=%zu a_smem=%d resident=%d bin_words=%d cache=%d gram=%d cluster=%d l2keep=%d):",
                 hc.it, pl.rpt, pl.kc, pl.stages, pl.smem, (int)pl.alpha_smem, (int)pl.resident, pl.bin_words,
-                pl.cache_slots, gram ? 1 : 0, pl.cluster);
+                pl.cache_slots, gram ? 1 : 0, pl.cluster, P.l2_keep_tiles);
         for (int k = 0; k < PH_N; ++k)
             fprintf(stderr, " %s=%.0f", nm[k], hc.it ? (double)tm[k] / hc.it : 0.0);
         fprintf(stderr, "\n");

@@ -18,8 +18,12 @@ import paper_2311_14908_b200 as S  # noqa: E402
 from gen import workloads as W  # noqa: E402
 
 for spec in sys.argv[1:]:
-    name, _, mi = spec.partition(":")
+    name, _, rest = spec.partition(":")
+    mi, _, kern = rest.partition(":")          # W4:20000:lin -> the linear kernel on W4's data
     w = W.get(name)
+    if kern == "lin":
+        import dataclasses
+        w = dataclasses.replace(w, kernel=0)
     X, y = w.train()
     Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
     kw = dict(max_iter=int(mi)) if mi and int(mi) > 0 else {}
