@@ -48,6 +48,7 @@ constexpr int PRODUCER_WARP = NWC + 1;
 constexpr int NTHREADS = NT + 64;  // + scalar warp + producer warp
 constexpr int NSYNC = NT + 32;     // participants of the named barriers
 constexpr int MAX_STAGES = 16;
+constexpr int MIX_MAXSEG = 8;      // mixed rows: at most this many runs of continuous / binary columns
 enum { BAR_A = 1, BAR_B = 2, BAR_C = 3, BAR_D = 4 };
 
 enum { ST_RUNNING = 0, ST_CONVERGED = 1, ST_MAXITER = 2, ST_LIMIT = 3, ST_TIMEOUT = -8 };
@@ -132,6 +133,18 @@ struct Params {
     int crw;                       // cluster mode: 16-byte words per record (4 + 2 ceil(crow/3))
     unsigned long long* timers;    // optional [8] per-phase cycle totals of CTA 0
     int poll_ns;                   // > 0: back-off between mailbox polls (tuning)
+    int dp;                        // dense pivot entries in shared memory (>= d; = d_pad unless mixed)
+    // Mixed compact rows (SURVEY §8(f) compact encodings): the columns whose values are all
+    // exactly 0 or 1 are stored as bits, the others as fp32.  A row of xblk holds mix_nc fp32
+    // slots (the continuous columns in order) then mix_nbw bit words (the binary columns in
+    // order).  mix_seg lists the runs of the original column order: > 0 = that many
+    // continuous columns, < 0 = that many binary columns.  A binary column adds a term of
+    // exactly 0 or 1 to the R13 recurrence, so a run adds 1.0 popcount times -- the same
+    // roundings as the dense recurrence.  mix_map[i]: original column of continuous slot i
+    // (i < mix_nc) / of binary bit i - mix_nc.
+    int mix_nseg, mix_nc, mix_nbw;
+    int mix_seg[MIX_MAXSEG];
+    const int* mix_map;
     int l2_keep_tiles;             // streamed X: tiles [0, l2_keep_tiles) of every CTA block are
                                    // copied with an L2 evict_last policy, the rest evict_first, so
                                    // that part of X stays in L2 across iterations (0 = no hints)
@@ -430,6 +443,82 @@ __device__ __forceinline__ double kcache_at(const Params& P, int s, long long g)
     return __ldcg(P.cache[r] + (long long)s * P.n_rows[r] + (g - P.row_off[r]));
 }
 
+// The RPT rows t*RPT .. t*RPT+RPT-1 of slot (feature) i of a stage [slots][rp]
+template <int RPT>
+__device__ __forceinline__ void load_slot(const float* st, int rp, int i, int t, uint32_t (&v)[RPT]) {
+    if (RPT == 4) {
+        const uint4 w = reinterpret_cast<const uint4*>(st + (size_t)i * rp)[t];
+        v[0] = w.x; v[1 % RPT] = w.y; v[2 % RPT] = w.z; v[3 % RPT] = w.w;
+    } else if (RPT == 2) {
+        const uint2 w = reinterpret_cast<const uint2*>(st + (size_t)i * rp)[t];
+        v[0] = w.x; v[1 % RPT] = w.y;
+    } else {
+        v[0] = reinterpret_cast<const uint32_t*>(st)[(size_t)i * rp + t];
+    }
+}
+// acc + 1.0, c times (the R13 terms of c binary columns whose term is 1), c >= 0: one add
+// when that add is exact and acc >= 0 (then every intermediate sum is exact too: they are
+// multiples of ulp(acc + c) no larger than it), else c sequential adds.
+__device__ __forceinline__ double add_ones(double acc, int c) {
+    const double cd = (double)c;
+    const double s = acc + cd;
+    const double bb = s - acc;
+    const double err = (acc - (s - bb)) + (cd - bb);
+    if (err == 0.0 && acc >= 0.0 && s < 9007199254740992.0) return s;
+    for (int i = 0; i < c; ++i) acc = acc + 1.0;
+    return acc;
+}
+// Mixed compact rows (Params::mix_*): the R13 recurrence of RPT rows against both pivots,
+// run by run in the original column order.
+template <int KERNEL, int RPT>
+__device__ __forceinline__ void mixed_rows(const Params& P, const float* st, int rp, int t,
+                                           const double2* pivm, const uint32_t* pbits,
+                                           double (&du)[RPT], double (&dl)[RPT]) {
+    int ci = 0, bb = 0;
+    for (int sg = 0; sg < P.mix_nseg; ++sg) {
+        const int len = P.mix_seg[sg];
+        if (len > 0) {
+#pragma unroll 2
+            for (int i = ci; i < ci + len; ++i) {
+                uint32_t v[RPT];
+                load_slot<RPT>(st, rp, i, t, v);
+                const double2 pv = pivm[i];
+#pragma unroll
+                for (int q = 0; q < RPT; ++q) {
+                    const double x = (double)__uint_as_float(v[q]);
+                    if (KERNEL == 1) {
+                        double e = x - pv.x; du[q] = fma(e, e, du[q]);
+                        e = x - pv.y; dl[q] = fma(e, e, dl[q]);
+                    } else {
+                        du[q] = fma(x, pv.x, du[q]); dl[q] = fma(x, pv.y, dl[q]);
+                    }
+                }
+            }
+            ci += len;
+        } else {
+            const int nb = -len;
+            int cu[RPT], cl[RPT];
+#pragma unroll
+            for (int q = 0; q < RPT; ++q) { cu[q] = 0; cl[q] = 0; }
+            for (int w = bb >> 5; w <= (bb + nb - 1) >> 5; ++w) {
+                const int lo = max(bb, 32 * w) - 32 * w, hi = min(bb + nb, 32 * w + 32) - 32 * w;
+                const uint32_t m = (hi - lo == 32) ? 0xffffffffu : (((1u << (hi - lo)) - 1u) << lo);
+                uint32_t v[RPT];
+                load_slot<RPT>(st, rp, P.mix_nc + w, t, v);
+                const uint32_t pu = pbits[w], pl = pbits[P.mix_nbw + w];
+#pragma unroll
+                for (int q = 0; q < RPT; ++q) {
+                    if (KERNEL == 1) { cu[q] += __popc((v[q] ^ pu) & m); cl[q] += __popc((v[q] ^ pl) & m); }
+                    else { cu[q] += __popc(v[q] & pu & m); cl[q] += __popc(v[q] & pl & m); }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < RPT; ++q) { du[q] = add_ones(du[q], cu[q]); dl[q] = add_ones(dl[q], cl[q]); }
+            bb += nb;
+        }
+    }
+}
+
 // BINCL: the kernel specialised for binary rows resident in a thread-block cluster (the
 // latency-bound small-problem path): the other modes compile out, so the per-iteration code
 // is short (instruction-cache resident).
@@ -445,7 +534,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
     Shared& sh = *reinterpret_cast<Shared*>(smem_raw);
     size_t off = (sizeof(Shared) + 127) & ~size_t(127);
     // pivots interleaved: piv[k] = (x_up[k], x_low[k]) -> one 16-byte broadcast load per k
-    double2* piv = reinterpret_cast<double2*>(smem_raw + off); off += (size_t)P.d_pad * 16;
+    double2* piv = reinterpret_cast<double2*>(smem_raw + off); off += (size_t)P.dp * 16;
+    // mixed rows: the pivots in the compact form (continuous pairs, then the bit words of
+    // x_up and of x_low)
+    const bool m_mixed = !BINCL && P.mix_nseg > 0;
+    double2* pivm = reinterpret_cast<double2*>(smem_raw + off);
+    if (m_mixed) off += (size_t)P.mix_nc * 16;
+    uint32_t* pbits = reinterpret_cast<uint32_t*>(smem_raw + off);
+    if (m_mixed) off += (((size_t)2 * P.mix_nbw * 4) + 15) & ~size_t(15);
     double* f_s = reinterpret_cast<double*>(smem_raw + off); off += (size_t)P.state_cap * 8;
     double* a_s = reinterpret_cast<double*>(smem_raw + off); if (A_SMEM) off += (size_t)P.state_cap * 8;
     uint8_t* fl_s = smem_raw + off; off += (size_t)P.state_cap;
@@ -462,7 +558,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
     // cache mode: the scalar warp compacts the k with a non-zero term of K(x_u, x_l) here
     off = (off + 15) & ~size_t(15);
     double2* kul_t = reinterpret_cast<double2*>(smem_raw + off);
-    if (m_cache > 0) off += (size_t)P.d_pad * 16;
+    if (m_cache > 0) off += (size_t)P.dp * 16;
     // cluster mode: records of the rank's CTAs, cmb[parity][cta][crw] (written remotely)
     uint4* cmb = reinterpret_cast<uint4*>(smem_raw + off);
     if (m_cluster) off += (size_t)2 * P.ctas_per_rank * P.crw * 16;
@@ -927,7 +1023,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
             } else {
                 const float* xu_g = xr + (long long)iu * P.d;
                 const float* xl_g = xr + (long long)il * P.d;
-                for (int k0 = 0; k0 < P.d_pad; k0 += 32 * 8) {
+                for (int k0 = 0; k0 < P.dp; k0 += 32 * 8) {
                     float vu[8], vl[8];
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
@@ -938,7 +1034,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
                         const int k = k0 + 32 * q + lane;
-                        if (k < P.d_pad) piv[k] = make_double2((double)vu[q], (double)vl[q]);
+                        if (k < P.dp) piv[k] = make_double2((double)vu[q], (double)vl[q]);
+                    }
+                }
+                if (m_mixed) {
+                    // compact pivots: continuous columns in order, binary columns as bit words
+                    __syncwarp();
+                    for (int i = lane; i < P.mix_nc; i += 32) pivm[i] = piv[__ldg(&P.mix_map[i])];
+                    const int nbin = P.d - P.mix_nc;
+                    for (int w = 0; w < P.mix_nbw; ++w) {
+                        const int b = 32 * w + lane;
+                        const double2 pv = b < nbin ? piv[__ldg(&P.mix_map[P.mix_nc + b])] : make_double2(0.0, 0.0);
+                        const unsigned mu = __ballot_sync(0xffffffffu, pv.x != 0.0);
+                        const unsigned ml = __ballot_sync(0xffffffffu, pv.y != 0.0);
+                        if (lane == 0) { pbits[w] = mu; pbits[P.mix_nbw + w] = ml; }
                     }
                 }
             }
@@ -1205,7 +1314,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                 if (!m_resident) mbar_wait(&full[cslot], cpar);
                 const float* st = m_resident ? ring + (size_t)ch * P.kc * rp : ring + (size_t)cslot * stage_floats;
                 const int k0 = ch * P.kc;
-                if (active) {
+                if (active && m_mixed) {
+                    mixed_rows<KERNEL, RPT>(P, st, rp, t, pivm, pbits, du, dl);
+                } else if (active) {
                     if (RPT == 4) {
                         const float4* sp = reinterpret_cast<const float4*>(st) + t;
                         const int ld4 = rp >> 2;

@@ -1,5 +1,6 @@
 // svm_internal.h -- shared declarations of the host driver (not part of the ABI).
 #pragma once
+#include <vector>
 
 #include <cuda_runtime.h>
 
@@ -63,6 +64,7 @@ struct SolveArgs {
     bool independent = false;                  // batched independent problems (one per rank)
     const float* xr_rank[svmk::MAXR] = {};
     long long max_iter_rank[svmk::MAXR] = {};
+    std::vector<int> mix_map;                  // (set by solve) mixed compact rows: column map
     SolveOut out;                              // rank_base's result
     SolveOut out_rank[svmk::MAXR];             // every served rank (independent mode)
 };

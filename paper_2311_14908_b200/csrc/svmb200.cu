@@ -67,6 +67,47 @@ __global__ void k_count_nonbinary(const float* __restrict__ X, long long nx, uns
     if (c) atomicAdd(out, c);
 }
 
+// per column: 1 if some value is not exactly 0 or 1 (racy stores of the same value)
+__global__ void k_col_nonbinary(const float* __restrict__ X, long long n, int d, int* __restrict__ nb) {
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n * d; e += (long long)gridDim.x * blockDim.x) {
+        const float v = X[e];
+        if (v != 0.0f && v != 1.0f) nb[e % d] = 1;
+    }
+}
+
+// Mixed compact rows (Params::mix_*): the CTA-blocked layout of k_build_xblk over d_pad
+// 32-bit slots per row -- slot i < nc: X[row][map[i]] (fp32), slot nc + w: bit b of word w
+// = X[row][map[nc + 32 w + b]] != 0 -- zero padded.
+__global__ void k_build_xblk_mixed(const float* __restrict__ X, long long n_r, int d, const int* __restrict__ map,
+                                   int nc, int nbw, int d_pad, int G, int rt, long long cta_stride,
+                                   float* __restrict__ xblk) {
+    const int c = blockIdx.y;
+    const long long r0 = (n_r * c) / G, r1 = (n_r * (c + 1)) / G;
+    const long long R = r1 - r0;
+    const long long total = R * d_pad;
+    const int nbin = d - nc;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long k = e / R;
+        const long long j = e - k * R;
+        const long long tile = j / rt, rin = j - tile * rt;
+        const long long rows_t = (R - tile * rt) < rt ? (R - tile * rt) : rt;
+        const long long rp = (rows_t + 3) & ~3ll;
+        const float* row = X + (r0 + j) * d;
+        uint32_t v = 0u;
+        if (k < nc) {
+            v = __float_as_uint(row[map[k]]);
+        } else if (k < nc + nbw) {
+            const int w = (int)(k - nc);
+            for (int b = 0; b < 32; ++b) {
+                const int i = 32 * w + b;
+                if (i < nbin && row[map[nc + i]] != 0.0f) v |= 1u << b;
+            }
+        }
+        xblk[(long long)c * cta_stride + tile * (long long)d_pad * rt + k * rp + rin] = __uint_as_float(v);
+    }
+}
+
 // bit rows: bit k of word k/32 of row r = X[r][k]
 __global__ void k_pack_bits(const float* __restrict__ X, long long n, int d, int W, uint32_t* __restrict__ out) {
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n * W; e += (long long)gridDim.x * blockDim.x) {
@@ -177,13 +218,21 @@ struct Plan {
     int cluster = 0;  // > 0: cluster mode with G CTAs per cluster (one cluster per rank)
     bool bincl = false;  // cluster mode on binary rows: the smo_bincl kernel (NTB threads)
     int crow = 0, crw = 0;
+    int dp = 0;          // dense pivot entries (shared memory)
+    int mix_nc = 0, mix_nbw = 0, mix_nseg = 0;   // mixed compact rows (mix_nseg > 0)
+    int mix_seg[MIX_MAXSEG] = {};
     long long cta_stride = 0;
     size_t smem = 0;
 };
 
 int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl, bool binary = false,
-              bool gram = false, int cache_slots = 0, int cl_words = 0) {
+              bool gram = false, int cache_slots = 0, int cl_words = 0, const Plan* mix = nullptr) {
     pl.G = G;
+    pl.dp = 0;
+    if (mix) {
+        pl.mix_nc = mix->mix_nc; pl.mix_nbw = mix->mix_nbw; pl.mix_nseg = mix->mix_nseg;
+        for (int i = 0; i < MIX_MAXSEG; ++i) pl.mix_seg[i] = mix->mix_seg[i];
+    }
     // cluster mode: the shared-memory mailbox cmb[2][G][cl_words] of 16-byte words
     const size_t cl_bytes = cl_words > 0 ? (size_t)2 * G * cl_words * 16 + 16 : 0;
     if (gram) {
@@ -240,15 +289,25 @@ int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl, bool bina
     }
     pl.d_pad = (d + pl.kc - 1) / pl.kc * pl.kc;
     pl.n_chunks = pl.d_pad / pl.kc;
+    pl.dp = pl.d_pad;
+    size_t mix_bytes = 0;
+    if (pl.mix_nseg > 0) {
+        // one stage holds whole compact rows: nc fp32 slots + nbw bit words
+        pl.kc = (pl.mix_nc + pl.mix_nbw + 3) & ~3;
+        pl.d_pad = pl.kc;
+        pl.n_chunks = 1;
+        pl.dp = (d + 3) & ~3;
+        mix_bytes = (size_t)pl.mix_nc * 16 + (((size_t)2 * pl.mix_nbw * 4 + 15) & ~size_t(15));
+    }
     const int n_tiles = (pl.state_cap + pl.rt - 1) / pl.rt;
     pl.cta_stride = (long long)n_tiles * pl.d_pad * pl.rt;
     pl.alpha_smem = pl.state_cap <= 2048;                  // else alpha stays in HBM
     size_t fixed = (sizeof(Shared) + 127) & ~size_t(127);
-    fixed += 2 * (size_t)pl.d_pad * 8 + (size_t)pl.state_cap * (pl.alpha_smem ? 17 : 9);  // pivots + state
+    fixed += 2 * (size_t)pl.dp * 8 + mix_bytes + (size_t)pl.state_cap * (pl.alpha_smem ? 17 : 9);  // pivots + state
     int hash = 0;
     if (cache_slots > 0) { hash = 1; while (hash < 2 * cache_slots) hash <<= 1; }
     fixed = ((fixed + 7) & ~size_t(7)) + (size_t)cache_slots * 4;                       // cache directory
-    fixed = ((fixed + 7) & ~size_t(7)) + (size_t)hash * 8 + (cache_slots > 0 ? (size_t)pl.d_pad * 16 + 8 : 0);
+    fixed = ((fixed + 7) & ~size_t(7)) + (size_t)hash * 8 + (cache_slots > 0 ? (size_t)pl.dp * 16 + 8 : 0);
     pl.cache_hash = hash;
     fixed += cl_bytes;
     fixed = (fixed + 127) & ~size_t(127);
@@ -349,9 +408,53 @@ int solve(SolveArgs& a) {
             return rc;
         }
     } else if (!binary) {
+        // mixed compact rows: binary columns as bits when that shrinks the rows (>= 32 of
+        // them, at most MIX_MAXSEG runs of the column order)
+        Plan mix;
+        std::vector<int> mix_map;
+        if (!a.independent && getenv("SVMB200_NO_MIXED") == nullptr && a.d >= 32) {
+            int* dnb = nullptr;
+            CKR(cudaMallocAsync(&dnb, (size_t)a.d * 4, a.stream));
+            CKR(cudaMemsetAsync(dnb, 0, (size_t)a.d * 4, a.stream));
+            k_col_nonbinary<<<1024, 256, 0, a.stream>>>(a.xr, a.n_global, (int)a.d, dnb);
+            counted();
+            std::vector<int> nb((size_t)a.d);
+            CKR(cudaMemcpyAsync(nb.data(), dnb, (size_t)a.d * 4, cudaMemcpyDeviceToHost, a.stream));
+            CKR(cudaFreeAsync(dnb, a.stream));
+            CKR(cudaStreamSynchronize(a.stream));
+            int nbin = 0, nseg = 0, prev = -1;
+            for (long long k = 0; k < a.d; ++k) {
+                const int isbin = nb[k] == 0;
+                nbin += isbin;
+                if (isbin != prev) { ++nseg; prev = isbin; }
+            }
+            const int nc = (int)a.d - nbin, nbw = (nbin + 31) / 32;
+            if (nbin >= 32 && nseg <= MIX_MAXSEG && 4 * (nc + nbw) <= 3 * a.d) {
+                mix.mix_nc = nc; mix.mix_nbw = nbw; mix.mix_nseg = nseg;
+                int sg = -1;
+                prev = -1;
+                for (long long k = 0; k < a.d; ++k) {
+                    const int isbin = nb[k] == 0;
+                    if (isbin != prev) { ++sg; prev = isbin; }
+                    mix.mix_seg[sg] += isbin ? -1 : 1;
+                }
+                for (long long k = 0; k < a.d; ++k) if (nb[k]) mix_map.push_back((int)k);
+                for (long long k = 0; k < a.d; ++k) if (!nb[k]) mix_map.push_back((int)k);
+            }
+        }
         pl = Plan();
-        rc = make_plan(a.n_rows_max, (int)a.d, a.ctas_per_rank, a.max_smem, pl);
-        if (rc) return rc;
+        if (mix.mix_nseg > 0) {
+            if (make_plan(a.n_rows_max, (int)a.d, a.ctas_per_rank, a.max_smem, pl, false, false, 0, 0, &mix) != SVM_OK) {
+                mix = Plan();
+                mix_map.clear();
+                pl = Plan();
+            }
+        }
+        if (mix.mix_nseg == 0) {
+            rc = make_plan(a.n_rows_max, (int)a.d, a.ctas_per_rank, a.max_smem, pl);
+            if (rc) return rc;
+        }
+        a.mix_map = mix_map;
         // kernel-row LRU cache (a8) for streamed X
         int slots = a.p.cache_rows;
         if (slots == 0 && !pl.resident && !a.independent && a.n_global <= 200000) {
@@ -365,7 +468,8 @@ int solve(SolveArgs& a) {
         if (slots > 0 && !pl.resident) {
             if (slots < 4) slots = 4;
             Plan pc;
-            if (make_plan(a.n_rows_max, (int)a.d, a.ctas_per_rank, a.max_smem, pc, false, false, slots) == SVM_OK &&
+            if (make_plan(a.n_rows_max, (int)a.d, a.ctas_per_rank, a.max_smem, pc, false, false, slots, 0,
+                          pl.mix_nseg > 0 ? &pl : nullptr) == SVM_OK &&
                 !pc.resident) {
                 pl = pc;
                 pl.cache_slots = slots;
@@ -377,7 +481,7 @@ int solve(SolveArgs& a) {
     // shared memory (~0.2 us) instead of global-memory mailboxes (~2.5 us); the candidates'
     // rows travel in the records.  Auto: the smallest power-of-two cluster with <= 2048 rows
     // per CTA (else 16 CTAs if <= 8192 rows each), when it is resident.
-    const bool cl_allowed = gram == nullptr && pl.cache_slots == 0 && a.p.cluster != -1 &&
+    const bool cl_allowed = gram == nullptr && pl.cache_slots == 0 && pl.mix_nseg == 0 && a.p.cluster != -1 &&
                             a.world == a.nranks_here && (a.world == 1 || a.independent) &&
                             (a.p.ctas <= 0 || a.p.cluster > 0) && getenv("SVMB200_NO_CLUSTER") == nullptr;
     if (a.p.cluster > 16 || a.p.cluster < -1) return fail(SVM_EINVAL, "cluster must be -1, 0 or 1..16");
@@ -432,6 +536,7 @@ int solve(SolveArgs& a) {
     const int nthreads = pl.bincl ? NTB : NTHREADS;
     {
         const char* mode = gram ? "gram" : pl.bin_words ? "binary-resident"
+                         : pl.mix_nseg ? (pl.resident ? "mixed-resident" : pl.cache_slots ? "mixed+row-cache" : "mixed-streamed")
                          : pl.resident ? "float-resident" : pl.cache_slots ? "streamed+row-cache" : "streamed";
         char buf[320];
         snprintf(buf, sizeof buf,
@@ -478,6 +583,9 @@ int solve(SolveArgs& a) {
     P.n_global = a.n_global; P.xr = a.xr; P.cta_stride = pl.cta_stride;
     P.check_interval = p.check_interval; P.state_cap = pl.state_cap; P.resident = pl.resident ? 1 : 0;
     P.bin_words = pl.bin_words;
+    P.dp = pl.dp > 0 ? pl.dp : pl.d_pad;
+    P.mix_nseg = pl.mix_nseg; P.mix_nc = pl.mix_nc; P.mix_nbw = pl.mix_nbw;
+    for (int i = 0; i < MIX_MAXSEG; ++i) P.mix_seg[i] = pl.mix_seg[i];
     P.gram = gram;
     P.cache_slots = pl.cache_slots;
     P.cache_hash = pl.cache_hash;
@@ -493,7 +601,7 @@ int solve(SolveArgs& a) {
     if (const char* e = getenv("SVMB200_POLL_NS")) P.poll_ns = atoi(e);
     // L2 residency of streamed X: keep the first tiles of every CTA block in L2
     // (SVMB200_L2_KEEP_MB, per GPU; tuning)
-    if (!pl.resident && pl.bin_words == 0 && !gram) {
+    if (!pl.resident && pl.bin_words == 0 && !gram && pl.mix_nseg == 0) {
         long long keep_mb = 0;
         if (const char* e = getenv("SVMB200_L2_KEEP_MB")) keep_mb = atoll(e);
         const long long tile_bytes = (long long)pl.d_pad * pl.rt * 4;
@@ -504,6 +612,12 @@ int solve(SolveArgs& a) {
     const bool want_timers = getenv("SVMB200_PHASE_TIMERS") != nullptr;
     for (int r = 0; r < world; ++r) { P.row_off[r] = a.row_off[r]; P.n_rows[r] = (int)a.n_rows[r]; P.mbox[r] = a.mbox[r]; }
 
+    if (pl.mix_nseg > 0) {
+        int* dm;
+        if ((rc = dalloc((void**)&dm, a.mix_map.size() * 4))) { release(); return rc; }
+        CKR(cudaMemcpyAsync(dm, a.mix_map.data(), a.mix_map.size() * 4, cudaMemcpyHostToDevice, st));
+        P.mix_map = dm;
+    }
     for (int r = a.rank_base; r < a.rank_base + a.nranks_here; ++r) {
         const long long nr = a.n_rows[r];
         float* xb; double* f; double* al; uint8_t* fl; Ctl* ctl;
@@ -534,6 +648,10 @@ int solve(SolveArgs& a) {
             k_build_xbits<<<bg, 256, 0, st>>>(P.xrbits + a.row_off[r] * pl.bin_words, nr, pl.bin_words,
                                                (pl.bin_words + 3) & ~3, pl.G, pl.cta_stride,
                                                reinterpret_cast<uint32_t*>(xb));
+        } else if (pl.mix_nseg > 0) {
+            counted(2);   // build + init_state below
+            k_build_xblk_mixed<<<bg, 256, 0, st>>>(a.x_rank[r], nr, (int)a.d, P.mix_map, pl.mix_nc, pl.mix_nbw,
+                                                   pl.d_pad, pl.G, pl.rt, pl.cta_stride, xb);
         } else {
             counted(2);   // build + init_state below
             k_build_xblk<<<bg, 256, 0, st>>>(a.x_rank[r], nr, (int)a.d, pl.d_pad, pl.G, pl.rt, pl.cta_stride, xb);

@@ -460,3 +460,61 @@ def test_row_cache_with_virtual_ranks(S, monkeypatch):
     X, y = w.train(2500)
     r_g, r_or = _run_pair(S, w, X, y, cache_rows=32, virtual_ranks=3)
     _assert_exact(r_g, r_or)
+
+
+def _mixed_data(rng, n, runs):
+    """Columns in runs of continuous (Gaussian, some negative, some exact 0/1 values
+    mixed in) and binary (exactly 0/1) features, in the given order."""
+    cols = []
+    for kind, k in runs:
+        if kind == "c":
+            c = rng.normal(0.3, 0.6, (n, k)).astype(np.float32)
+            c[rng.random((n, k)) < 0.2] = 1.0             # 0/1 values inside a continuous column
+            c[rng.random((n, k)) < 0.2] = 0.0
+            cols.append(c)
+        else:
+            cols.append((rng.random((n, k)) < 0.15).astype(np.float32))
+    X = np.ascontiguousarray(np.concatenate(cols, axis=1))
+    s = X[:, :3].sum(1) - X[:, -3:].sum(1) + 0.4 * rng.normal(size=n)
+    y = np.where(s > np.median(s), 1, -1).astype(np.int8)
+    return X, y
+
+
+@pytest.mark.parametrize("runs,kern,gamma", [
+    ((("c", 10), ("b", 44)), O.RBF, 1 / 54),                       # covtype-like order
+    ((("c", 5), ("b", 40), ("c", 3), ("b", 33)), O.RBF, 0.05),     # interleaved runs, words split
+    ((("b", 70), ("c", 6)), O.RBF, 0.1),                            # binary first: integral sums
+    ((("c", 7), ("b", 36), ("c", 2)), O.LINEAR, 0.0),               # linear, negative partial sums
+])
+def test_mixed_rows_parity(S, monkeypatch, runs, kern, gamma):
+    """Mixed compact rows (binary columns as bits, the rest fp32) equal
+    the oracle and the dense fp32 path bit for bit, for several RPT values, virtual
+    ranks and the row cache."""
+    rng = np.random.default_rng(sum(k for _, k in runs))
+    n = 2311
+    X, y = _mixed_data(rng, n, runs)
+    d = X.shape[1]
+    w = W.Workload("mix", "", n, d, kern, gamma, 2.0, 1e-3, 0, 0, 0, None)
+    r_or = O.train(X, y, w.C, w.kernel, w.gamma, w.tol, trace_cap=100000)
+    r_g = S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol, want_f=True, trace_cap=100000, cluster=-1)
+    assert S.last_plan()["mode"].startswith("mixed")
+    _assert_exact(r_g, r_or)
+    for rpt in ("1", "2"):
+        monkeypatch.setenv("SVMB200_RPT", rpt)
+        r2 = S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol, want_f=True, cluster=-1, ctas=37)
+        _assert_exact(r2, r_or)
+    monkeypatch.delenv("SVMB200_RPT")
+    r3 = S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol, want_f=True, virtual_ranks=3)
+    _assert_exact(r3, r_or)
+    monkeypatch.setenv("SVMB200_NO_RESIDENT", "1")          # streamed stages, with / without cache
+    r4 = S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol, want_f=True, cache_rows=16, cluster=-1)
+    assert S.last_plan()["mode"] == "mixed+row-cache"
+    _assert_exact(r4, r_or)
+    r6 = S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol, want_f=True, cache_rows=-1, cluster=-1)
+    assert S.last_plan()["mode"] == "mixed-streamed"
+    _assert_exact(r6, r_or)
+    monkeypatch.delenv("SVMB200_NO_RESIDENT")
+    monkeypatch.setenv("SVMB200_NO_MIXED", "1")
+    r5 = S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol, want_f=True, cluster=-1)
+    assert not S.last_plan()["mode"].startswith("mixed")
+    _assert_exact(r5, r_or)
