@@ -37,6 +37,10 @@
 namespace svmexp {
 
 #if defined(__CUDACC__)
+// fast-phase coefficients in the constant bank: DFMA takes them as c[][] operands directly
+// (as literals they cost two uniform moves each)
+__constant__ double c_IF_hi[16] = {SVM_EXP_IF_HI_INIT};
+__constant__ double c_RED[4] = {SVM_EXP_INV_L32, SVM_EXP_L32_1, SVM_EXP_L32_2, SVM_EXP_L32_3};
 __device__ const double d_T_hi[32] = {SVM_EXP_T_HI_INIT};
 __device__ const double d_T_lo[32] = {SVM_EXP_T_LO_INIT};
 __device__ const double d_IF_hi[16] = {SVM_EXP_IF_HI_INIT};
@@ -101,6 +105,16 @@ SVM_HD bool rounding_safe(double hi, double lo, int shift) {
     return fabs(fabs(lo) - g) > margin;
 }
 
+// The same test for 0.98 <= hi < 2 (the fast phase's R before scaling) in plain fp64
+// compares: half an ulp of hi is 2^-53 in [1, 2) and 2^-54 below 1 -- also when hi = 1 and
+// lo < 0, the one power of two in range -- and the margin is 2^-67 / 2^-68 (shift 67).
+SVM_HD bool rounding_safe_r(double hi, double lo) {
+    const bool up = hi >= 1.0;
+    const double g = (hi > 1.0 || (hi == 1.0 && lo >= 0.0)) ? 0x1p-53 : 0x1p-54;
+    const double margin = up ? 0x1p-67 : 0x1p-68;
+    return fabs(fabs(lo) - g) > margin;
+}
+
 // Table accessors: host arrays, device global arrays (read-only path), or a caller-
 // provided pointer (e.g. a shared-memory copy laid out T_hi[32] T_lo[32] IF_hi[16] IF_lo[16]).
 struct HostTab {
@@ -141,25 +155,31 @@ constexpr int EXP_TABLE_DOUBLES = 96;
 // table 2^-106: < 2^-71 in all, against the 2^-67 margin of the rounding test.
 template <class Tab>
 SVM_HDM double exp_cr_fast(double x, const Tab& tab, bool& safe) {
+#if defined(__CUDA_ARCH__)
+    const double* IFH = c_IF_hi;
+    const double INV_L32 = c_RED[0], L32_1 = c_RED[1], L32_2 = c_RED[2], L32_3 = c_RED[3];
+#else
+    constexpr double IFH[16] = {SVM_EXP_IF_HI_INIT};
+    const double INV_L32 = SVM_EXP_INV_L32, L32_1 = SVM_EXP_L32_1, L32_2 = SVM_EXP_L32_2, L32_3 = SVM_EXP_L32_3;
+#endif
     const bool special = (x == 0.0) || (x < -708.0);
     const double xc = special ? -1.0 : x;
     // N = nearest integer to x 32/ln2 by the 1.5 2^52 shift (exact: |N| < 2^16); the low
     // word of the shifted value is N as a 32-bit integer
     const double SH = 0x1.8p52;
-    const double tN = fma(xc, SVM_EXP_INV_L32, SH);
+    const double tN = fma(xc, INV_L32, SH);
     const double N = tN - SH;
     const int Ni = (int)(uint32_t)bits_of(tN);
     const int j = Ni & 31;
     const int k = Ni >> 5;                                 // floor(N / 32)
     // r = x - N ln2/32 = rh + rl
-    const double r1 = fma(-N, SVM_EXP_L32_1, xc);          // exact (Sterbenz, 38-bit L1)
-    const double p2h = N * SVM_EXP_L32_2;
-    const double p2l = fma(N, SVM_EXP_L32_2, -p2h);
+    const double r1 = fma(-N, L32_1, xc);          // exact (Sterbenz, 38-bit L1)
+    const double p2h = N * L32_2;
+    const double p2l = fma(N, L32_2, -p2h);
     const dd s = two_sum(r1, -p2h);
     const double rh = s.hi;
-    const double rl = fma(-N, SVM_EXP_L32_3, s.lo - p2l);
+    const double rl = fma(-N, L32_3, s.lo - p2l);
     // exp(r) - 1 = qh + ql:  rh + rh^2/2 (error-free), + rl (1 + rh) + rh^3 P(rh)
-    constexpr double IFH[16] = {SVM_EXP_IF_HI_INIT};
     const double sqh = rh * rh, sql = fma(rh, rh, -sqh);
     const double h = 0.5 * sqh;
     const double qh = rh + h;                              // fast two-sum: |rh| >= |h|
@@ -186,7 +206,7 @@ SVM_HDM double exp_cr_fast(double x, const Tab& tab, bool& safe) {
                            Rl * from_bits((uint64_t)(k + 1023) << 52),
                            !rounding_safe(Rh, Rl, 67));
 #endif
-    safe = special || rounding_safe(Rh, Rl, 67);
+    safe = special || rounding_safe_r(Rh, Rl);
     const double scale = from_bits((uint64_t)(k + 1023) << 52);  // k >= -1022: normal
     const double v = Rh * scale;
     return x == 0.0 ? 1.0 : (x < -708.0 ? 0.0 : v);
