@@ -60,6 +60,8 @@ def lib():
             L.oracle_dual_objective.argtypes = [P, P, P, i64, i64, i32, f64]
             L.oracle_dual_objective.restype = f64
             L.oracle_num_threads.restype = i32
+            L.oracle_gd_train.argtypes = [P, P, i64, i64, f64, i32, f64, f64, i64, P, P, P, P]
+            L.oracle_gd_train.restype = i32
             _lib = L
     return _lib
 
@@ -163,3 +165,26 @@ def dual_objective(X, y, alpha, kernel: int, gamma: float = 0.0) -> float:
 def dual_objective_from_f(alpha, y, f) -> float:
     """W = 1/2 sum_i alpha_i (1 - y_i f_i)  (identity from the f definition)."""
     return 0.5 * float(np.sum(np.asarray(alpha) * (1.0 - np.asarray(y, dtype=np.float64) * np.asarray(f))))
+
+
+class GdResult:
+    def __init__(self, alpha, g, b, W):
+        self.alpha, self.g, self.b, self.W = alpha, g, b, W
+
+
+def gd_train(X, y, C: float, kernel: int, gamma: float, lr: float, epochs: int) -> GdResult:
+    """Projected-gradient dual trainer (oracle_gd_train): alpha after `epochs` epochs,
+    g = K (alpha o y) of the final alpha, bias b (R25) and W(alpha)."""
+    X = _f32(X)
+    y = np.ascontiguousarray(y, dtype=np.int8)
+    n, d = X.shape
+    alpha = np.zeros(n)
+    g = np.zeros(n)
+    b = ctypes.c_double()
+    W = ctypes.c_double()
+    rc = lib().oracle_gd_train(_p(X), _p(y), n, d, float(C), int(kernel), float(gamma), float(lr),
+                               int(epochs), _p(alpha), _p(g), ctypes.byref(b), ctypes.byref(W))
+    if rc:
+        raise MemoryError("oracle_gd_train: allocation failed")
+    return GdResult(alpha, g, b.value, W.value)
+

@@ -23,7 +23,8 @@
  * Pins (tests/test_oracle_*.py): closed-form two/three-point duals, RBF two-point,
  * eta = 0 duplicates, separable toy with known margin, brute-force active-set QP,
  * KKT at convergence, invariants per step, mpmath-rounded exp; the second-order working
- * set (oracle_select_second_order, wss = 2) against scikit-learn's libsvm.
+ * set (oracle_select_second_order, wss = 2) against scikit-learn's libsvm; the projected-GD
+ * trainer (oracle_gd_train) against a brute-force box-constrained QP and closed forms.
  */
 #include <math.h>
 #include <stdint.h>
@@ -339,4 +340,74 @@ int oracle_svm_train(const float* X, const int8_t* y, int64_t n, int64_t d, doub
     return oracle_svm_train_wss(X, y, n, d, C, kernel, gamma, tol, max_iter, alpha0, f0, alpha, f,
                                 b_out, iters_out, converged_out, b_up_out, b_low_out, pair_trace,
                                 trace_cap, 1);
+}
+
+/* ---------------------------------------------------------------- projected-GD dual trainer
+ * The paper's TensorFlow path (§3.3, Fig. 5: "describing the Gaussian RBF kernel
+ * function ... declaring the gradient descent optimizer algorithm") read as full-batch
+ * projected gradient ascent on the same dual W(alpha) (DESIGN.md
+ * readings R23-R26), step by step:
+ *   alpha^0 = 0
+ *   epoch:  v_j = alpha_j y_j
+ *           g_i = sum_j K_ij v_j            (ascending j, one fma per term)       R24
+ *           grad_i = 1 - y_i g_i            (dW/dalpha_i)
+ *           alpha_i <- min(C, max(0, fma(lr, grad_i, alpha_i)))  (box projection)  R23
+ *   after the last epoch g = K (alpha o y) for the final alpha, and
+ *   b = mean over {1e-8 < alpha_i < C - 1e-8} of (y_i - g_i)  (ascending i)        R25
+ *       else -(max g_i + min g_i)/2 over {alpha_i > 1e-8}, else over all i
+ *   W = sum alpha_i - 1/2 sum_i v_i g_i
+ * K is the full kernel matrix of oracle_kernel (R13, R14, R16). */
+int oracle_gd_train(const float* X, const int8_t* y, int64_t n, int64_t d, double C, int kernel,
+                    double gamma, double lr, int64_t epochs, double* alpha, double* g,
+                    double* b_out, double* W_out) {
+    oracle_init();
+    double* K = (double*)malloc((size_t)n * (size_t)n * sizeof(double));
+    double* v = (double*)malloc((size_t)n * sizeof(double));
+    double* an = (double*)malloc((size_t)n * sizeof(double));
+    if (!K || !v || !an) { free(K); free(v); free(an); return -5; }
+    #pragma omp parallel for schedule(static) if (n * n * d > 65536)
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t j = 0; j < n; ++j)
+            K[i * n + j] = oracle_kernel(kernel, gamma, X + i * d, X + j * d, d, i == j);
+    for (int64_t i = 0; i < n; ++i) alpha[i] = 0.0;
+    for (int64_t e = 0; e <= epochs; ++e) {
+        for (int64_t j = 0; j < n; ++j) v[j] = y[j] > 0 ? alpha[j] : -alpha[j];
+        #pragma omp parallel for schedule(static) if (n * n > 65536)
+        for (int64_t i = 0; i < n; ++i) {
+            double acc = 0.0;
+            for (int64_t j = 0; j < n; ++j) acc = fma(K[i * n + j], v[j], acc);
+            g[i] = acc;
+        }
+        if (e == epochs) break;                     /* the final pass only evaluates g */
+        for (int64_t i = 0; i < n; ++i) {
+            const double grad = 1.0 - (y[i] > 0 ? g[i] : -g[i]);
+            double a = fma(lr, grad, alpha[i]);
+            if (a < 0.0) a = 0.0;
+            if (a > C) a = C;
+            an[i] = a;
+        }
+        for (int64_t i = 0; i < n; ++i) alpha[i] = an[i];
+    }
+    const double eps = 1e-8;
+    double sum = 0.0;
+    int64_t cnt = 0;
+    for (int64_t i = 0; i < n; ++i)
+        if (alpha[i] > eps && alpha[i] < C - eps) { sum += (double)y[i] - g[i]; ++cnt; }
+    double b;
+    if (cnt > 0) {
+        b = sum / (double)cnt;
+    } else {
+        int any = 0;
+        for (int64_t i = 0; i < n; ++i) any |= alpha[i] > eps;
+        double mx = -INFINITY, mn = INFINITY;
+        for (int64_t i = 0; i < n; ++i)
+            if (!any || alpha[i] > eps) { if (g[i] > mx) mx = g[i]; if (g[i] < mn) mn = g[i]; }
+        b = -(mx + mn) / 2.0;
+    }
+    double lin = 0.0, quad = 0.0;
+    for (int64_t i = 0; i < n; ++i) { lin += alpha[i]; quad += v[i] * g[i]; }
+    *b_out = b;
+    *W_out = lin - 0.5 * quad;
+    free(K); free(v); free(an);
+    return 0;
 }
