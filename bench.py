@@ -331,8 +331,9 @@ def run_ours(args):
     streamed = None
     if world == 1 and not args.no_streamed:
         streamed = []
+        from gen import workloads as WL
         for name, k_it in (("W5", 1500), ("W4", 6000)):
-            ws = W.get(name)
+            ws = WL.get(name)
             Xs, ys = ws.train()
             Xs_d = torch.from_numpy(Xs).to(dev)
             ys_d = torch.from_numpy(ys).to(dev)
