@@ -180,6 +180,31 @@ int svm_train_shard(void* comm, const float* X_local, const int8_t* y_local, int
                     double* alpha_local, double* b, svm_info* info, void* cuda_stream);
 void svm_comm_destroy(void* comm);
 
+/* ---- projected-gradient dual trainer ------------------------
+ * The paper's TensorFlow path (§3.3, Fig. 5: "declaring the gradient descent
+ * optimizer algorithm") read as full-batch projected gradient ascent on the same dual W
+ * (R23-R26): from alpha = 0, `epochs` times
+ *     g = K (alpha o y)   (g_i summed in ascending j, one fma per term),
+ *     alpha_i <- min(C, max(0, fma(lr, 1 - y_i g_i, alpha_i))),
+ * then b = mean of y_i - g_i over 1e-8 < alpha_i < C - 1e-8 (else -(max g + min g)/2 over
+ * the alpha_i > 1e-8, else over all i) and W = sum alpha - 1/2 sum alpha_i y_i g_i for the
+ * final alpha.  The equality constraint sum alpha y = 0 is not enforced (box projection
+ * only).  K is the full fp64 kernel matrix (R13/R14/R16), built once in HBM (8 n^2 bytes;
+ * SVM_ENOMEM when it does not fit); every epoch streams it once.
+ * Device pointers X [n][d] float32 row-major, y int8 (+1/-1), alpha [n] out; b, info host
+ * out (info nullable).  lr > 0 finite, epochs >= 0.  Errors as svm_train_dev. */
+typedef struct {
+    double objective;        /* W(alpha) of the returned alpha */
+    double seconds_gram;     /* device time of building K */
+    double seconds_epochs;   /* device time of the epochs (+ the final evaluation pass) */
+    int64_t epochs;
+    int64_t gram_bytes;      /* bytes of K in HBM (column blocks of one CTA each, zero padded) */
+} svm_gd_info;
+
+int svm_train_gd_dev(const float* X, const int8_t* y, int64_t n, int64_t d, double C, int kernel,
+                     double gamma, double lr, int64_t epochs, double* alpha, double* b,
+                     svm_gd_info* info, void* cuda_stream);
+
 /* Number of CUDA kernels this library has launched from the calling thread so far
  * (validation, staging, the persistent solver launches, prediction). */
 int64_t svm_kernel_launches(void);

@@ -17,7 +17,7 @@ import numpy as np
 
 __all__ = ["LINEAR", "RBF", "PREDICT_EXACT", "PREDICT_TENSOR", "SvmError", "lib", "svm_train", "svm_train_ex", "svm_train_dev",
            "svm_predict", "svm_predict_dev", "svm_train_batch_dev", "svm_comm_unique_id", "svm_comm_init",
-           "svm_train_shard", "svm_comm_destroy", "Params", "Info", "version"]
+           "svm_train_shard", "svm_comm_destroy", "svm_train_gd_dev", "Params", "Info", "version"]
 
 LINEAR = 0
 RBF = 1
@@ -82,6 +82,7 @@ def lib():
         L.svm_comm_unique_id.argtypes = [P]
         L.svm_comm_init.argtypes = [ctypes.POINTER(ctypes.c_void_p), i32, i32, P, i32]
         L.svm_train_shard.argtypes = [P, P, P, i64, i64, i64, i64, P, P, P, P, P]
+        L.svm_train_gd_dev.argtypes = [P, P, i64, i64, f64, i32, f64, f64, i64, P, P, P, P]
         L.svm_comm_destroy.argtypes = [P]
         L.svm_comm_destroy.restype = None
         L.svm_last_error.restype = ctypes.c_char_p
@@ -90,7 +91,7 @@ def lib():
         L.svm_version.restype = ctypes.c_char_p
         for name in ("svm_train", "svm_train_ex", "svm_train_dev", "svm_predict", "svm_predict_dev",
                      "svm_predict_ex", "svm_predict_dev_ex", "svm_train_batch_dev",
-                     "svm_comm_unique_id", "svm_comm_init", "svm_train_shard"):
+                     "svm_comm_unique_id", "svm_comm_init", "svm_train_shard", "svm_train_gd_dev"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -207,6 +208,32 @@ def svm_train_dev(X, y, C: float, kernel: int, gamma: float = 0.0, tol: float = 
     if f is not None:
         out["f"] = f
     return out
+
+
+class GdInfo(ctypes.Structure):
+    _fields_ = [("objective", ctypes.c_double), ("seconds_gram", ctypes.c_double),
+                ("seconds_epochs", ctypes.c_double), ("epochs", ctypes.c_int64),
+                ("gram_bytes", ctypes.c_int64)]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+def svm_train_gd_dev(X, y, C: float, kernel: int, gamma: float, lr: float, epochs: int, stream=None):
+    """Projected-gradient dual trainer (C ABI svm_train_gd_dev): torch CUDA tensors
+    (X float32 [n, d] contiguous, y int8 [n]) -> dict(alpha tensor, b, info)."""
+    import torch
+    assert X.is_cuda and X.dtype == torch.float32 and X.is_contiguous()
+    assert y.is_cuda and y.dtype == torch.int8 and y.is_contiguous()
+    n, d = X.shape
+    alpha = torch.empty(n, dtype=torch.float64, device=X.device)
+    b = ctypes.c_double()
+    info = GdInfo()
+    _check(lib().svm_train_gd_dev(ctypes.c_void_p(X.data_ptr()), ctypes.c_void_p(y.data_ptr()), n, d,
+                                  float(C), int(kernel), float(gamma), float(lr), int(epochs),
+                                  ctypes.c_void_p(alpha.data_ptr()), ctypes.byref(b), ctypes.byref(info),
+                                  _stream_ptr(stream)))
+    return dict(alpha=alpha, b=b.value, info=info.as_dict())
 
 
 PREDICT_EXACT = 0

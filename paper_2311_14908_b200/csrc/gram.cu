@@ -1,6 +1,7 @@
 // gram.cu -- the full kernel matrix for the Gram path.
 //
-// K[i][j] = K(x_i, x_j) for all i, j < n, fp64, row-major [n][n], computed with the same
+// K[i][j] = K(x_i, x_j) for all i, j < n, fp64, row-major [n][ld] (or column-blocked for the
+// GD trainer, see gd.cu), computed with the same
 // arithmetic as the streaming row pass (R13: ascending-k fp64 recurrence, one fma per
 // term, from the fp32 inputs; R14: correctly rounded exp; R16: K_ii = 1), so a solve that
 // reads rows of K takes exactly the same decisions as one that recomputes them.  The
@@ -24,7 +25,7 @@ constexpr int GK = 32;    // features per slab
 
 template <int KERNEL>
 __global__ void __launch_bounds__(256) k_gram(const float* __restrict__ X, long long n, int d,
-                                              double gamma, double* __restrict__ K) {
+                                              double gamma, double* __restrict__ K, long long ld, int blk) {
     __shared__ double a[GK][GT + 1];
     __shared__ double b[GK][GT + 1];
     // blockIdx.x enumerates the upper-triangular tile pairs (bi <= bj)
@@ -74,21 +75,28 @@ __global__ void __launch_bounds__(256) k_gram(const float* __restrict__ X, long 
                 double v;
                 if (KERNEL == 1) v = (i == j) ? 1.0 : svmexp::exp_cr(-(gamma * acc[p][q]));
                 else v = acc[p][q];
-                K[i * n + j] = v;
-                K[j * n + i] = v;
+                if (blk > 0) {
+                    // column-blocked layout (gd.cu): K[r][c] at ((c / blk) n + r) blk + c % blk
+                    K[((j / blk) * n + i) * blk + (j % blk)] = v;
+                    K[((i / blk) * n + j) * blk + (i % blk)] = v;
+                } else {
+                    K[i * ld + j] = v;
+                    K[j * ld + i] = v;
+                }
             }
         }
 }
 
 int gram_device(const float* X, long long n, long long d, int kernel, double gamma, double* K,
-                cudaStream_t st) {
+                cudaStream_t st, long long ld, int blk) {
+    if (ld <= 0) ld = n;
     const long long nt = (n + GT - 1) / GT;
     const long long tiles = nt * (nt + 1) / 2;
     if (tiles > 0x7fffffffll) return fail(SVM_EINVAL, "Gram too large");
     if (kernel == SVM_RBF)
-        k_gram<1><<<(unsigned)tiles, 256, 0, st>>>(X, n, (int)d, gamma, K);
+        k_gram<1><<<(unsigned)tiles, 256, 0, st>>>(X, n, (int)d, gamma, K, ld, blk);
     else
-        k_gram<0><<<(unsigned)tiles, 256, 0, st>>>(X, n, (int)d, gamma, K);
+        k_gram<0><<<(unsigned)tiles, 256, 0, st>>>(X, n, (int)d, gamma, K, ld, blk);
     counted();
     CKR(cudaGetLastError());
     return SVM_OK;

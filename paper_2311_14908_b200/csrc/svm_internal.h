@@ -12,6 +12,7 @@
 namespace svmint {
 
 extern thread_local std::string g_err;
+extern thread_local std::string g_plan;            // svm_last_plan
 int fail(int code, const std::string& msg);
 // kernels this library launched from the calling thread (svm_kernel_launches)
 extern thread_local long long g_launches;
@@ -77,7 +78,7 @@ int solve(SolveArgs& a);
 
 // gram.cu: K[i][j] for all i, j < n (fp64, row-major), same arithmetic as the row pass
 int gram_device(const float* X, long long n, long long d, int kernel, double gamma, double* K,
-                cudaStream_t st);
+                cudaStream_t st, long long ld = 0, int blk = 0);
 
 // predict.cu
 int predict_device(const float* X_sv, const double* coef, long long n_sv, long long d, double b,
