@@ -145,6 +145,12 @@ struct Params {
     int mix_nseg, mix_nc, mix_nbw;
     int mix_seg[MIX_MAXSEG];
     const int* mix_map;
+    // Dictionary-coded rows (SURVEY §8(f) compact encodings: uint8 pixels): when X holds at
+    // most 256 distinct fp32 values, xblk stores one byte per element, the index of its
+    // value in dict (the values widened to fp64 exactly); the row pass looks the value up,
+    // so the arithmetic is the dense path's.  dict_n = 0: not dictionary-coded.
+    int dict_n;
+    const double* dict;
     int l2_keep_tiles;             // streamed X: tiles [0, l2_keep_tiles) of every CTA block are
                                    // copied with an L2 evict_last policy, the rest evict_first, so
                                    // that part of X stays in L2 across iterations (0 = no hints)
@@ -519,6 +525,32 @@ __device__ __forceinline__ void mixed_rows(const Params& P, const float* st, int
     }
 }
 
+// Dictionary-coded rows (Params::dict_n): the R13 recurrence of RPT rows over the kc
+// features of one stage [kc][rp] of byte codes; values from the fp64 dictionary.
+template <int KERNEL, int RPT>
+__device__ __forceinline__ void dict_rows(int kc, const unsigned char* stb, int rp, int t,
+                                          const double2* pv0, const double* dict,
+                                          double (&du)[RPT], double (&dl)[RPT]) {
+#pragma unroll 4
+    for (int kk = 0; kk < kc; ++kk) {
+        uint32_t w;
+        if (RPT == 4) w = reinterpret_cast<const uint32_t*>(stb + (size_t)kk * rp)[t];
+        else if (RPT == 2) w = reinterpret_cast<const uint16_t*>(stb + (size_t)kk * rp)[t];
+        else w = stb[(size_t)kk * rp + t];
+        const double2 pv = pv0[kk];
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+            const double x = dict[(w >> (8 * q)) & 0xffu];
+            if (KERNEL == 1) {
+                double e = x - pv.x; du[q] = fma(e, e, du[q]);
+                e = x - pv.y; dl[q] = fma(e, e, dl[q]);
+            } else {
+                du[q] = fma(x, pv.x, du[q]); dl[q] = fma(x, pv.y, dl[q]);
+            }
+        }
+    }
+}
+
 // BINCL: the kernel specialised for binary rows resident in a thread-block cluster (the
 // latency-bound small-problem path): the other modes compile out, so the per-iteration code
 // is short (instruction-cache resident).
@@ -542,6 +574,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
     if (m_mixed) off += (size_t)P.mix_nc * 16;
     uint32_t* pbits = reinterpret_cast<uint32_t*>(smem_raw + off);
     if (m_mixed) off += (((size_t)2 * P.mix_nbw * 4) + 15) & ~size_t(15);
+    // dictionary-coded rows: the values of the codes (fp64) and the element size of xblk
+    const bool m_dict = !BINCL && P.dict_n > 0;
+    const int esz = m_dict ? 1 : 4;
+    double* dict_s = reinterpret_cast<double*>(smem_raw + off);
+    if (m_dict) off += 256 * 8;
     double* f_s = reinterpret_cast<double*>(smem_raw + off); off += (size_t)P.state_cap * 8;
     double* a_s = reinterpret_cast<double*>(smem_raw + off); if (A_SMEM) off += (size_t)P.state_cap * 8;
     uint8_t* fl_s = smem_raw + off; off += (size_t)P.state_cap;
@@ -564,7 +601,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
     if (m_cluster) off += (size_t)2 * P.ctas_per_rank * P.crw * 16;
     off = (off + 127) & ~size_t(127);
     float* ring = reinterpret_cast<float*>(smem_raw + off);
-    const int stage_floats = P.kc * P.rt;
+    unsigned char* ring_b = smem_raw + off;
+    const int stage_floats = P.kc * P.rt;                    // elements per stage
     uint64_t* full = reinterpret_cast<uint64_t*>(sh.bars);
     uint64_t* empty = full + MAX_STAGES;
 
@@ -580,6 +618,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
     const int n_tiles = (R + P.rt - 1) / P.rt;
     const int rt_log2 = __ffs(P.rt) - 1;                     // rt = 256 RPT: a power of two
     const float* xcta = P.xblk[rank] + (long long)cta * P.cta_stride;
+    const unsigned char* xcta_b = reinterpret_cast<const unsigned char*>(P.xblk[rank]) + (long long)cta * P.cta_stride * esz;
     double* alpha_g = P.alpha[rank] + r0;                    // this CTA's alpha (global)
     const double C = P.C;
 
@@ -590,6 +629,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
     }
     for (int e = t; e < svmexp::EXP_TABLE_DOUBLES; e += NTHREADS) sh.exp_tab[e] = svmexp::table_entry(e);
     for (int e = t; e < m_cache; e += NTHREADS) dir_owner[e] = -1;
+    if (m_dict) for (int e = t; e < 256; e += NTHREADS) dict_s[e] = e < P.dict_n ? P.dict[e] : 0.0;
     for (int e = t; e < P.cache_hash; e += NTHREADS) dir_hash[e] = make_int2(-1, -1);
     if (m_cluster)
         for (int e = t; e < 2 * P.ctas_per_rank * P.crw; e += NTHREADS) cmb[e] = make_uint4(0u, 0u, 0u, 0u);
@@ -622,9 +662,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
             if (lane == 0 && n_tiles > 0) {
                 const int rp = (R + 3) & ~3;
                 const uint32_t bytes = m_isbin ? (uint32_t)(n_tiles * ((P.bin_words + 3) & ~3) * P.rt * 4)
-                                                   : (uint32_t)P.d_pad * rp * 4u;
+                                                   : (uint32_t)P.d_pad * rp * (uint32_t)esz;
                 mbar_arrive_tx(&full[0], bytes);
-                bulk_g2s(ring, xcta, bytes, &full[0]);
+                bulk_g2s(ring, xcta_b, bytes, &full[0]);
             }
             if (lane == 0) { sh.issued = 0; __threadfence_block(); sh.producer_done = 1; }
             if (m_cluster) cluster_sync_all();
@@ -644,14 +684,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                 if (sh.stop) break;
                 const int rows_t = min(P.rt, R - tile * P.rt);
                 const int rp = (rows_t + 3) & ~3;
-                const uint32_t bytes = (uint32_t)P.kc * rp * 4u;
-                const float* src = xcta + (long long)tile * P.d_pad * P.rt + (long long)chunk * P.kc * rp;
+                const uint32_t bytes = (uint32_t)P.kc * rp * (uint32_t)esz;
+                const unsigned char* src = xcta_b + ((long long)tile * P.d_pad * P.rt + (long long)chunk * P.kc * rp) * esz;
+                unsigned char* dst = ring_b + (size_t)slot * stage_floats * esz;
                 mbar_arrive_tx(&full[slot], bytes);
                 if (P.l2_keep_tiles > 0)
-                    bulk_g2s_hint(ring + (size_t)slot * stage_floats, src, bytes, &full[slot],
-                                  tile < P.l2_keep_tiles ? pol_keep : pol_stream);
+                    bulk_g2s_hint(dst, src, bytes, &full[slot], tile < P.l2_keep_tiles ? pol_keep : pol_stream);
                 else
-                    bulk_g2s(ring + (size_t)slot * stage_floats, src, bytes, &full[slot]);
+                    bulk_g2s(dst, src, bytes, &full[slot]);
                 ++s;
                 sh.issued = s;
                 if (++slot == (unsigned)P.stages) { slot = 0; par ^= 1u; wrapped = true; }
@@ -1313,9 +1353,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
             for (int ch = 0; ch < ((m_isbin || rows_ready) ? 0 : P.n_chunks); ++ch) {
                 if (!m_resident) mbar_wait(&full[cslot], cpar);
                 const float* st = m_resident ? ring + (size_t)ch * P.kc * rp : ring + (size_t)cslot * stage_floats;
+                const unsigned char* stb = ring_b + (m_resident ? (size_t)ch * P.kc * rp : (size_t)cslot * stage_floats) * esz;
                 const int k0 = ch * P.kc;
                 if (active && m_mixed) {
                     mixed_rows<KERNEL, RPT>(P, st, rp, t, pivm, pbits, du, dl);
+                } else if (active && m_dict) {
+                    dict_rows<KERNEL, RPT>(P.kc, stb, rp, t, piv + k0, dict_s, du, dl);
                 } else if (active) {
                     if (RPT == 4) {
                         const float4* sp = reinterpret_cast<const float4*>(st) + t;

@@ -66,6 +66,9 @@ struct SolveArgs {
     const float* xr_rank[svmk::MAXR] = {};
     long long max_iter_rank[svmk::MAXR] = {};
     std::vector<int> mix_map;                  // (set by solve) mixed compact rows: column map
+    std::vector<double> dict_vals;             // (set by solve) dictionary-coded rows: values,
+    std::vector<unsigned> dict_keys;           //   the value set (fp32 bit patterns, hashed)
+    std::vector<unsigned char> dict_code;      //   and the code of every set slot
     SolveOut out;                              // rank_base's result
     SolveOut out_rank[svmk::MAXR];             // every served rank (independent mode)
 };

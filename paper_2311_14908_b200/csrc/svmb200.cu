@@ -108,6 +108,73 @@ __global__ void k_build_xblk_mixed(const float* __restrict__ X, long long n_r, i
     }
 }
 
+// Dictionary of X's distinct fp32 values (bit patterns): an open-addressing set of 1024
+// slots; per-block sets in shared memory merged into the global one.  *count ends > 256 if
+// X has more than 256 distinct values (then the build stops early).
+constexpr int DICT_SLOTS = 1024;
+constexpr unsigned DICT_EMPTY = 0xffffffffu;                // a NaN pattern: never in X
+__device__ __forceinline__ unsigned dict_hash(unsigned u) { return (u * 2654435761u) >> 22; }
+__global__ void k_dict_insert(const float* __restrict__ X, long long nx, unsigned* __restrict__ keys,
+                              int* __restrict__ count) {
+    __shared__ unsigned sk[DICT_SLOTS];
+    __shared__ int scount;
+    for (int i = threadIdx.x; i < DICT_SLOTS; i += blockDim.x) sk[i] = DICT_EMPTY;
+    if (threadIdx.x == 0) scount = 0;
+    __syncthreads();
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < nx; e += (long long)gridDim.x * blockDim.x) {
+        if (*(volatile int*)&scount > 256 || *(volatile int*)count > 256) break;
+        const unsigned u = __float_as_uint(X[e]);
+        unsigned h = dict_hash(u);
+        for (int probe = 0;; ++probe) {
+            if (probe == DICT_SLOTS) { atomicAdd(&scount, 1000); break; }
+            const unsigned prev = atomicCAS(&sk[h], DICT_EMPTY, u);
+            if (prev == DICT_EMPTY) { atomicAdd(&scount, 1); break; }
+            if (prev == u) break;
+            h = (h + 1) & (DICT_SLOTS - 1);
+        }
+    }
+    __syncthreads();
+    if (scount > 256) {
+        if (threadIdx.x == 0) atomicAdd(count, 1000);
+        return;
+    }
+    for (int i = threadIdx.x; i < DICT_SLOTS; i += blockDim.x) {
+        const unsigned u = sk[i];
+        if (u == DICT_EMPTY) continue;
+        unsigned h = dict_hash(u);
+        for (int probe = 0; probe < DICT_SLOTS; ++probe) {
+            const unsigned prev = atomicCAS(&keys[h], DICT_EMPTY, u);
+            if (prev == DICT_EMPTY) { atomicAdd(count, 1); break; }
+            if (prev == u) break;
+            h = (h + 1) & (DICT_SLOTS - 1);
+        }
+    }
+}
+__device__ __forceinline__ unsigned dict_code(const unsigned* keys, const unsigned char* code, unsigned u) {
+    unsigned h = dict_hash(u);
+    while (keys[h] != u) h = (h + 1) & (DICT_SLOTS - 1);
+    return code[h];
+}
+// The CTA-blocked layout of k_build_xblk with one byte per element: the dictionary code.
+__global__ void k_build_xblk_dict(const float* __restrict__ X, long long n_r, int d, int d_pad, int G, int rt,
+                                  long long cta_stride, const unsigned* __restrict__ keys,
+                                  const unsigned char* __restrict__ code, unsigned char* __restrict__ xblk) {
+    const int c = blockIdx.y;
+    const long long r0 = (n_r * c) / G, r1 = (n_r * (c + 1)) / G;
+    const long long R = r1 - r0;
+    const long long total = R * d_pad;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long k = e / R;
+        const long long j = e - k * R;
+        const long long tile = j / rt, rin = j - tile * rt;
+        const long long rows_t = (R - tile * rt) < rt ? (R - tile * rt) : rt;
+        const long long rp = (rows_t + 3) & ~3ll;
+        const unsigned char v = (k < d) ? (unsigned char)dict_code(keys, code, __float_as_uint(X[(r0 + j) * d + k])) : 0;
+        xblk[(long long)c * cta_stride + tile * (long long)d_pad * rt + k * rp + rin] = v;
+    }
+}
+
 // bit rows: bit k of word k/32 of row r = X[r][k]
 __global__ void k_pack_bits(const float* __restrict__ X, long long n, int d, int W, uint32_t* __restrict__ out) {
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n * W; e += (long long)gridDim.x * blockDim.x) {
@@ -221,6 +288,7 @@ struct Plan {
     int dp = 0;          // dense pivot entries (shared memory)
     int mix_nc = 0, mix_nbw = 0, mix_nseg = 0;   // mixed compact rows (mix_nseg > 0)
     int mix_seg[MIX_MAXSEG] = {};
+    int esz = 4;         // bytes per xblk element (1: dictionary codes)
     long long cta_stride = 0;
     size_t smem = 0;
 };
@@ -232,6 +300,7 @@ int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl, bool bina
     if (mix) {
         pl.mix_nc = mix->mix_nc; pl.mix_nbw = mix->mix_nbw; pl.mix_nseg = mix->mix_nseg;
         for (int i = 0; i < MIX_MAXSEG; ++i) pl.mix_seg[i] = mix->mix_seg[i];
+        pl.esz = mix->esz;
     }
     // cluster mode: the shared-memory mailbox cmb[2][G][cl_words] of 16-byte words
     const size_t cl_bytes = cl_words > 0 ? (size_t)2 * G * cl_words * 16 + 16 : 0;
@@ -282,7 +351,7 @@ int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl, bool bina
         if (r == 1 || r == 2 || r == 4) pl.rpt = r;
     }
     pl.rt = NT * pl.rpt;
-    pl.kc = 8192 / pl.rt;                                  // 32 KB stages
+    pl.kc = 8192 * (4 / pl.esz) / pl.rt;                   // 32 KB stages
     if (const char* e = getenv("SVMB200_KC")) {           // tuning override (features per stage)
         const int v = atoi(e);
         if (v >= 1 && v <= 64) pl.kc = v;
@@ -299,6 +368,13 @@ int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl, bool bina
         pl.dp = (d + 3) & ~3;
         mix_bytes = (size_t)pl.mix_nc * 16 + (((size_t)2 * pl.mix_nbw * 4 + 15) & ~size_t(15));
     }
+    if (pl.esz == 1) {
+        pl.kc = (pl.kc + 3) & ~3;                          // byte stages: 16-byte multiples
+        pl.d_pad = (d + pl.kc - 1) / pl.kc * pl.kc;
+        pl.n_chunks = pl.d_pad / pl.kc;
+        pl.dp = pl.d_pad;
+        mix_bytes = 256 * 8;                               // the dictionary values
+    }
     const int n_tiles = (pl.state_cap + pl.rt - 1) / pl.rt;
     pl.cta_stride = (long long)n_tiles * pl.d_pad * pl.rt;
     pl.alpha_smem = pl.state_cap <= 2048;                  // else alpha stays in HBM
@@ -311,9 +387,9 @@ int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl, bool bina
     pl.cache_hash = hash;
     fixed += cl_bytes;
     fixed = (fixed + 127) & ~size_t(127);
-    const size_t stage_bytes = (size_t)pl.kc * pl.rt * 4;
+    const size_t stage_bytes = (size_t)pl.kc * pl.rt * pl.esz;
     // resident mode: the whole (single-tile) X block of a CTA fits next to the state
-    const size_t resident_bytes = (size_t)pl.d_pad * ((pl.state_cap + 3) & ~3) * 4;
+    const size_t resident_bytes = (size_t)pl.d_pad * ((pl.state_cap + 3) & ~3) * pl.esz;
     pl.resident = n_tiles == 1 && fixed + resident_bytes <= (size_t)max_smem && getenv("SVMB200_NO_RESIDENT") == nullptr;
     if (pl.resident) {
         pl.stages = 1;
@@ -442,15 +518,60 @@ int solve(SolveArgs& a) {
                 for (long long k = 0; k < a.d; ++k) if (!nb[k]) mix_map.push_back((int)k);
             }
         }
+        // dictionary-coded rows: <= 256 distinct fp32 values in X (uint8 pixels, SURVEY
+        // §8(f)); preferred when smaller than the mixed rows
+        std::vector<double> dict_vals;
+        std::vector<unsigned char> dict_code((size_t)DICT_SLOTS, 0);
+        std::vector<unsigned> dict_keys((size_t)DICT_SLOTS, DICT_EMPTY);
+        if (!a.independent && getenv("SVMB200_NO_DICT") == nullptr && a.d >= 8 &&
+            (mix.mix_nseg == 0 || a.d < 4 * (mix.mix_nc + mix.mix_nbw))) {
+            unsigned* dk = nullptr;
+            int* dcnt = nullptr;
+            CKR(cudaMallocAsync(&dk, DICT_SLOTS * 4, a.stream));
+            CKR(cudaMallocAsync(&dcnt, 4, a.stream));
+            CKR(cudaMemsetAsync(dk, 0xff, DICT_SLOTS * 4, a.stream));
+            CKR(cudaMemsetAsync(dcnt, 0, 4, a.stream));
+            k_dict_insert<<<592, 256, 0, a.stream>>>(a.xr, a.n_global * a.d, dk, dcnt);
+            counted();
+            int cnt = 0;
+            CKR(cudaMemcpyAsync(&cnt, dcnt, 4, cudaMemcpyDeviceToHost, a.stream));
+            CKR(cudaMemcpyAsync(dict_keys.data(), dk, DICT_SLOTS * 4, cudaMemcpyDeviceToHost, a.stream));
+            CKR(cudaFreeAsync(dk, a.stream));
+            CKR(cudaFreeAsync(dcnt, a.stream));
+            CKR(cudaStreamSynchronize(a.stream));
+            if (cnt >= 1 && cnt <= 256) {
+                for (int h = 0; h < DICT_SLOTS; ++h) {
+                    if (dict_keys[h] == DICT_EMPTY) continue;
+                    float f;
+                    memcpy(&f, &dict_keys[h], 4);
+                    dict_code[h] = (unsigned char)dict_vals.size();
+                    dict_vals.push_back((double)f);
+                }
+            }
+        }
         pl = Plan();
-        if (mix.mix_nseg > 0) {
+        if (!dict_vals.empty()) {
+            Plan dp_;
+            dp_.esz = 1;
+            if (make_plan(a.n_rows_max, (int)a.d, a.ctas_per_rank, a.max_smem, pl, false, false, 0, 0, &dp_) == SVM_OK) {
+                mix = Plan();
+                mix_map.clear();
+                a.dict_vals = dict_vals;
+                a.dict_keys = dict_keys;
+                a.dict_code = dict_code;
+            } else {
+                pl = Plan();
+                dict_vals.clear();
+            }
+        }
+        if (dict_vals.empty() && mix.mix_nseg > 0) {
             if (make_plan(a.n_rows_max, (int)a.d, a.ctas_per_rank, a.max_smem, pl, false, false, 0, 0, &mix) != SVM_OK) {
                 mix = Plan();
                 mix_map.clear();
                 pl = Plan();
             }
         }
-        if (mix.mix_nseg == 0) {
+        if (mix.mix_nseg == 0 && pl.esz != 1) {
             rc = make_plan(a.n_rows_max, (int)a.d, a.ctas_per_rank, a.max_smem, pl);
             if (rc) return rc;
         }
@@ -469,7 +590,7 @@ int solve(SolveArgs& a) {
             if (slots < 4) slots = 4;
             Plan pc;
             if (make_plan(a.n_rows_max, (int)a.d, a.ctas_per_rank, a.max_smem, pc, false, false, slots, 0,
-                          pl.mix_nseg > 0 ? &pl : nullptr) == SVM_OK &&
+                          (pl.mix_nseg > 0 || pl.esz != 4) ? &pl : nullptr) == SVM_OK &&
                 !pc.resident) {
                 pl = pc;
                 pl.cache_slots = slots;
@@ -481,7 +602,7 @@ int solve(SolveArgs& a) {
     // shared memory (~0.2 us) instead of global-memory mailboxes (~2.5 us); the candidates'
     // rows travel in the records.  Auto: the smallest power-of-two cluster with <= 2048 rows
     // per CTA (else 16 CTAs if <= 8192 rows each), when it is resident.
-    const bool cl_allowed = gram == nullptr && pl.cache_slots == 0 && pl.mix_nseg == 0 && a.p.cluster != -1 &&
+    const bool cl_allowed = gram == nullptr && pl.cache_slots == 0 && pl.mix_nseg == 0 && pl.esz == 4 && a.p.cluster != -1 &&
                             a.world == a.nranks_here && (a.world == 1 || a.independent) &&
                             (a.p.ctas <= 0 || a.p.cluster > 0) && getenv("SVMB200_NO_CLUSTER") == nullptr;
     if (a.p.cluster > 16 || a.p.cluster < -1) return fail(SVM_EINVAL, "cluster must be -1, 0 or 1..16");
@@ -537,6 +658,7 @@ int solve(SolveArgs& a) {
     {
         const char* mode = gram ? "gram" : pl.bin_words ? "binary-resident"
                          : pl.mix_nseg ? (pl.resident ? "mixed-resident" : pl.cache_slots ? "mixed+row-cache" : "mixed-streamed")
+                         : pl.esz == 1 ? (pl.resident ? "dict-resident" : pl.cache_slots ? "dict+row-cache" : "dict-streamed")
                          : pl.resident ? "float-resident" : pl.cache_slots ? "streamed+row-cache" : "streamed";
         char buf[320];
         snprintf(buf, sizeof buf,
@@ -601,7 +723,7 @@ int solve(SolveArgs& a) {
     if (const char* e = getenv("SVMB200_POLL_NS")) P.poll_ns = atoi(e);
     // L2 residency of streamed X: keep the first tiles of every CTA block in L2
     // (SVMB200_L2_KEEP_MB, per GPU; tuning)
-    if (!pl.resident && pl.bin_words == 0 && !gram && pl.mix_nseg == 0) {
+    if (!pl.resident && pl.bin_words == 0 && !gram && pl.mix_nseg == 0 && pl.esz == 4) {
         long long keep_mb = 0;
         if (const char* e = getenv("SVMB200_L2_KEEP_MB")) keep_mb = atoll(e);
         const long long tile_bytes = (long long)pl.d_pad * pl.rt * 4;
@@ -612,6 +734,19 @@ int solve(SolveArgs& a) {
     const bool want_timers = getenv("SVMB200_PHASE_TIMERS") != nullptr;
     for (int r = 0; r < world; ++r) { P.row_off[r] = a.row_off[r]; P.n_rows[r] = (int)a.n_rows[r]; P.mbox[r] = a.mbox[r]; }
 
+    unsigned* d_keys = nullptr;
+    unsigned char* d_code = nullptr;
+    if (pl.esz == 1) {
+        double* dv;
+        if ((rc = dalloc((void**)&dv, 256 * 8))) { release(); return rc; }
+        if ((rc = dalloc((void**)&d_keys, DICT_SLOTS * 4))) { release(); return rc; }
+        if ((rc = dalloc((void**)&d_code, DICT_SLOTS))) { release(); return rc; }
+        CKR(cudaMemcpyAsync(dv, a.dict_vals.data(), a.dict_vals.size() * 8, cudaMemcpyHostToDevice, st));
+        CKR(cudaMemcpyAsync(d_keys, a.dict_keys.data(), DICT_SLOTS * 4, cudaMemcpyHostToDevice, st));
+        CKR(cudaMemcpyAsync(d_code, a.dict_code.data(), DICT_SLOTS, cudaMemcpyHostToDevice, st));
+        P.dict = dv;
+        P.dict_n = (int)a.dict_vals.size();
+    }
     if (pl.mix_nseg > 0) {
         int* dm;
         if ((rc = dalloc((void**)&dm, a.mix_map.size() * 4))) { release(); return rc; }
@@ -621,7 +756,7 @@ int solve(SolveArgs& a) {
     for (int r = a.rank_base; r < a.rank_base + a.nranks_here; ++r) {
         const long long nr = a.n_rows[r];
         float* xb; double* f; double* al; uint8_t* fl; Ctl* ctl;
-        if ((rc = dalloc((void**)&xb, (size_t)pl.cta_stride * pl.G * 4 + 16))) { release(); return rc; }
+        if ((rc = dalloc((void**)&xb, (size_t)pl.cta_stride * pl.G * pl.esz + 16))) { release(); return rc; }
         if ((rc = dalloc((void**)&f, (size_t)nr * 8 + 8))) { release(); return rc; }
         if ((rc = dalloc((void**)&fl, (size_t)nr + 8))) { release(); return rc; }
         if ((rc = dalloc((void**)&ctl, sizeof(Ctl)))) { release(); return rc; }
@@ -631,7 +766,7 @@ int solve(SolveArgs& a) {
             P.cache[r] = cache;
         }
         al = a.alpha_out[r];
-        CKR(cudaMemsetAsync(xb, 0, (size_t)pl.cta_stride * pl.G * 4, st));
+        CKR(cudaMemsetAsync(xb, 0, (size_t)pl.cta_stride * pl.G * pl.esz, st));
         CKR(cudaMemsetAsync(ctl, 0, sizeof(Ctl), st));
         dim3 bg(256, pl.G);
         if (gram) {
@@ -648,6 +783,10 @@ int solve(SolveArgs& a) {
             k_build_xbits<<<bg, 256, 0, st>>>(P.xrbits + a.row_off[r] * pl.bin_words, nr, pl.bin_words,
                                                (pl.bin_words + 3) & ~3, pl.G, pl.cta_stride,
                                                reinterpret_cast<uint32_t*>(xb));
+        } else if (pl.esz == 1) {
+            counted(2);   // build + init_state below
+            k_build_xblk_dict<<<bg, 256, 0, st>>>(a.x_rank[r], nr, (int)a.d, pl.d_pad, pl.G, pl.rt, pl.cta_stride,
+                                                  d_keys, d_code, reinterpret_cast<unsigned char*>(xb));
         } else if (pl.mix_nseg > 0) {
             counted(2);   // build + init_state below
             k_build_xblk_mixed<<<bg, 256, 0, st>>>(a.x_rank[r], nr, (int)a.d, P.mix_map, pl.mix_nc, pl.mix_nbw,

@@ -518,3 +518,51 @@ def test_mixed_rows_parity(S, monkeypatch, runs, kern, gamma):
     r5 = S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol, want_f=True, cluster=-1)
     assert not S.last_plan()["mode"].startswith("mixed")
     _assert_exact(r5, r_or)
+
+
+@pytest.mark.parametrize("case", ["W3", "levels256", "linear_neg"])
+def test_dict_rows_parity(S, monkeypatch, case):
+    """Dictionary-coded rows (<= 256 distinct fp32 values stored as one-byte codes, e.g.
+    uint8 pixels) equal the oracle bit for bit: streamed / resident / row
+    cache, RPT 1/2/4, virtual ranks; 257 distinct values fall back to fp32 rows."""
+    rng = np.random.default_rng(41)
+    if case == "W3":
+        w = W.get("W3")
+        X, y = w.train(1700)
+    else:
+        n, d = 1900, 40
+        levels = rng.normal(0.0, 1.0, 256).astype(np.float32)
+        levels[0] = 0.0
+        X = levels[rng.integers(0, 256, size=(n, d))]
+        X[rng.random((n, d)) < 0.5] = 0.0
+        X = np.ascontiguousarray(X)
+        s = X[:, :5].sum(1) + 0.3 * rng.normal(size=n)
+        y = np.where(s > np.median(s), 1, -1).astype(np.int8)
+        kern, gamma = (O.RBF, 0.03) if case == "levels256" else (O.LINEAR, 0.0)
+        w = W.Workload("lv", "", n, d, kern, gamma, 1.0, 1e-3, 0, 0, 0, None)
+    r_or = O.train(X, y, w.C, w.kernel, w.gamma, w.tol, trace_cap=100000)
+    r_g = S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol, want_f=True, trace_cap=100000, cluster=-1)
+    assert S.last_plan()["mode"].startswith("dict")
+    _assert_exact(r_g, r_or)
+    for rpt in ("1", "2", "4"):
+        monkeypatch.setenv("SVMB200_RPT", rpt)
+        r2 = S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol, want_f=True, cluster=-1, ctas=23)
+        _assert_exact(r2, r_or)
+    monkeypatch.delenv("SVMB200_RPT")
+    r3 = S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol, want_f=True, virtual_ranks=3)
+    _assert_exact(r3, r_or)
+    monkeypatch.setenv("SVMB200_NO_RESIDENT", "1")
+    r4 = S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol, want_f=True, cache_rows=16, cluster=-1)
+    assert S.last_plan()["mode"] == "dict+row-cache"
+    _assert_exact(r4, r_or)
+    r5 = S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol, want_f=True, cache_rows=-1, cluster=-1)
+    assert S.last_plan()["mode"] == "dict-streamed"
+    _assert_exact(r5, r_or)
+    monkeypatch.delenv("SVMB200_NO_RESIDENT")
+    if case == "levels256":
+        X2 = X.copy()
+        X2[0, 0] = np.float32(0.123456)                       # a 257th value
+        r_o2 = O.train(X2, y, w.C, w.kernel, w.gamma, w.tol)
+        r6 = S.svm_train_ex(X2, y, w.C, w.kernel, w.gamma, w.tol, want_f=True, cluster=-1)
+        assert not S.last_plan()["mode"].startswith("dict")
+        np.testing.assert_array_equal(r6["alpha"], r_o2.alpha)
