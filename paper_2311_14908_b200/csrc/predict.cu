@@ -81,6 +81,7 @@ int predict_device_tc(const float* X_sv, const double* coef, long long n_sv, lon
                       int kernel, double gamma, const float* X_test, long long m, double* dec,
                       cudaStream_t st) {
     using namespace svmtc;
+    pool_setup();
     const long long m_pad = (m + BM - 1) / BM * BM;
     const long long n_pad = (n_sv + BN - 1) / BN * BN;
     const int k_chunks = (int)((d + BK - 1) / BK);

@@ -77,6 +77,7 @@ int check_params(long long n, long long d, const svm_params* p, svm_params* q);
 int validate_device(const float* X, const int8_t* y, long long n, long long d, cudaStream_t st,
                     int* n_pos);
 int device_limits(int* n_sm, int* max_smem);
+void pool_setup();
 int solve(SolveArgs& a);
 
 // gram.cu: K[i][j] for all i, j < n (fp64, row-major), same arithmetic as the row pass

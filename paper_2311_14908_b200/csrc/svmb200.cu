@@ -235,8 +235,26 @@ __global__ void k_validate(const float* __restrict__ X, long long nx, const int8
     if (neg) atomicAdd(&counts[3], neg);
 }
 
+// The library allocates its scratch with cudaMallocAsync and frees it before returning.
+// With the default pool's release threshold (0) every stream synchronisation hands the
+// memory back to the driver, so every call would map it again; keep up to 2 GiB cached
+// in the current device's default pool (a caching allocator's behaviour).
+void pool_setup() {
+    static thread_local int done_mask = 0;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev >= 31 || (done_mask >> dev) & 1) { cudaGetLastError(); return; }
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        unsigned long long thr = 2ull << 30;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    done_mask |= 1 << dev;
+}
+
 int validate_device(const float* X, const int8_t* y, long long n, long long d, cudaStream_t st,
                     int* n_pos) {
+    pool_setup();
     unsigned long long* dc = nullptr;
     CKR(cudaMallocAsync(&dc, 4 * sizeof(unsigned long long), st));
     CKR(cudaMemsetAsync(dc, 0, 4 * sizeof(unsigned long long), st));
@@ -425,6 +443,7 @@ KernelFn pick_kernel(int kernel, int rpt, bool a_smem, bool bincl = false) {
 }
 
 int device_limits(int* n_sm, int* max_smem) {
+    pool_setup();
     int dev;
     CKR(cudaGetDevice(&dev));
     CKR(cudaDeviceGetAttribute(n_sm, cudaDevAttrMultiProcessorCount, dev));
