@@ -115,10 +115,56 @@ __global__ void __launch_bounds__(NTB, 1) smo_bincl(const Params P) {
 #pragma unroll
     for (int k = 0; k < BINCL_MAXW; ++k) { pu[k] = 0u; pl[k] = 0u; }
     double cu = 0.0, cl = 0.0;
+    int yu = 0, yl = 0;                  // the selected pair's labels and alphas (pending update)
+    double au = 0.0, al = 0.0;
     const int nq = (R + NTB - 1) / NTB;  // rows per thread (upper bound)
     const bool trace_on = P.trace != nullptr && cta == 0 && rank == 0;
     int progress_left = 1;               // the host-visible progress word, every check_interval
 
+    // ---- pair update (a2) of the pair selected last iteration (it - 1), in every warp: eta,
+    // clipped step, snapped alphas; the owners of rows u and l update them.  Called inside
+    // the row pass between the popcounts and the first use of c_u, c_l (and of the owners'
+    // flags), so its serial fp64 chain overlaps the POPC-bound distance work.
+    auto pair_update = [&]() {
+        double Kuu, Kll, Kul;
+        {
+            int cuu = 0, cll = 0, cul = 0, cx = 0;
+#pragma unroll
+            for (int k = 0; k < BINCL_MAXW; ++k) {
+                cuu += __popc(pu[k]); cll += __popc(pl[k]);
+                cul += __popc(pu[k] & pl[k]); cx += __popc(pu[k] ^ pl[k]);
+            }
+            if (KERNEL == 1) { Kuu = 1.0; Kll = 1.0; Kul = (iu == il) ? 1.0 : ktab[cx]; }
+            else { Kuu = (double)cuu; Kll = (double)cll; Kul = (double)cul; }
+        }
+        const double eta = Kuu + Kll - 2.0 * Kul;
+        const double gap = fl - fu;
+        const double yu_d = (double)yu, yl_d = (double)yl;
+        const double tu = (yu == 1) ? C - au : au;
+        const double tl = (yl == 1) ? al : C - al;
+        double tt = gap / (eta > 1e-12 ? eta : 1e-12);
+        if (tu < tt) tt = tu;
+        if (tl < tt) tt = tl;
+        const double au2 = (tt == tu) ? (yu == 1 ? C : 0.0) : au + yu_d * tt;
+        const double al2 = (tt == tl) ? (yl == 1 ? 0.0 : C) : al - yl_d * tt;
+        cu = yu_d * (au2 - au);
+        cl = yl_d * (al2 - al);
+        // the owners of rows u and l (thread j % NTB of the owning CTA) update them before
+        // their next row pass
+        {
+            const int lu = (int)((long long)iu - gbase), ll = (int)((long long)il - gbase);   // |.| < 2^31
+            const bool own_u = (unsigned)lu < (unsigned)R && (lu & (NTB - 1)) == t;
+            const bool own_l = (unsigned)ll < (unsigned)R && (ll & (NTB - 1)) == t;
+            if (own_u) { a_s[lu] = au2; fl_s[lu] = flags_of(yu, au2, C); }
+            if (own_l) { a_s[ll] = al2; fl_s[ll] = flags_of(yl, al2, C); }
+        }
+        if (--progress_left == 0) {
+            progress_left = P.check_interval;
+            if (t == 0 && cta == 0 && rank == 0 && P.progress)
+                *(volatile unsigned long long*)P.progress = (unsigned long long)(it - 1);
+        }
+        if (trace_on && t == 0 && it - 1 < P.trace_cap) { P.trace[2 * (it - 1)] = iu; P.trace[2 * (it - 1) + 1] = il; }
+    };
     const bool timing = P.timers != nullptr && blockIdx.x == 0 && t == 0;
     unsigned long long ph_acc[PH_N] = {};
     long long ph_t = clock64();
@@ -158,6 +204,7 @@ __global__ void __launch_bounds__(NTB, 1) smo_bincl(const Params P) {
                         }
                     }
                 }
+                if (q0 == 0) pair_update();      // c_u, c_l; owners' alpha / flags
                 double ku[BT], kl[BT];
 #pragma unroll
                 for (int q = 0; q < BT; ++q) {
@@ -340,10 +387,10 @@ __global__ void __launch_bounds__(NTB, 1) smo_bincl(const Params P) {
                 if (++spins > (1u << 24)) break;
             }
         }
-        const int yu = (int)(int16_t)(__shfl_sync(0xffffffffu, wa.y, 0) & 0xffffu);
-        const double au = __hiloint2double((int)__shfl_sync(0xffffffffu, wa.w, 0), (int)__shfl_sync(0xffffffffu, wa.z, 0));
-        const int yl = (int)(int16_t)(__shfl_sync(0xffffffffu, wa.y, 1) >> 16);
-        const double al = __hiloint2double((int)__shfl_sync(0xffffffffu, wa.w, 2), (int)__shfl_sync(0xffffffffu, wa.z, 2));
+        yu = (int)(int16_t)(__shfl_sync(0xffffffffu, wa.y, 0) & 0xffffu);
+        au = __hiloint2double((int)__shfl_sync(0xffffffffu, wa.w, 0), (int)__shfl_sync(0xffffffffu, wa.z, 0));
+        yl = (int)(int16_t)(__shfl_sync(0xffffffffu, wa.y, 1) >> 16);
+        al = __hiloint2double((int)__shfl_sync(0xffffffffu, wa.w, 2), (int)__shfl_sync(0xffffffffu, wa.z, 2));
 #pragma unroll
         for (int k = 0; k < BINCL_MAXW; ++k) {
             const int su = 3 + k / 3, sl = 3 + rw + k / 3;
@@ -354,45 +401,6 @@ __global__ void __launch_bounds__(NTB, 1) smo_bincl(const Params P) {
             pl[k] = k < W ? vl : 0u;
         }
         BPHASE(PH_S_PIVOT);
-        // ---- pair update (a2), in every warp: eta, clipped step, snapped alphas
-        double Kuu, Kll, Kul;
-        {
-            int cuu = 0, cll = 0, cul = 0, cx = 0;
-#pragma unroll
-            for (int k = 0; k < BINCL_MAXW; ++k) {
-                cuu += __popc(pu[k]); cll += __popc(pl[k]);
-                cul += __popc(pu[k] & pl[k]); cx += __popc(pu[k] ^ pl[k]);
-            }
-            if (KERNEL == 1) { Kuu = 1.0; Kll = 1.0; Kul = (iu == il) ? 1.0 : ktab[cx]; }
-            else { Kuu = (double)cuu; Kll = (double)cll; Kul = (double)cul; }
-        }
-        const double eta = Kuu + Kll - 2.0 * Kul;
-        const double gap = fl - fu;
-        const double yu_d = (double)yu, yl_d = (double)yl;
-        const double tu = (yu == 1) ? C - au : au;
-        const double tl = (yl == 1) ? al : C - al;
-        double tt = gap / (eta > 1e-12 ? eta : 1e-12);
-        if (tu < tt) tt = tu;
-        if (tl < tt) tt = tl;
-        const double au2 = (tt == tu) ? (yu == 1 ? C : 0.0) : au + yu_d * tt;
-        const double al2 = (tt == tl) ? (yl == 1 ? 0.0 : C) : al - yl_d * tt;
-        cu = yu_d * (au2 - au);
-        cl = yl_d * (al2 - al);
-        // the owners of rows u and l (thread j % NTB of the owning CTA) update them before
-        // their next row pass
-        {
-            const int lu = (int)((long long)iu - gbase), ll = (int)((long long)il - gbase);   // |.| < 2^31
-            const bool own_u = (unsigned)lu < (unsigned)R && (lu & (NTB - 1)) == t;
-            const bool own_l = (unsigned)ll < (unsigned)R && (ll & (NTB - 1)) == t;
-            if (own_u) { a_s[lu] = au2; fl_s[lu] = flags_of(yu, au2, C); }
-            if (own_l) { a_s[ll] = al2; fl_s[ll] = flags_of(yl, al2, C); }
-        }
-        if (--progress_left == 0) {
-            progress_left = P.check_interval;
-            if (t == 0 && cta == 0 && rank == 0 && P.progress)
-                *(volatile unsigned long long*)P.progress = (unsigned long long)it;
-        }
-        if (trace_on && t == 0 && it < P.trace_cap) { P.trace[2 * it] = iu; P.trace[2 * it + 1] = il; }
         BPHASE(PH_S_KUL);
         have_update = true;
         ++it;
