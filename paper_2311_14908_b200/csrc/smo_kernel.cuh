@@ -948,6 +948,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
             // ---- row cache (a8): every CTA runs the same directory operations on the same
             // pair sequence (hash lookup, FIFO replacement), so every CTA agrees
             int c_hit = 0, su = -1, sl = -1;
+            double kul_pre = 0.0;                   // lane 0: K_ul read early from the row cache
             if (m_cache > 0) {
                 if (lane == 0) {
                     const int hm = P.cache_hash - 1;
@@ -992,6 +993,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                     if (su < 0) { fu_ = victim(sl); dir_owner[fu_] = iu; insert(iu, fu_); }
                     if (sl < 0) { fl_ = victim(su >= 0 ? su : fu_); dir_owner[fl_] = il; insert(il, fl_); }
                     sh.c_hit = c_hit; sh.c_su = su; sh.c_sl = sl; sh.c_fill_u = fu_; sh.c_fill_l = fl_;
+                    // both rows cached: start the load of K_ul (column l of u's row) now, so its
+                    // latency overlaps the winners' words and barrier A
+                    if (c_hit && kul_cache_ok(P, iu, il)) kul_pre = kcache_at(P, su, il);
                 }
                 c_hit = __shfl_sync(0xffffffffu, c_hit, 0);
                 su = __shfl_sync(0xffffffffu, su, 0);
@@ -1153,7 +1157,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                     // both rows cached: K_ul is column l of the cached row of u (computed by
                     // l's owner CTA with the row-pass arithmetic, made visible by its fence);
                     // K(x, x) is column u of u's row / column l of l's row
-                    Kul = kcache_at(P, su, l);
+                    Kul = kul_pre;
                     if (KERNEL == 1) { Kuu = 1.0; Kll = 1.0; }
                     else { Kuu = kcache_at(P, su, u); Kll = kcache_at(P, sl, l); }
                 } else if (m_cache > 0) {
