@@ -330,7 +330,9 @@ def run_ours(args):
         W = (d + 31) // 32
         sms = int(plan.get("ctas_per_rank", 1)) * int(plan.get("ranks", 1))
         mhz = clk.summary().get("sm_mhz") or 1965.0
-        popc_iter = n_r * 2 * W
+        # POPC instructions the row pass executes: per pivot and row, 3 for every group of 4
+        # bit words (carry-save form, smo_bincl) -- 2 (3 ceil(W/4)) per row
+        popc_iter = n_r * 2 * 3 * ((W + 3) // 4)
         alu_ach = popc_iter * it_per_s / 1e9
         alu_peak = 16 * sms * mhz * 1e6 / 1e9
         roofline = {"bound": "alu", "pipe": "POPC, 16/clk/SM x %d SMs x %.0f MHz" % (sms, mhz),
@@ -338,7 +340,8 @@ def run_ours(args):
                     "traffic": traffic, "kernel": plan.get("kernel"), "ops_per_iter": popc_iter,
                     "latency_bound": True,
                     "note": "one SMO iteration is a serial chain (row pass -> CTA barrier -> DSMEM exchange "
-                            "-> pair update); the POPC pipe is the busiest throughput unit of the row pass"}
+                            "-> pair update); the POPC pipe is the busiest throughput unit of the row pass "
+                            "(ops = POPC instructions executed, 3 per 4 bit words per pivot)"}
         hbm_roof["effective"] = True
         hbm_roof["note"] = ("fp32-equivalent algorithmic bytes per iteration (SURVEY 8(d)); served from "
                             "shared memory as bit rows, so this exceeds what streaming X from HBM could do")
