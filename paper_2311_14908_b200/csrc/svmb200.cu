@@ -244,8 +244,9 @@ void pool_setup() {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev >= 31 || (done_mask >> dev) & 1) { cudaGetLastError(); return; }
     cudaMemPool_t pool;
+    unsigned long long thr = 2ull << 30;
+    if (const char* e = getenv("SVMB200_POOL_KEEP_MB")) thr = (unsigned long long)atoll(e) << 20;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        unsigned long long thr = 2ull << 30;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     cudaGetLastError();
