@@ -217,11 +217,13 @@ __device__ __forceinline__ uint64_t l2_policy(bool keep) {
     else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+template <int NS = NSYNC>
 __device__ __forceinline__ void named_sync(int id) {
-    asm volatile("bar.sync %0, %1;" :: "r"(id), "n"(NSYNC) : "memory");
+    asm volatile("bar.sync %0, %1;" :: "r"(id), "n"(NS) : "memory");
 }
+template <int NS = NSYNC>
 __device__ __forceinline__ void named_arrive(int id) {
-    asm volatile("bar.arrive %0, %1;" :: "r"(id), "n"(NSYNC) : "memory");
+    asm volatile("bar.arrive %0, %1;" :: "r"(id), "n"(NS) : "memory");
 }
 
 // ---- thread-block cluster (distributed shared memory) helpers
@@ -269,8 +271,8 @@ struct Shared {
     int u, l;                      // global winners of this iteration
     double f_up, f_low;
     double cu, cl;                 // written by the scalar warp before barrier B
-    double red_f[2][NWC];          // per consumer warp candidates (local row index)
-    int red_i[2][NWC];
+    double red_f[2][16];           // per consumer warp candidates (local row index; <= 16 warps)
+    int red_i[2][16];
     int c_hit, c_su, c_sl;         // row cache: both rows cached / their slots
     int c_fill_u, c_fill_l;        // row cache: the slot this iteration fills (miss), else -1
     int c_fifo;                    // next FIFO victim slot
@@ -554,8 +556,12 @@ __device__ __forceinline__ void dict_rows(int kc, const unsigned char* stb, int 
 // BINCL: the kernel specialised for binary rows resident in a thread-block cluster (the
 // latency-bound small-problem path): the other modes compile out, so the per-iteration code
 // is short (instruction-cache resident).
-template <int KERNEL, int RPT, bool A_SMEM, bool BINCL>
-__global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
+template <int KERNEL, int RPT, bool A_SMEM, bool BINCL, int NTC = NT>
+__global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
+    // NTC consumer threads (8 or 16 warps), then the scalar and the producer warp
+    constexpr int NT_ = NTC, NWC_ = NTC / 32, SCALAR_ = NWC_, PRODUCER_ = NWC_ + 1;
+    constexpr int NTHREADS_ = NTC + 64, NSYNC_ = NTC + 32;
+    static_assert(NWC_ <= 16, "at most 16 consumer warps");
     // mode switches: compile-time constants in the BINCL specialisation
     const bool m_cluster = BINCL || P.cluster != 0;
     const bool m_isbin = BINCL || P.bin_words > 0;
@@ -624,17 +630,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
 
     if (t == 0) {
         sh.stop = 0; sh.producer_done = 0; sh.issued = 0; sh.timeout = 0;
-        for (int s = 0; s < P.stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NWC); }
+        for (int s = 0; s < P.stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NWC_); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    for (int e = t; e < svmexp::EXP_TABLE_DOUBLES; e += NTHREADS) sh.exp_tab[e] = svmexp::table_entry(e);
-    for (int e = t; e < m_cache; e += NTHREADS) dir_owner[e] = -1;
-    if (m_dict) for (int e = t; e < 256; e += NTHREADS) dict_s[e] = e < P.dict_n ? P.dict[e] : 0.0;
-    for (int e = t; e < P.cache_hash; e += NTHREADS) dir_hash[e] = make_int2(-1, -1);
+    for (int e = t; e < svmexp::EXP_TABLE_DOUBLES; e += NTHREADS_) sh.exp_tab[e] = svmexp::table_entry(e);
+    for (int e = t; e < m_cache; e += NTHREADS_) dir_owner[e] = -1;
+    if (m_dict) for (int e = t; e < 256; e += NTHREADS_) dict_s[e] = e < P.dict_n ? P.dict[e] : 0.0;
+    for (int e = t; e < P.cache_hash; e += NTHREADS_) dir_hash[e] = make_int2(-1, -1);
     if (m_cluster)
-        for (int e = t; e < 2 * P.ctas_per_rank * P.crw; e += NTHREADS) cmb[e] = make_uint4(0u, 0u, 0u, 0u);
+        for (int e = t; e < 2 * P.ctas_per_rank * P.crw; e += NTHREADS_) cmb[e] = make_uint4(0u, 0u, 0u, 0u);
     if (t == 0) sh.c_fifo = 0;
-    for (int j = t; j < R; j += NTHREADS) {
+    for (int j = t; j < R; j += NTHREADS_) {
         f_s[j] = P.f[rank][r0 + j];
         if (A_SMEM) a_s[j] = alpha_g[j];
         fl_s[j] = P.flags[rank][r0 + j];
@@ -642,7 +648,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
     __syncthreads();
     const svmexp::PtrTab tab{sh.exp_tab};
     if (KERNEL == 1 && m_isbin) {
-        for (int e = t; e <= 32 * P.bin_words; e += NTHREADS) ktab[e] = svmexp::exp_cr_t(-(P.gamma * (double)e), tab);
+        for (int e = t; e <= 32 * P.bin_words; e += NTHREADS_) ktab[e] = svmexp::exp_cr_t(-(P.gamma * (double)e), tab);
         __syncthreads();
     }
 
@@ -650,7 +656,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
     if (m_cluster) cluster_sync_all();
 
     // ============================================================ producer warp
-    if (warp == PRODUCER_WARP) {
+    if (warp == PRODUCER_) {
         // (cluster mode: the producer waits in the final cluster barrier, so no CTA exits
         // while a peer may still address its shared memory)
         if (m_gram) {
@@ -706,7 +712,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
 
     unsigned long long ph_acc[PH_N] = {};
     long long ph_t = clock64();
-    const bool is_scalar = (warp == SCALAR_WARP);
+    const bool is_scalar = (warp == SCALAR_);
     const bool timing = P.timers != nullptr && blockIdx.x == 0 && (t == 0 || (is_scalar && lane == 0));
     int final_state = ST_RUNNING;
     Ctl* ctl = P.ctl[rank];
@@ -726,7 +732,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
     if (!is_scalar) {
         double fu = INF, fl = -INF;
         int ju = INT_MAX, jl = INT_MAX;
-        for (int j = t; j < R; j += NT) {
+        for (int j = t; j < R; j += NT_) {
             const uint8_t g = fl_s[j];
             const double fj = f_s[j];
             if ((g & FL_UP) && better_up(fj, j, fu, ju)) { fu = fj; ju = j; }
@@ -741,13 +747,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
     }
 
     for (;;) {
-        named_sync(BAR_C);                  // consumer candidates are in sh.red_*
+        named_sync<NSYNC_>(BAR_C);                  // consumer candidates are in sh.red_*
         SVM_PHASE(timing, is_scalar ? PH_S_WAITC : PH_C_REDUCE);
         ++seq;
         if (!is_scalar) {
             // consumers: the scalar warp runs the exchange, the selection, the stopping test,
             // the row-cache directory and the pivot gather, then releases barrier A
-            named_sync(BAR_A);
+            named_sync<NSYNC_>(BAR_A);
             SVM_PHASE(timing, PH_C_EXCH);
             const int dec = sh.decision;
             if (dec != ST_RUNNING) { final_state = dec; break; }
@@ -776,7 +782,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                 const unsigned hmask = lowh ? 0xffff0000u : 0x0000ffffu;
                 unsigned long long kv = 0xffffffffffffffffull;
                 unsigned jv = 0xffffffffu;
-                if (hl < NWC) {
+                if (hl < NWC_) {
                     const unsigned long long k = fkey(sh.red_f[lowh ? 1 : 0][hl]);
                     kv = lowh ? ~k : k;
                     jv = (unsigned)sh.red_i[lowh ? 1 : 0][hl];
@@ -876,12 +882,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                 Cand c;
                 int ju, jl;                                   // this CTA's candidates (local rows)
                 {
-                    double fu = lane < NWC ? sh.red_f[0][lane] : INF;
-                    ju = lane < NWC ? sh.red_i[0][lane] : INT_MAX;
-                    double fl = lane < NWC ? sh.red_f[1][lane] : -INF;
-                    jl = lane < NWC ? sh.red_i[1][lane] : INT_MAX;
-                    warp_reduce_fi<true>(fu, ju, NWC);
-                    warp_reduce_fi<false>(fl, jl, NWC);
+                    double fu = lane < NWC_ ? sh.red_f[0][lane] : INF;
+                    ju = lane < NWC_ ? sh.red_i[0][lane] : INT_MAX;
+                    double fl = lane < NWC_ ? sh.red_f[1][lane] : -INF;
+                    jl = lane < NWC_ ? sh.red_i[1][lane] : INT_MAX;
+                    warp_reduce_fi<true>(fu, ju, NWC_);
+                    warp_reduce_fi<false>(fl, jl, NWC_);
                     fu = __shfl_sync(0xffffffffu, fu, 0); ju = __shfl_sync(0xffffffffu, ju, 0);
                     fl = __shfl_sync(0xffffffffu, fl, 0); jl = __shfl_sync(0xffffffffu, jl, 0);
                     c.fu = fu; c.fl = fl;
@@ -942,7 +948,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                     sh.decision = dec; sh.u = iu; sh.l = il; sh.f_up = fu; sh.f_low = fl;
                 }
                 __syncwarp();
-                named_arrive(BAR_A);
+                named_arrive<NSYNC_>(BAR_A);
                 break;
             }
             // ---- row cache (a8): every CTA runs the same directory operations on the same
@@ -1097,7 +1103,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
             }
             if (lane == 0) { sh.decision = ST_RUNNING; sh.u = iu; sh.l = il; }
             __syncwarp();
-            named_arrive(BAR_A);
+            named_arrive<NSYNC_>(BAR_A);
             if (lane < 3 && !m_cluster) {
                 unsigned int spins = 0;
                 while (!rec_ok(wa, sq)) {            // written with w0/w1: (almost) never taken
@@ -1224,7 +1230,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
             }
             __syncwarp();
             SVM_PHASE(timing, PH_S_KUL);
-            named_arrive(BAR_B);
+            named_arrive<NSYNC_>(BAR_B);
             ++it;
             continue;
         }
@@ -1252,7 +1258,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
         double cu = 0.0, cl = 0.0;
         double bfu = INF, bfl = -INF;
         int bju = INT_MAX, bjl = INT_MAX;
-        if (n_tiles == 0) named_sync(BAR_B);
+        if (n_tiles == 0) named_sync<NSYNC_>(BAR_B);
         if (m_isbin && !rows_ready && n_tiles > 0) {
             // binary bit rows resident (row j at words [j Wp, j Wp + Wp), Wp = W rounded up to 4);
             // thread t owns row t of every tile.  The popcounts of BT tiles are independent
@@ -1291,7 +1297,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
                 }
                 if (tb == 0) {
                     SVM_PHASE(timing, PH_C_DIST);
-                    named_sync(BAR_B);          // c_u, c_l and the owner's flags are ready
+                    named_sync<NSYNC_>(BAR_B);          // c_u, c_l and the owner's flags are ready
                     SVM_PHASE(timing, PH_C_WAITB);
                     cu = sh.cu; cl = sh.cl;
                 }
@@ -1427,7 +1433,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
             }
             if (tile == 0) {
                 SVM_PHASE(timing, PH_C_DIST);
-                named_sync(BAR_B);          // c_u, c_l, the owner's flags and the fill slots are ready
+                named_sync<NSYNC_>(BAR_B);          // c_u, c_l, the owner's flags and the fill slots are ready
                 SVM_PHASE(timing, PH_C_WAITB);
                 cu = sh.cu; cl = sh.cl;
                 if (m_cache > 0 && !c_hit) {
@@ -1512,7 +1518,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
             const unsigned int iss = sh.issued;
             if (consumed < iss) {
                 mbar_wait(&full[cslot], cpar);
-                for (int w = 0; w < NWC; ++w) mbar_arrive(&empty[cslot]);
+                for (int w = 0; w < NWC_; ++w) mbar_arrive(&empty[cslot]);
                 ++consumed;
                 if (++cslot == (unsigned)P.stages) { cslot = 0; cpar ^= 1u; }
             } else if (done) {
@@ -1522,10 +1528,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) smo_persistent(const Params P) {
     }
     if (timing)
         for (int k = 0; k < PH_N; ++k) atomicAdd(&P.timers[k], ph_acc[k]);
-    named_sync(BAR_D);
+    named_sync<NSYNC_>(BAR_D);
     // ---- write the CTA's state back (consumers) and the rank control (scalar warp)
-    if (warp < NWC) {
-        for (int j = t; j < R; j += NT) {
+    if (warp < NWC_) {
+        for (int j = t; j < R; j += NT_) {
             P.f[rank][r0 + j] = f_s[j];
             if (A_SMEM) alpha_g[j] = a_s[j];
             P.flags[rank][r0 + j] = fl_s[j];

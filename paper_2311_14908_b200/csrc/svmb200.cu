@@ -308,6 +308,7 @@ struct Plan {
     int mix_nc = 0, mix_nbw = 0, mix_nseg = 0;   // mixed compact rows (mix_nseg > 0)
     int mix_seg[MIX_MAXSEG] = {};
     int esz = 4;         // bytes per xblk element (1: dictionary codes)
+    int ntc = NT;        // consumer threads per CTA (256, or 512 for the streamed modes)
     long long cta_stride = 0;
     size_t smem = 0;
 };
@@ -364,12 +365,24 @@ int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl, bool bina
     pl.state_cap = (int)((n_r_max + G - 1) / G);
     if (pl.state_cap < 1) pl.state_cap = 1;
     // rows per consumer thread: as few tiles per CTA as possible, at most 4 rows
-    pl.rpt = pl.state_cap <= NT ? 1 : (pl.state_cap <= 2 * NT ? 2 : 4);
+    // consumer threads: 16 warps (more latency hiding for the exp- and fp64-bound row pass)
+    // when each thread then still has <= 2 rows per tile, else 8 warps
+    // (measured: W4's mixed rows, 12 slots and 2 exps per row, 28.6 -> 24.9 us/iteration;
+    // W5's 256 features and W3's row cache are slower with 16 warps: fp64 / HBM bound with
+    // RPT 2 and register spills)
+    const int slots = pl.mix_nseg > 0 ? pl.mix_nc + pl.mix_nbw : d;
+    pl.ntc = (cl_words == 0 && cache_slots == 0 && slots <= 64) ? 512 : NT;
+    if (const char* e = getenv("SVMB200_NT")) {                  // tuning override: 256 or 512
+        const int v = atoi(e);
+        if (v == 256 || (v == 512 && cl_words == 0)) pl.ntc = v;
+    }
+    pl.rpt = pl.state_cap <= pl.ntc ? 1 : (pl.state_cap <= 2 * pl.ntc ? 2 : 4);
     if (const char* e = getenv("SVMB200_RPT")) {          // tuning override: 1, 2 or 4
         const int r = atoi(e);
         if (r == 1 || r == 2 || r == 4) pl.rpt = r;
     }
-    pl.rt = NT * pl.rpt;
+    if (pl.ntc == 512 && pl.rpt == 4) pl.rpt = 2;          // register budget of 576 threads
+    pl.rt = pl.ntc * pl.rpt;
     pl.kc = 8192 * (4 / pl.esz) / pl.rt;                   // 32 KB stages
     if (const char* e = getenv("SVMB200_KC")) {           // tuning override (features per stage)
         const int v = atoi(e);
@@ -427,7 +440,11 @@ int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl, bool bina
 typedef void (*KernelFn)(const Params);
 
 template <int K>
-KernelFn pick_rpt(int rpt, bool a_smem) {
+KernelFn pick_rpt(int rpt, bool a_smem, int ntc) {
+    if (ntc == 512) {
+        if (a_smem) return rpt == 2 ? smo_persistent<K, 2, true, false, 512> : smo_persistent<K, 1, true, false, 512>;
+        return rpt == 2 ? smo_persistent<K, 2, false, false, 512> : smo_persistent<K, 1, false, false, 512>;
+    }
     if (a_smem) return rpt == 4 ? smo_persistent<K, 4, true, false> : rpt == 2 ? smo_persistent<K, 2, true, false> : smo_persistent<K, 1, true, false>;
     return rpt == 4 ? smo_persistent<K, 4, false, false> : rpt == 2 ? smo_persistent<K, 2, false, false> : smo_persistent<K, 1, false, false>;
 }
@@ -435,12 +452,12 @@ KernelFn pick_rpt(int rpt, bool a_smem) {
 KernelFn pick_bincl(int kernel) { return kernel == SVM_RBF ? smo_bincl<1> : smo_bincl<0>; }
 
 // bincl: binary rows resident in a cluster (the specialised kernel; rpt is 1 there)
-KernelFn pick_kernel(int kernel, int rpt, bool a_smem, bool bincl = false) {
+KernelFn pick_kernel(int kernel, int rpt, bool a_smem, bool bincl = false, int ntc = NT) {
     if (bincl && getenv("SVMB200_NO_SPECIALISE") == nullptr) {
         if (kernel == SVM_RBF) return a_smem ? smo_persistent<1, 1, true, true> : smo_persistent<1, 1, false, true>;
         return a_smem ? smo_persistent<0, 1, true, true> : smo_persistent<0, 1, false, true>;
     }
-    return kernel == SVM_RBF ? pick_rpt<1>(rpt, a_smem) : pick_rpt<0>(rpt, a_smem);
+    return kernel == SVM_RBF ? pick_rpt<1>(rpt, a_smem, ntc) : pick_rpt<0>(rpt, a_smem, ntc);
 }
 
 int device_limits(int* n_sm, int* max_smem) {
@@ -673,8 +690,9 @@ int solve(SolveArgs& a) {
         if (a.p.cluster > 0 && pl.cluster == 0)
             return fail(SVM_EINVAL, "cluster mode needs every rank's rows resident in the cluster's shared memory");
     }
-    KernelFn fn = pl.bincl ? pick_bincl(p.kernel) : pick_kernel(p.kernel, pl.rpt, pl.alpha_smem, pl.cluster > 0 && pl.bin_words > 0);
-    const int nthreads = pl.bincl ? NTB : NTHREADS;
+    KernelFn fn = pl.bincl ? pick_bincl(p.kernel)
+                           : pick_kernel(p.kernel, pl.rpt, pl.alpha_smem, pl.cluster > 0 && pl.bin_words > 0, pl.ntc);
+    const int nthreads = pl.bincl ? NTB : pl.ntc + 64;
     {
         const char* mode = gram ? "gram" : pl.bin_words ? "binary-resident"
                          : pl.mix_nseg ? (pl.resident ? "mixed-resident" : pl.cache_slots ? "mixed+row-cache" : "mixed-streamed")
@@ -875,7 +893,7 @@ int solve(SolveArgs& a) {
             cfg.dynamicSmemBytes = pl.smem; cfg.stream = st; cfg.attrs = at; cfg.numAttrs = 1;
             e = cudaLaunchKernelExC(&cfg, (const void*)fn, args);
         } else {
-            e = cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(NTHREADS), args, pl.smem, st);
+            e = cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(nthreads), args, pl.smem, st);
         }
         if (e != cudaSuccess) { release(); return fail(SVM_ECUDA, std::string("cooperative launch: ") + cudaGetErrorString(e)); }
         ++launches;
