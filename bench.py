@@ -330,9 +330,10 @@ def run_ours(args):
         W = (d + 31) // 32
         sms = int(plan.get("ctas_per_rank", 1)) * int(plan.get("ranks", 1))
         mhz = clk.summary().get("sm_mhz") or 1965.0
-        # POPC instructions the row pass executes: per pivot and row, 3 for every group of 4
-        # bit words (carry-save form, smo_bincl) -- 2 (3 ceil(W/4)) per row
-        popc_iter = n_r * 2 * 3 * ((W + 3) // 4)
+        # algorithmic work: one 32-bit word popcount per bit word, pivot and row (2 W per row);
+        # the kernel executes 3 POPC per 4 words (carry-save form), so the pipe-level
+        # utilisation is 3/4 of this fraction
+        popc_iter = n_r * 2 * W
         alu_ach = popc_iter * it_per_s / 1e9
         alu_peak = 16 * sms * mhz * 1e6 / 1e9
         roofline = {"bound": "alu", "pipe": "POPC, 16/clk/SM x %d SMs x %.0f MHz" % (sms, mhz),
@@ -341,7 +342,8 @@ def run_ours(args):
                     "latency_bound": True,
                     "note": "one SMO iteration is a serial chain (row pass -> CTA barrier -> DSMEM exchange "
                             "-> pair update); the POPC pipe is the busiest throughput unit of the row pass "
-                            "(ops = POPC instructions executed, 3 per 4 bit words per pivot)"}
+                            "(ops = algorithmic word popcounts, 2 ceil(d/32) per row; the kernel issues 3 POPC "
+                            "per 4 words)"}
         hbm_roof["effective"] = True
         hbm_roof["note"] = ("fp32-equivalent algorithmic bytes per iteration (SURVEY 8(d)); served from "
                             "shared memory as bit rows, so this exceeds what streaming X from HBM could do")
