@@ -151,9 +151,10 @@ struct Params {
     // so the arithmetic is the dense path's.  dict_n = 0: not dictionary-coded.
     int dict_n;
     const double* dict;
-    int l2_keep_tiles;             // streamed X: tiles [0, l2_keep_tiles) of every CTA block are
-                                   // copied with an L2 evict_last policy, the rest evict_first, so
-                                   // that part of X stays in L2 across iterations (0 = no hints)
+    int l2_keep_chunks;            // streamed X: the first l2_keep_chunks stages (tile-major) of
+                                   // every CTA block are copied with an L2 evict_last policy, the
+                                   // rest evict_first, so that part of X stays in L2 across
+                                   // iterations (0 = no hints)
 };
 
 // phase timers (cycles, CTA 0): scalar warp lane 0 ...
@@ -694,8 +695,9 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
                 const unsigned char* src = xcta_b + ((long long)tile * P.d_pad * P.rt + (long long)chunk * P.kc * rp) * esz;
                 unsigned char* dst = ring_b + (size_t)slot * stage_floats * esz;
                 mbar_arrive_tx(&full[slot], bytes);
-                if (P.l2_keep_tiles > 0)
-                    bulk_g2s_hint(dst, src, bytes, &full[slot], tile < P.l2_keep_tiles ? pol_keep : pol_stream);
+                if (P.l2_keep_chunks > 0)
+                    bulk_g2s_hint(dst, src, bytes, &full[slot],
+                                  tile * P.n_chunks + chunk < P.l2_keep_chunks ? pol_keep : pol_stream);
                 else
                     bulk_g2s(dst, src, bytes, &full[slot]);
                 ++s;

@@ -762,11 +762,13 @@ int solve(SolveArgs& a) {
     // L2 residency of streamed X: keep the first tiles of every CTA block in L2
     // (SVMB200_L2_KEEP_MB, per GPU; tuning)
     if (!pl.resident && pl.bin_words == 0 && !gram && pl.mix_nseg == 0 && pl.esz == 4) {
-        long long keep_mb = 0;
+        // (measured on W5 shards: 48 MB kept per GPU -> 125k rows 31.4 -> 30.1 us/iteration,
+        // 1M rows 187 -> 184; more is not better, profiles/r1h/l2_keep_W5_shards.txt)
+        long long keep_mb = pl.cache_slots == 0 ? 48 : 0;
         if (const char* e = getenv("SVMB200_L2_KEEP_MB")) keep_mb = atoll(e);
-        const long long tile_bytes = (long long)pl.d_pad * pl.rt * 4;
+        const long long stage_bytes = (long long)pl.kc * pl.rt * 4;
         const long long ctas_here = (long long)a.ctas_per_rank * a.nranks_here;
-        if (keep_mb > 0 && tile_bytes > 0) P.l2_keep_tiles = (int)((keep_mb << 20) / (tile_bytes * ctas_here));
+        if (keep_mb > 0 && stage_bytes > 0) P.l2_keep_chunks = (int)((keep_mb << 20) / (stage_bytes * ctas_here));
     }
     P.sys_scope = a.mbox_local_alloc ? 0 : 1;
     const bool want_timers = getenv("SVMB200_PHASE_TIMERS") != nullptr;
@@ -938,7 +940,7 @@ int solve(SolveArgs& a) {
                                 "S.cand", "S.build"};
         fprintf(stderr, "[svmb200] cycles/iter of CTA 0 over %lld iters (rpt=%d kc=%d stages=%d smem=%zu a_smem=%d resident=%d bin_words=%d cache=%d gram=%d cluster=%d l2keep=%d):",
                 hc.it, pl.rpt, pl.kc, pl.stages, pl.smem, (int)pl.alpha_smem, (int)pl.resident, pl.bin_words,
-                pl.cache_slots, gram ? 1 : 0, pl.cluster, P.l2_keep_tiles);
+                pl.cache_slots, gram ? 1 : 0, pl.cluster, P.l2_keep_chunks);
         for (int k = 0; k < PH_N; ++k)
             fprintf(stderr, " %s=%.0f", nm[k], hc.it ? (double)tm[k] / hc.it : 0.0);
         fprintf(stderr, "\n");
