@@ -624,7 +624,6 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
     const long long gbase = P.row_off[rank] + r0;            // global index of local row 0
     const int n_tiles = (R + P.rt - 1) / P.rt;
     const int rt_log2 = __ffs(P.rt) - 1;                     // rt = 256 RPT: a power of two
-    const float* xcta = P.xblk[rank] + (long long)cta * P.cta_stride;
     const unsigned char* xcta_b = reinterpret_cast<const unsigned char*>(P.xblk[rank]) + (long long)cta * P.cta_stride * esz;
     double* alpha_g = P.alpha[rank] + r0;                    // this CTA's alpha (global)
     const double C = P.C;
