@@ -36,7 +36,9 @@ constexpr int BK = 32;           // tf32 elements per stage (128 B per row)
 constexpr int STAGES = 3;
 constexpr int TILE_FLOATS = BM * BK;           // 4096 floats = 16 KB per operand block
 constexpr int STAGE_BYTES = 4 * TILE_FLOATS * 4;  // A hi, A lo, B hi, B lo
-constexpr int NTHREADS = 192;
+constexpr int EPI_WARPS = 16;                     // epilogue: EPI_WARPS / 4 warps per TMEM lane quarter
+constexpr int NPART = EPI_WARPS / 4;              // column parts of an accumulator tile
+constexpr int NTHREADS = 64 + 32 * EPI_WARPS;
 constexpr int TMEM_COLS = 2 * BN;
 
 // element (r, k) of a [rows][BK] block in the core-matrix order
@@ -102,12 +104,13 @@ k_predict_tc(const float* __restrict__ A,   // packed test rows [m_tiles][k_chun
     float* stage_base = reinterpret_cast<float*>(smem_raw);
     __shared__ uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
     __shared__ uint32_t tmem_base_sh;
+    __shared__ double part_sh[NPART][BM];           // the column parts' partial sums
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int mt = blockIdx.x;
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+        for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], EPI_WARPS); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -173,8 +176,10 @@ k_predict_tc(const float* __restrict__ A,   // packed test rows [m_tiles][k_chun
             }
         }
     } else {
-        // ---------------- epilogue: warps 2..5 -> TMEM lane quarter (warp % 4)
+        // ---------------- epilogue: warps 2.. -> TMEM lane quarter (warp % 4); the warps of a
+        // quarter split the columns of every accumulator tile into NPART parts
         const int quarter = warp & 3;
+        const int half = (warp - 2) >> 2;                 // column part
         const int row = quarter * 32 + lane;
         const long long gi = (long long)mt * BM + row;
         const double q_t = qt[(long long)mt * BM + row];
@@ -186,7 +191,7 @@ k_predict_tc(const float* __restrict__ A,   // packed test rows [m_tiles][k_chun
             const double* qs_t = qs + (size_t)nt * BN;
             const double* cf_t = cf + (size_t)nt * BN;
 #pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += 32) {
+            for (int c0 = half * (BN / NPART); c0 < (half + 1) * (BN / NPART); c0 += 32) {
                 uint32_t v[32];
                 const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN + c0;
                 asm volatile(
@@ -217,7 +222,14 @@ k_predict_tc(const float* __restrict__ A,   // packed test rows [m_tiles][k_chun
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
         }
-        if (gi < m) dec[gi] = acc_d + b;
+        // the parts' partial sums, combined in a fixed order (part 0, 1, ...)
+        part_sh[half][row] = acc_d;
+        asm volatile("bar.sync 1, %0;" :: "n"(32 * EPI_WARPS) : "memory");
+        if (half == 0 && gi < m) {
+            double sum = acc_d;
+            for (int p = 1; p < NPART; ++p) sum += part_sh[p][row];
+            dec[gi] = sum + b;
+        }
     }
     __syncthreads();
     if (warp == 1) {
