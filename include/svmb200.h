@@ -15,6 +15,12 @@
  *     b_low - b_up <= 2 tol, b = -(b_up + b_low)/2
  *     Kernels: linear x.z and RBF exp(-gamma ||x - z||^2)
  *   svm_predict                dec(x) = sum_s coef_s K(x_s, x) + b
+ *   svm_train_gd_dev           the paper's gradient-descent (TensorFlow) trainer read as
+ *                              projected gradient ascent on the same dual
+ *
+ * Row storage is chosen per solve and never changes the arithmetic: fp32 rows; bit rows
+ * when every value is 0 or 1; mixed bit / fp32 rows when >= 32 columns are 0/1; one-byte
+ * dictionary codes when X has <= 256 distinct values (svm_last_plan() reports which).
  *
  * Arithmetic contract: X is float32; every kernel value,
  * the error vector f, the multipliers and all reductions are fp64; distances and
