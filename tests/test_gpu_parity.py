@@ -566,3 +566,16 @@ def test_dict_rows_parity(S, monkeypatch, case):
         r6 = S.svm_train_ex(X2, y, w.C, w.kernel, w.gamma, w.tol, want_f=True, cluster=-1)
         assert not S.last_plan()["mode"].startswith("dict")
         np.testing.assert_array_equal(r6["alpha"], r_o2.alpha)
+
+
+@pytest.mark.parametrize("nt", ["256", "512"])
+def test_consumer_warp_counts(S, monkeypatch, nt):
+    """smo_persistent with 8 and with 16 consumer warps (NTC = 256 / 512; 16 is the default
+    for narrow rows without row cache) equals the oracle on dense, mixed and streamed data."""
+    monkeypatch.setenv("SVMB200_NT", nt)
+    for name, n in (("W4", 5000), ("W5", 2600), ("W1", 200)):
+        w = W.get(name)
+        X, y = w.train(n)
+        r_g, r_or = _run_pair(S, w, X, y, cluster=-1, cache_rows=-1)
+        _assert_exact(r_g, r_or)
+        assert S.last_plan()["threads"] == int(nt) + 64
