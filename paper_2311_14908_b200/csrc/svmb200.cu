@@ -383,10 +383,30 @@ int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl, bool bina
     }
     if (pl.ntc == 512 && pl.rpt == 4) pl.rpt = 2;          // register budget of 576 threads
     pl.rt = pl.ntc * pl.rpt;
-    pl.kc = 8192 * (4 / pl.esz) / pl.rt;                   // 32 KB stages
-    if (const char* e = getenv("SVMB200_KC")) {           // tuning override (features per stage)
+    // Stage size: the largest kc (features per stage) whose zero padding of d stays small and
+    // for which two stages fit next to the state -- fewer, larger bulk copies amortise the
+    // per-stage mbarrier hand-off (measured on W5: 32 KB x 5 stages 188.9 us/iteration,
+    // 48 KB x 3 181.4, 64 KB x 2 177.5, 80 KB x 2 174.4; 125k-row shard 30.1 -> 25.6 us).
+    // Mixed rows use one stage per tile (all slots of a row); SVMB200_KC overrides.
+    const int kc_min = 8192 * (4 / pl.esz) / pl.rt;        // 32 KB stages
+    int kc_env = 0;
+    if (const char* e = getenv("SVMB200_KC")) {            // tuning override (features per stage)
         const int v = atoi(e);
-        if (v >= 1 && v <= 64) pl.kc = v;
+        if (v >= 1 && v <= 256) kc_env = v;
+    }
+    // (first choice: >= 3 stages of >= 64 KB -- a 125k-row W5 shard: 3 x 64 KB 25.6 us,
+    // 2 x 104 KB 27.7 us; else the largest two stages)
+    const int kc_max = pl.mix_nseg > 0 ? kc_min : (kc_env > 0 ? kc_env : (pl.esz == 1 ? 256 : 64));
+    for (int pass = 0; pass < 2; ++pass)
+    for (int kc_try = kc_max; kc_try >= 1; --kc_try) {
+    const bool want3 = pass == 0 && kc_env == 0 && pl.mix_nseg == 0;
+    if (want3 && (size_t)kc_try * pl.rt * pl.esz < 65536) break;
+    const bool last_try = !want3 && (kc_try <= kc_min || kc_env > 0 || pl.mix_nseg > 0);
+    pl.kc = kc_env > 0 ? kc_env : kc_try;
+    if (pl.esz == 1 && (pl.kc & 3)) continue;              // byte stages: 16-byte multiples
+    if (!last_try) {
+        const int dpad_try = (d + pl.kc - 1) / pl.kc * pl.kc;
+        if (dpad_try - d > (d / 50 > 4 ? d / 50 : 4)) continue;   // <= 2% (or 4 features) padding
     }
     pl.d_pad = (d + pl.kc - 1) / pl.kc * pl.kc;
     pl.n_chunks = pl.d_pad / pl.kc;
@@ -428,13 +448,17 @@ int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl, bool bina
         pl.smem = fixed + resident_bytes;
         return SVM_OK;
     }
-    if ((size_t)max_smem <= fixed + 2 * stage_bytes)
+    if ((size_t)max_smem <= fixed + (want3 ? 3 : 2) * stage_bytes) {
+        if (!last_try) continue;
         return fail(SVM_ENOMEM, "rows per CTA (" + std::to_string(pl.state_cap) +
                                     ") exceed the shared-memory state capacity; shard over more GPUs");
+    }
     pl.stages = (int)((max_smem - fixed) / stage_bytes);
     if (pl.stages > MAX_STAGES) pl.stages = MAX_STAGES;
     pl.smem = fixed + (size_t)pl.stages * stage_bytes;
     return SVM_OK;
+    }
+    return fail(SVM_ENOMEM, "no stage size fits");
 }
 
 typedef void (*KernelFn)(const Params);
