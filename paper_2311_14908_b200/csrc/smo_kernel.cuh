@@ -926,11 +926,20 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
                       sh.timeout != 0;
                 if (timing) ph_acc[PH_C_PIVOT] += rounds;     // (timers only) poll rounds of lane 0
                 SVM_PHASE(timing, PH_S_POLL);
-                // the warp's winners and the records they came from
-                fu = best.fu; fl = best.fl;
-                iu = best.iu; il = best.il;
-                warp_reduce_fi<true>(fu, iu);
-                warp_reduce_fi<false>(fl, il);
+                // the warp's winners (lexicographic (f, index) minimum / maximum through three
+                // redux.sync on the order-preserving key, R22) and the records they came from
+                {
+                    unsigned long long kwu, kwl;
+                    unsigned iwu, iwl;
+                    argmin_redux(0xffffffffu, best.iu == INT_MAX ? ~0ull : fkey(best.fu),
+                                 best.iu == INT_MAX ? 0xffffffffu : (unsigned)best.iu, kwu, iwu);
+                    argmin_redux(0xffffffffu, best.il == INT_MAX ? ~0ull : ~fkey(best.fl),
+                                 best.il == INT_MAX ? 0xffffffffu : (unsigned)best.il, kwl, iwl);
+                    iu = iwu == 0xffffffffu ? INT_MAX : (int)iwu;
+                    il = iwl == 0xffffffffu ? INT_MAX : (int)iwl;
+                    fu = iu == INT_MAX ? INF : fkey_inv(kwu);
+                    fl = il == INT_MAX ? -INF : fkey_inv(~kwl);
+                }
                 const unsigned mu = __ballot_sync(0xffffffffu, best.iu == iu);
                 const unsigned ml = __ballot_sync(0xffffffffu, best.il == il);
                 rec_u = __shfl_sync(0xffffffffu, best.gu, mu ? __ffs(mu) - 1 : 0);
