@@ -883,14 +883,20 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
                 Cand c;
                 int ju, jl;                                   // this CTA's candidates (local rows)
                 {
-                    double fu = lane < NWC_ ? sh.red_f[0][lane] : INF;
-                    ju = lane < NWC_ ? sh.red_i[0][lane] : INT_MAX;
-                    double fl = lane < NWC_ ? sh.red_f[1][lane] : -INF;
-                    jl = lane < NWC_ ? sh.red_i[1][lane] : INT_MAX;
-                    warp_reduce_fi<true>(fu, ju, NWC_);
-                    warp_reduce_fi<false>(fl, jl, NWC_);
-                    fu = __shfl_sync(0xffffffffu, fu, 0); ju = __shfl_sync(0xffffffffu, ju, 0);
-                    fl = __shfl_sync(0xffffffffu, fl, 0); jl = __shfl_sync(0xffffffffu, jl, 0);
+                    // the CTA candidate: lexicographic minimum / maximum of the consumer
+                    // warps' candidates (local rows: lower local = lower global index)
+                    const int wju = lane < NWC_ ? sh.red_i[0][lane] : INT_MAX;
+                    const int wjl = lane < NWC_ ? sh.red_i[1][lane] : INT_MAX;
+                    unsigned long long kwu, kwl;
+                    unsigned iwu, iwl;
+                    argmin_redux(0xffffffffu, wju == INT_MAX ? ~0ull : fkey(sh.red_f[0][lane & (NWC_ - 1)]),
+                                 wju == INT_MAX ? 0xffffffffu : (unsigned)wju, kwu, iwu);
+                    argmin_redux(0xffffffffu, wjl == INT_MAX ? ~0ull : ~fkey(sh.red_f[1][lane & (NWC_ - 1)]),
+                                 wjl == INT_MAX ? 0xffffffffu : (unsigned)wjl, kwl, iwl);
+                    ju = iwu == 0xffffffffu ? INT_MAX : (int)iwu;
+                    jl = iwl == 0xffffffffu ? INT_MAX : (int)iwl;
+                    const double fu = ju == INT_MAX ? INF : fkey_inv(kwu);
+                    const double fl = jl == INT_MAX ? -INF : fkey_inv(~kwl);
                     c.fu = fu; c.fl = fl;
                     c.iu = (ju == INT_MAX) ? INT_MAX : (int)(gbase + ju);
                     c.il = (jl == INT_MAX) ? INT_MAX : (int)(gbase + jl);
