@@ -1,13 +1,26 @@
 """bench.py -- SVM train time-to-converge on B200 (BASELINE.json metric), one JSON line.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload W2]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload W5]
 
-A step is one pass of the whole hot path over the workload: stage + SMO solve to
-convergence and batched prediction of the held-out rows
-(a11).  `value` is the time-to-converge of the solve (seconds, lower is better; mean of
-K steps, max over ranks), measured with CUDA events on the launching stream with the
-inputs already resident in HBM.  `e2e` is the same solve through the host C-ABI call
-(svm_train_ex / svm_predict) with host buffers, H2D/D2H inside the timed region.
+Headline workload: W5 (BASELINE.json configs[4], the "1/2/4/8 GPUs" scaling config,
+n = 1,000,000, d = 256, RBF).  `value` = the time-to-converge of the SMO solve (seconds,
+lower is better) on inputs already resident in HBM, measured with CUDA events on the
+launching stream, max over ranks.
+
+Steps.  One W5 solve is ~4*10^5 SMO iterations (~1 minute), so a step is one contiguous
+window of that solve: the library runs the solve as K persistent launches of
+ceil(T / K) iterations each (svm_params.iters_per_launch; T = the trajectory's iteration
+count, deterministic), and the timed region -- barrier + synchronize on
+both sides -- is the whole solve from device-resident X to alpha and b: validation,
+staging (a1), the K launches (a2-a7) and finalisation (a10).  `value` = the sum of the K
+windows = time-to-converge; `ms_per_step` = value / K.  The W warm-up steps are the first
+W windows of a separate solve (same launch configuration).  Small workloads (--workload
+W1..W3) instead time K whole solves (`value` = their mean).
+
+`e2e` = the same solve through the host C-ABI call (svm_train_ex, host buffers, H2D of X
+and y and D2H of alpha inside the timed region).  Extra keys: the batched prediction of
+the 1M held-out rows on the tensor cores (a11), the time-to-converge of W2-W4, the
+projected-GD trainer, and the CPU oracle timed on a bounded sample (`cpu_baseline`).
 
 N > 1 is launched by torchrun (one process per GPU): the rows are sharded and every
 iteration exchanges per-CTA candidate records over NVLink (strong scaling: the problem
@@ -17,7 +30,9 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -29,18 +44,37 @@ sys.path.insert(0, ROOT)
 
 METRIC = "SVM train time-to-converge (s) & SMO iters/s at 1/2/4/8 B200; kernel-row HBM GB/s"
 
+# Iteration counts of the deterministic trajectories (the oracle and the GPU
+# take the same steps).  Used only to size the windows of a step; if a solve takes a
+# different count, the number of launches (reported as `launches`) differs from K.
+PLAN_ITERS = {"W2": 42790, "W3": 11659, "W4": 133952, "W5": 411469}
+WINDOWED = ("W4", "W5")
+
 
 def peaks():
+    """(HBM GB/s, bf16 dense TF/s, kind) from the driver-written MEASURED_PEAKS.json."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
             p = json.load(fh)
-        return float(p["hbm_gbs"]), "measured"
+        return float(p["hbm_gbs"]), float(p.get("bf16_tflops", 2250.0)), "measured"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, 2250.0, "fallback"
+
+
+def cpu_model() -> str:
+    try:
+        out = subprocess.check_output(["lscpu"], timeout=10).decode()
+        for ln in out.splitlines():
+            if ln.startswith("Model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return platform.processor() or "unknown"
 
 
 class Clocks:
-    """Samples nvidia-smi during the timed region (B200_PROFILING.md clocks line)."""
+    """Samples SM clocks and throttle reasons during the timed region (NVML in-process;
+    B200_PROFILING.md clocks line)."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -53,8 +87,6 @@ class Clocks:
         self._t = None
 
     def _nvml_row(self, pynvml, h):
-        # the same fields as the nvidia-smi query, read in-process through NVML (an
-        # nvidia-smi subprocess every 0.2 s contends with the timed region's driver calls)
         sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
         mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
         pw = pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0
@@ -83,7 +115,7 @@ class Clocks:
                         self.rows.append([c.strip() for c in out.split(",")])
                 except Exception:
                     pass
-                self._stop.wait(0.2)
+                self._stop.wait(0.5)
         self._t = threading.Thread(target=run, daemon=True)
         self._t.start()
         return self
@@ -110,53 +142,50 @@ def oracle_sample(w, X, y, budget_s: float, iters_total: int):
     budget_s seconds of CPU work; returns (iters/s, iterations run, threads)."""
     from oracle import oracle as O
     t0 = time.perf_counter()
-    O.train(X, y, w.C, w.kernel, w.gamma, w.tol, max_iter=5)
-    probe = max(time.perf_counter() - t0, 1e-6) / 5
-    k = int(max(5, min(iters_total, budget_s / probe)))
+    O.train(X, y, w.C, w.kernel, w.gamma, w.tol, max_iter=2)
+    probe = max(time.perf_counter() - t0, 1e-6) / 2
+    k = int(max(2, min(iters_total, budget_s / probe)))
     t0 = time.perf_counter()
     r = O.train(X, y, w.C, w.kernel, w.gamma, w.tol, max_iter=k)
     dt = time.perf_counter() - t0
     return r.iterations / dt, r.iterations, O.num_threads()
 
 
-def golden_iterations(name: str):
-    import numpy as np
-    p = os.path.join(ROOT, "tests", "golden", f"{name}_oracle.npz")
-    if os.path.exists(p):
-        return int(np.load(p)["iterations"])
-    return None
-
-
 # ------------------------------------------------------------------ reference arm
 def run_reference(args):
+    """The CPU oracle (the tier's reference arm), as it stands, on the bench workload:
+    each step times a bounded sample of its trajectory (~args.ref_budget s, capped so
+    the whole run stays within a few minutes); value = the time-to-converge projected
+    from the sampled iteration rate."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     from gen import workloads as W
     w = W.get(args.workload)
     X, y = w.train()
-    iters = golden_iterations(args.workload)
+    iters = PLAN_ITERS.get(w.name)
+    budget = min(args.ref_budget, 150.0 / max(1, args.steps + args.warmup))
     per_step = []
     k_iters = 0
     threads = 1
     for s in range(args.warmup + args.steps):
-        ips, k, threads = oracle_sample(w, X, y, args.ref_budget, iters or 10 ** 9)
+        ips, k, threads = oracle_sample(w, X, y, budget, iters or 10 ** 9)
         if s >= args.warmup:
             per_step.append(ips)
             k_iters = k
     ips = statistics.mean(per_step)
     value = (iters / ips) if iters else None
+    sample = (f"first {k_iters} SMO iterations of {w.name} (n={w.n}) per step on {threads} host threads "
+              f"({cpu_model()}); time-to-converge projected to the trajectory's {iters} iterations")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * k_iters / ips, "higher_is_better": False, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "ms_per_step": 1e3 * value / args.steps if value else None, "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{w.name}: {w.config}", "n": w.n, "d": w.d},
         "smo_iters_per_s": ips,
         "cpu_baseline": {"value": value, "unit": "s", "cores": threads, "kind": "oracle",
-                         "sample": f"{k_iters} SMO iterations of {w.name} per step on {threads} host "
-                                   f"threads; time-to-converge projected with the oracle's own "
-                                   f"iteration count {iters}"},
+                         "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -180,21 +209,17 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     S.lib()
+    hbm, bf16, peak_kind = peaks()
     w = W.get(args.workload)
     X, y = w.train()
-    Xt, _ = w.test(args.predict_rows if args.predict_rows >= 0 else None)
     n, d = X.shape
-    m = Xt.shape[0]
     blocks = S.shard_rows(n, world)
     lo, hi = blocks[rank]
     stream = torch.cuda.current_stream()
     Xd_full = torch.from_numpy(X).to(dev)
     yd_full = torch.from_numpy(y).to(dev)
-    Xl = Xd_full[lo:hi].contiguous()
-    yl = yd_full[lo:hi].contiguous()
-    mt = -(-m // world)
-    tl, th = min(m, rank * mt), min(m, (rank + 1) * mt)
-    Xt_d = torch.from_numpy(Xt[tl:th]).to(dev).contiguous()
+    Xl = Xd_full[lo:hi].contiguous() if world > 1 else Xd_full
+    yl = yd_full[lo:hi].contiguous() if world > 1 else yd_full
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > L2 (126 MB)
     comm = None
     if world > 1:
@@ -202,248 +227,271 @@ def run_ours(args):
         uid = broadcast_uid(S.svm_comm_unique_id() if rank == 0 else None, dev)
         comm = S.svm_comm_init(rank, world, uid, local)
 
-    def train_once():
-        if world == 1:
-            return S.svm_train_dev(Xd_full, yd_full, w.C, w.kernel, w.gamma, w.tol, stream=stream)
-        return S.svm_train_shard(comm, Xl, yl, lo, n, w.C, w.kernel, w.gamma, w.tol, stream=stream)
+    windowed = w.name in WINDOWED and w.name in PLAN_ITERS
+    window = math.ceil(PLAN_ITERS[w.name] / args.steps) if windowed else 0
 
-    def predict_once(r):
-        # support vectors of the whole model (alpha gathered across ranks at N > 1)
-        alpha = r["alpha"]
-        if world > 1:
-            from paper_2311_14908_b200.dist import gather_rows
-            alpha = gather_rows(alpha.contiguous(), blocks, dev)
-        sv = alpha > 1e-8
-        coef = (alpha * yd_full.to(torch.float64))[sv].contiguous()
-        Xsv = Xd_full[sv].contiguous()
-        return S.svm_predict_dev(Xsv, coef, r["b"], w.kernel, w.gamma, Xt_d, stream=stream,
-                                 mode=args.predict_mode), int(sv.sum())
+    def train(**kw):
+        if world == 1:
+            return S.svm_train_dev(Xd_full, yd_full, w.C, w.kernel, w.gamma, w.tol, stream=stream, **kw)
+        return S.svm_train_shard(comm, Xl, yl, lo, n, w.C, w.kernel, w.gamma, w.tol, stream=stream, **kw)
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
-    # ---- warm-up
-    for _ in range(args.warmup):
-        r = train_once()
-        predict_once(r)
-    barrier()
-
-    # ---- timed steps
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    infos = []
-    nsv = 0
-    launches0 = S.kernel_launches()
-    with Clocks(local) as clk:
-        barrier()
-        for k in range(args.steps):
-            flush.fill_(float(k))                      # L2 flush between steps
-            e0, e1, e2 = ev[k]
-            e0.record(stream)
-            r = train_once()
-            e1.record(stream)
-            _, nsv = predict_once(r)
-            e2.record(stream)
-            infos.append(r["info"])
-        barrier()
-    our_launches = S.kernel_launches() - launches0
-    plan = S.last_plan()
-    t_train = [a.elapsed_time(b) * 1e-3 for a, b, _ in ev]
-    t_step = [a.elapsed_time(c) * 1e-3 for a, _, c in ev]
-    t_solve = [i["seconds_solve"] for i in infos]
-    iters = infos[-1]["iterations"]
-    launches = infos[-1]["launches"]
-
-    def gmax(vals):
+    def gmax(v):
         if world > 1:
             from paper_2311_14908_b200.dist import max_over_ranks
-            return max_over_ranks(statistics.mean(vals), dev)
-        return statistics.mean(vals)
+            return max_over_ranks(v, dev)
+        return v
 
-    train_s = gmax(t_train)
-    step_s = gmax(t_step)
-    solve_s = gmax(t_solve)
-
-    # ---- e2e through the host C-ABI (host buffers; H2D/D2H inside the timed region)
-    e2e = None
-    if world == 1:
-        e2e_t = []
-        for k in range(max(1, min(args.steps, 3))):
-            flush.fill_(float(k))
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            rr = S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol)
-            svh = rr["alpha"] > 1e-8
-            S.svm_predict(X[svh], (rr["alpha"] * y)[svh], rr["b"], w.kernel, w.gamma, Xt, mode=args.predict_mode)
-            e2e_t.append(time.perf_counter() - t0)
-        nsv_h = int(svh.sum())
-        e2e = {"value": statistics.mean(e2e_t), "unit": "s",
-               "h2d_bytes_per_step": int(n * d * 4 + n + nsv_h * d * 4 + nsv_h * 8 + m * d * 4),
-               "d2h_bytes_per_step": int(2 * n * 8 + m * 8),
-               "api": "svm_train_ex + svm_predict (host pointers)"}
+    # ---- warm-up: the first W windows of a solve (windowed) / W whole solves
+    if windowed:
+        if args.warmup > 0:
+            train(iters_per_launch=window, max_iter=args.warmup * window)
     else:
-        e2e_t = []
-        Xh = torch.from_numpy(X[lo:hi]).pin_memory()
-        yh = torch.from_numpy(y[lo:hi]).pin_memory()
-        ah = torch.empty(hi - lo, dtype=torch.float64).pin_memory()
-        for k in range(max(1, min(args.steps, 3))):
-            barrier()
-            e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            Xl.copy_(Xh, non_blocking=True); yl.copy_(yh, non_blocking=True)
-            rr = S.svm_train_shard(comm, Xl, yl, lo, n, w.C, w.kernel, w.gamma, w.tol, stream=stream)
-            ah.copy_(rr["alpha"], non_blocking=True)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            e2e_t.append(e0.elapsed_time(e1) * 1e-3)
-        e2e = {"value": gmax(e2e_t), "unit": "s",
-               "h2d_bytes_per_step": int((hi - lo) * (d * 4 + 1)),
-               "d2h_bytes_per_step": int((hi - lo) * 8),
-               "api": "svm_train_shard (pinned host -> device copies in the timed region)"}
+        for _ in range(args.warmup):
+            train()
+    barrier()
 
-    # ---- roofline of the dominant kernel (the persistent solver launch; its time is the
-    # device-event solve time).  Algorithmic bytes per iteration (miss
-    # path): n_r (4 d_p + 25) -- the fp32 X rows plus f read/write and the status byte.
-    hbm, peak_kind = peaks()
+    # ---- timed: one solve in K windows (windowed) / K whole solves
+    launches0 = S.kernel_launches()
+    infos = []
+    with Clocks(local) as clk:
+        flush.fill_(1.0)                               # L2 flush before the timed region
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        if windowed:
+            e0.record(stream)
+            r = train(iters_per_launch=window)
+            e1.record(stream)
+            infos.append(r["info"])
+            barrier()
+            t_total = e0.elapsed_time(e1) * 1e-3
+            t_step = t_total / args.steps
+        else:
+            ts = []
+            for k in range(args.steps):
+                flush.fill_(float(k))                  # L2 flush between steps
+                e0.record(stream)
+                r = train()
+                e1.record(stream)
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1) * 1e-3)
+                infos.append(r["info"])
+            barrier()
+            t_total = statistics.mean(ts)
+            t_step = t_total
+    our_launches = S.kernel_launches() - launches0
+    plan = S.last_plan()
+    info = infos[-1]
+    iters = info["iterations"]
+    value = gmax(t_total)
+    solve_s = gmax(statistics.mean(i["seconds_solve"] for i in infos))
+    alpha_last, b_last = r["alpha"], r["b"]
+
+    # ---- roofline of the dominant kernel, the persistent solver launch (~98% of the step):
+    # algorithmic bytes per iteration (miss path) n_r (4 d_p + 25) -- the
+    # fp32 X rows, f read + write, the status byte -- times the iterations of one launch,
+    # over the average launch duration (device events around the launch loop / launches).
     n_r = hi - lo
     d_p = (d + 3) // 4 * 4
     bytes_iter = n_r * (4 * d_p + 25)
-    it_per_s = iters / statistics.mean(t_solve)
-    achieved = bytes_iter * it_per_s / 1e9
+    per_launch_s = info["seconds_solve"] / max(1, info["launches"])
+    it_per_launch = iters / max(1, info["launches"])
+    achieved = bytes_iter * it_per_launch / per_launch_s / 1e9
     traffic = None
+    traffic_note = None
     tp = os.path.join(ROOT, "profiles", f"traffic_{w.name}.json")
     if os.path.exists(tp):
         try:
             tj = json.load(open(tp))
             if tj.get("kernel", "").split("<")[0] == plan.get("kernel", "").split("<")[0]:
-                traffic = tj.get("dram_bytes_per_launch")
+                if tj.get("dram_bytes_per_iter"):
+                    traffic = int(tj["dram_bytes_per_iter"] * it_per_launch)
+                    traffic_note = (f"ncu dram__bytes_read.sum + dram__bytes_write.sum per iteration "
+                                    f"({tj['dram_bytes_per_iter']:.4g} B, {tj.get('iterations')} iterations "
+                                    f"captured, {tj.get('source')}) x iterations per launch")
+                else:
+                    traffic = tj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    hbm_roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": traffic, "peak_kind": peak_kind, "kernel": plan.get("kernel"), "bytes_per_iter": bytes_iter}
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "traffic": traffic, "peak_kind": peak_kind, "kernel": plan.get("kernel"),
+                "bytes_per_iter": bytes_iter, "iters_per_launch": it_per_launch,
+                "launch_ms": per_launch_s * 1e3}
+    if traffic:
+        roofline["frac_measured_traffic"] = traffic / per_launch_s / 1e9 / hbm
+        roofline["traffic_note"] = traffic_note
+    hbm_eff = None
     if plan.get("mode") == "binary-resident":
-        # X is resident in shared memory as bit rows: no HBM stream.  The throughput-bound
-        # unit of the row pass is the POPC pipe (16 ops/clk/SM, tools/popc_bench.cu) on the
-        # SMs the solver occupies: 2 W popcounts per row per iteration (W = ceil(d/32)).
-        W = (d + 31) // 32
+        # X resident in shared memory as bit rows: no HBM stream; the POPC pipe of the SMs the
+        # solver occupies bounds the row pass
+        Wd = (d + 31) // 32
         sms = int(plan.get("ctas_per_rank", 1)) * int(plan.get("ranks", 1))
         mhz = clk.summary().get("sm_mhz") or 1965.0
-        # algorithmic work: one 32-bit word popcount per bit word, pivot and row (2 W per row);
-        # the kernel executes 3 POPC per 4 words (carry-save form), so the pipe-level
-        # utilisation is 3/4 of this fraction
-        popc_iter = n_r * 2 * W
-        alu_ach = popc_iter * it_per_s / 1e9
+        popc_iter = n_r * 2 * Wd
+        alu_ach = popc_iter * it_per_launch / per_launch_s / 1e9
         alu_peak = 16 * sms * mhz * 1e6 / 1e9
+        hbm_eff = dict(roofline, effective=True,
+                       note="fp32-equivalent algorithmic bytes; served from shared memory as bit rows")
         roofline = {"bound": "alu", "pipe": "POPC, 16/clk/SM x %d SMs x %.0f MHz" % (sms, mhz),
                     "achieved": alu_ach, "peak": alu_peak, "unit": "Gpopc/s", "frac": alu_ach / alu_peak,
+                    "frac_whole_chip": alu_ach / (16 * 148 * mhz * 1e6 / 1e9),
                     "traffic": traffic, "kernel": plan.get("kernel"), "ops_per_iter": popc_iter,
-                    "latency_bound": True,
-                    "note": "one SMO iteration is a serial chain (row pass -> CTA barrier -> DSMEM exchange "
-                            "-> pair update); the POPC pipe is the busiest throughput unit of the row pass "
-                            "(ops = algorithmic word popcounts, 2 ceil(d/32) per row; the kernel issues 3 POPC "
-                            "per 4 words)"}
-        hbm_roof["effective"] = True
-        hbm_roof["note"] = ("fp32-equivalent algorithmic bytes per iteration (SURVEY 8(d)); served from "
-                            "shared memory as bit rows, so this exceeds what streaming X from HBM could do")
-    else:
-        roofline = hbm_roof
-        hbm_roof = None
+                    "latency_bound": True}
 
-    # ---- the streamed (HBM-bound) configurations, measured beside the bench workload:
-    # a fixed prefix of the full-size W5 and W4 solves (same kernels, same launch
-    # configuration as their full solves), HBM roofline of the persistent solver launch.
-    streamed = None
-    if world == 1 and not args.no_streamed:
-        streamed = []
-        from gen import workloads as WL
-        for name, k_it in (("W5", 1500), ("W4", 6000)):
-            ws = WL.get(name)
-            Xs, ys = ws.train()
-            Xs_d = torch.from_numpy(Xs).to(dev)
-            ys_d = torch.from_numpy(ys).to(dev)
-            del Xs
-            times = []
-            for rep in range(3):
-                flush.fill_(float(rep))
-                rs = S.svm_train_dev(Xs_d, ys_d, ws.C, ws.kernel, ws.gamma, ws.tol, max_iter=k_it, stream=stream)
-                if rep:
-                    times.append(rs["info"]["seconds_solve"])
-            ps = S.last_plan()
-            its = rs["info"]["iterations"]
-            t_it = statistics.mean(times) / its
-            dps = (ws.d + 3) // 4 * 4
-            b_fp32 = ws.n * (4 * dps + 25)                   # fp32 rows + f r/w + status
-            ent = {"workload": f"{ws.name}: {ws.config}", "iterations": its, "us_per_iter": 1e6 * t_it,
-                   "plan": ps, "bytes_per_iter_fp32": b_fp32}
-            if str(ps.get("mode", "")).startswith("mixed"):
-                # exactly-0/1 columns stored as bits: the bytes the kernel streams per iteration
-                nbin = int(((Xs_d == 0) | (Xs_d == 1)).all(dim=0).sum())
-                slots = -(-((ws.d - nbin) + -(-nbin // 32)) // 4) * 4
-                b_cmp = ws.n * (4 * slots + 25)
-                ent["roofline"] = {"bound": "hbm", "achieved": b_cmp / t_it / 1e9, "peak": hbm, "unit": "GB/s",
-                                   "frac": b_cmp / t_it / 1e9 / hbm, "peak_kind": peak_kind,
-                                   "bytes_per_iter": b_cmp, "encoding": f"{ws.d - nbin} fp32 + {nbin} bit columns"}
-                ent["roofline_hbm_effective"] = {"achieved": b_fp32 / t_it / 1e9, "frac": b_fp32 / t_it / 1e9 / hbm,
-                                                 "effective": True,
-                                                 "note": "fp32-equivalent bytes (SURVEY 8(d)) over the same time"}
-            else:
-                ent["roofline"] = {"bound": "hbm", "achieved": b_fp32 / t_it / 1e9, "peak": hbm, "unit": "GB/s",
-                                   "frac": b_fp32 / t_it / 1e9 / hbm, "peak_kind": peak_kind, "bytes_per_iter": b_fp32}
-            streamed.append(ent)
-            del Xs_d, ys_d
+    # ---- e2e: the same solve through the host C-ABI (host X / y, H2D + D2H timed)
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rr = S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol, iters_per_launch=window)
+        e2e_s = time.perf_counter() - t0
+        e2e = {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(n * d * 4 + n),
+               "d2h_bytes_per_step": int(n * 8),
+               "api": "svm_train_ex (host pointers: X, y in; alpha, b out)",
+               "iterations": rr["info"]["iterations"], "seconds_h2d": rr["info"].get("seconds_h2d")}
+    elif world > 1 and not args.no_e2e:
+        Xh = torch.from_numpy(X[lo:hi]).pin_memory()
+        yh = torch.from_numpy(y[lo:hi]).pin_memory()
+        ah = torch.empty(hi - lo, dtype=torch.float64).pin_memory()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        Xl.copy_(Xh, non_blocking=True); yl.copy_(yh, non_blocking=True)
+        rr = train(iters_per_launch=window)
+        ah.copy_(rr["alpha"], non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e = {"value": gmax(e0.elapsed_time(e1) * 1e-3), "unit": "s",
+               "h2d_bytes_per_step": int((hi - lo) * (d * 4 + 1)), "d2h_bytes_per_step": int((hi - lo) * 8),
+               "api": "svm_train_shard (pinned host -> device copies in the timed region)"}
+
+    # ---- batched prediction (a11) of the held-out rows on the tensor cores (tcgen05 3xTF32):
+    # each rank predicts its share of the test rows against the whole model's SVs
+    predict = None
+    if not args.no_predict:
+        if world > 1:
+            from paper_2311_14908_b200.dist import gather_rows
+            alpha_full = gather_rows(alpha_last.contiguous(), blocks, dev)
+        else:
+            alpha_full = alpha_last
+        Xsv, coef, _ = S.svm_support_vectors_dev(Xd_full, yd_full, alpha_full, stream=stream)
+        Xt, _ = w.test(args.predict_rows if args.predict_rows >= 0 else None)
+        m = Xt.shape[0]
+        mt = -(-m // world)
+        tl, th = min(m, rank * mt), min(m, (rank + 1) * mt)
+        Xt_d = torch.from_numpy(Xt[tl:th]).to(dev).contiguous()
+        del Xt
+        S.svm_predict_dev(Xsv, coef, b_last, w.kernel, w.gamma, Xt_d[:1024], stream=stream, mode=1)   # warm
+        barrier()
+        p0 = torch.cuda.Event(enable_timing=True); p1 = torch.cuda.Event(enable_timing=True)
+        p0.record(stream)
+        S.svm_predict_dev(Xsv, coef, b_last, w.kernel, w.gamma, Xt_d, stream=stream, mode=1)
+        p1.record(stream)
+        barrier()
+        tp_s = gmax(p0.elapsed_time(p1) * 1e-3)
+        nsv = int(coef.shape[0])
+        flops = 2.0 * m * nsv * d
+        tf32_peak = bf16 * 0.5            # nominal TF32 : BF16 dense ratio (1.1 : 2.25 PF), no TF32 measured peak
+        predict = {"rows": m, "n_sv": nsv, "seconds": tp_s, "mode": "tcgen05 kind::tf32 3xTF32 + fp64 epilogue",
+                   "roofline": {"bound": "tensor", "achieved": 3 * flops / tp_s / 1e12, "peak": tf32_peak,
+                                "unit": "TFLOP/s", "frac": 3 * flops / tp_s / 1e12 / tf32_peak,
+                                "algorithmic_tflops": flops / tp_s / 1e12,
+                                "peak_kind": f"{peak_kind} bf16 x 0.5 (nominal TF32/BF16 ratio)",
+                                "note": "achieved counts the 3 TF32 MMA passes issued (hi*hi + hi*lo + lo*hi)"},
+                   "exp_per_s": m * nsv / tp_s}
+        del Xt_d, Xsv, coef
+
+    # ---- time-to-converge of the other configs (one warm + one timed whole solve each)
+    others = None
+    if world == 1 and not args.no_others:
+        others = []
+        for name in ("W2", "W3", "W4"):
+            if name == w.name:
+                continue
+            wo = W.get(name)
+            Xo, yo = wo.train()
+            Xo_d, yo_d = torch.from_numpy(Xo).to(dev), torch.from_numpy(yo).to(dev)
+            S.svm_train_dev(Xo_d, yo_d, wo.C, wo.kernel, wo.gamma, wo.tol, stream=stream)
+            flush.fill_(2.0)
+            torch.cuda.synchronize()
+            a0 = torch.cuda.Event(enable_timing=True); a1 = torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            ro = S.svm_train_dev(Xo_d, yo_d, wo.C, wo.kernel, wo.gamma, wo.tol, stream=stream)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            po = S.last_plan()
+            it_o = ro["info"]["iterations"]
+            ent = {"workload": f"{wo.name}: {wo.config}", "time_to_converge_s": a0.elapsed_time(a1) * 1e-3,
+                   "iterations": it_o, "us_per_iter": 1e6 * ro["info"]["seconds_solve"] / max(1, it_o),
+                   "converged": ro["info"]["converged"], "plan": po,
+                   "cache_hits": ro["info"].get("cache_hits"), "cache_misses": ro["info"].get("cache_misses")}
+            dpo = (wo.d + 3) // 4 * 4
+            b_fp32 = wo.n * (4 * dpo + 25)
+            ent["hbm_fp32_equivalent_gbs"] = b_fp32 * it_o / ro["info"]["seconds_solve"] / 1e9
+            others.append(ent)
+            del Xo_d, yo_d
             torch.cuda.empty_cache()
 
-    # ---- projected-gradient dual trainer on the bench workload: K built
-    # once in HBM, every epoch one pass over it (k_gd_epoch, HBM-bound GEMV + fused update)
+    # ---- projected-gradient dual trainer on W2: K built once in HBM,
+    # every epoch one pass over it (k_gd_epoch, HBM-bound GEMV + fused update)
     gd = None
     if world == 1 and not args.no_gd:
-        # per-epoch time = difference of two runs (10 and 30 epochs): the Gram build, the
-        # final evaluation pass and the bias/objective kernel cancel
+        wg = W.get("W2")
+        Xg, yg = wg.train()
+        Xg_d, yg_d = torch.from_numpy(Xg).to(dev), torch.from_numpy(yg).to(dev)
+        ng = Xg.shape[0]
         ep = 30
-        S.svm_train_gd_dev(Xd_full, yd_full, w.C, w.kernel, w.gamma, 1e-4, 2, stream=stream)      # warm
-        g10 = S.svm_train_gd_dev(Xd_full, yd_full, w.C, w.kernel, w.gamma, 1e-4, 10, stream=stream)["info"]
-        gi = S.svm_train_gd_dev(Xd_full, yd_full, w.C, w.kernel, w.gamma, 1e-4, ep, stream=stream)["info"]
+        S.svm_train_gd_dev(Xg_d, yg_d, wg.C, wg.kernel, wg.gamma, 1e-4, 2, stream=stream)      # warm
+        g10 = S.svm_train_gd_dev(Xg_d, yg_d, wg.C, wg.kernel, wg.gamma, 1e-4, 10, stream=stream)["info"]
+        gi = S.svm_train_gd_dev(Xg_d, yg_d, wg.C, wg.kernel, wg.gamma, 1e-4, ep, stream=stream)["info"]
         per_epoch = (gi["seconds_epochs"] - g10["seconds_epochs"]) / (ep - 10)
-        # algorithmic bytes per epoch: K once (8 n^2) + v, alpha read, alpha, v, g written
-        gbytes = 8 * n * n + 40 * n
-        gd = {"workload": f"{w.name}", "epochs": ep, "lr": 1e-4, "seconds_gram": gi["seconds_gram"],
-              "seconds_epochs_total": gi["seconds_epochs"],
-              "ms_per_epoch": 1e3 * per_epoch, "objective": gi["objective"], "plan": S.last_plan(),
+        gbytes = 8 * ng * ng + 40 * ng
+        gd = {"workload": "W2", "epochs": ep, "lr": 1e-4, "seconds_gram": gi["seconds_gram"],
+              "ms_per_epoch": 1e3 * per_epoch, "objective": gi["objective"],
               "roofline": {"bound": "hbm", "kernel": "k_gd_epoch", "achieved": gbytes / per_epoch / 1e9,
                            "peak": hbm, "unit": "GB/s", "frac": gbytes / per_epoch / 1e9 / hbm,
                            "peak_kind": peak_kind, "bytes_per_epoch": gbytes,
-                           "gram_bytes_padded": gi["gram_bytes"],
                            "note": "a read-only stream of K; the measured peak is a copy (read + write) "
                                    "figure, which a pure read stream can exceed"}}
+        del Xg_d, yg_d
 
     line = None
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             ips, k_it, thr = oracle_sample(w, X, y, args.cpu_budget, iters)
-            cpu = {"value": iters / ips, "unit": "s", "cores": thr, "kind": "oracle",
+            cpu = {"value": iters / ips, "unit": "s", "cores": thr, "kind": "oracle", "cpu_model": cpu_model(),
                    "sample": f"first {k_it} SMO iterations of {w.name} (n={n}) on {thr} host threads "
-                             f"({ips:.1f} iters/s); time-to-converge projected to the {iters} iterations "
+                             f"({ips:.2f} iters/s); time-to-converge projected to the {iters} iterations "
                              f"of the identical trajectory"}
         line = {
-            "metric": METRIC, "value": train_s, "unit": "s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
+            "metric": METRIC, "value": value, "unit": "s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": gmax(t_step) * 1e3,
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{w.name}: {w.config}", "n": n, "d": d, "kernel": "rbf" if w.kernel else "linear",
-                       "gamma": w.gamma, "C": w.C, "tol": w.tol, "predict_rows": m, "n_sv": nsv,
-                       "predict": "tcgen05 3xTF32" if args.predict_mode == 1 else "fp64 exact",
-                       "parallelism": f"rows sharded over {world} GPU(s)", "l2": "flushed between steps (256 MB write)"},
+            "config": {"workload": f"{w.name}: {w.config}", "n": n, "d": d,
+                       "kernel": "rbf" if w.kernel else "linear", "gamma": w.gamma, "C": w.C, "tol": w.tol,
+                       "step": (f"one window of {window} SMO iterations of the solve (iters_per_launch); "
+                                f"value = the K windows = the whole solve" if windowed else "one whole solve"),
+                       "parallelism": f"rows sharded over {world} GPU(s)",
+                       "l2": "X (1 GB) larger than L2; L2 flushed (256 MB write) before the timed region"
+                             if windowed else "flushed between steps (256 MB write)"},
             "iterations": iters,
-            "smo_iters_per_s": iters / train_s,
+            "converged": info["converged"],
+            "launches": info["launches"],
+            "smo_iters_per_s": iters / value,
             "us_per_iter": 1e6 * solve_s / max(iters, 1),
             "solve_s": solve_s,
             "kernel_row_gbs": achieved,
             "roofline": roofline,
-            "roofline_hbm_effective": hbm_roof,
-            "streamed": streamed,
+            "roofline_hbm_effective": hbm_eff,
+            "predict": predict,
+            "others": others,
             "gd": gd,
             "plan": plan,
             "cpu_baseline": cpu,
@@ -462,16 +510,17 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="W2")
+    ap.add_argument("--workload", default="W5")
     ap.add_argument("--predict-rows", type=int, default=-1)
-    ap.add_argument("--predict-mode", type=int, default=1, help="0 exact fp64 SIMT, 1 tcgen05 3xTF32")
-    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--ref-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-streamed", action="store_true", help="skip the W5/W4 streamed-prefix rooflines")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-predict", action="store_true")
+    ap.add_argument("--no-others", action="store_true", help="skip the W2-W4 time-to-converge entries")
     ap.add_argument("--no-gd", action="store_true", help="skip the projected-GD trainer measurement")
     args = ap.parse_args()
     if args.impl == "reference":

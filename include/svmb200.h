@@ -109,9 +109,20 @@ typedef struct {
     double seconds_solve;   /* device time of the solver launches (CUDA events) */
     double seconds_total;   /* host wall time of the call, including H2D / D2H */
     int64_t launches;       /* persistent-kernel launches used */
+    int64_t cache_hits;     /* kernel-row cache (a8): row lookups served from the cache (two per
+                               SMO iteration: x_up's row and x_low's row) */
+    int64_t cache_misses;   /* row lookups that computed the row (and filled a slot) */
+    double seconds_h2d;     /* host entry points: device time of the H2D copy of X and y (0 for
+                               device entry points) */
 } svm_info;
 
-/* Optional debug / test hooks; a NULL svm_debug costs nothing. */
+/* Optional debug / test hooks; a NULL svm_debug costs nothing.  Host entry points
+ * (svm_train_ex) take host pointers for alpha0 / f0 / f_out; device entry points
+ * (svm_train_dev, svm_train_shard) take DEVICE pointers for them, of the rank's rows
+ * ([n_local], the rank's slice) for svm_train_shard.  pair_trace is always a host pointer
+ * (svm_train_shard: filled on rank 0 only).  A warm start resumes a saved state: the
+ * solve continues from (alpha0, f0) exactly as the interrupted solve would have
+ * (segment parity). */
 typedef struct {
     const double* alpha0;     /* warm start [n] (both alpha0 and f0, or neither) */
     const double* f0;         /* warm start [n]: the error vector matching alpha0 */
@@ -130,7 +141,8 @@ int svm_train_ex(const float* X, const int8_t* y, int64_t n, int64_t d, const sv
 
 /* Train on device data already resident in HBM (X row-major [n][d] float32, y int8),
  * on `cuda_stream` (cudaStream_t, NULL = legacy default).  alpha (device, [n]) out,
- * b and info host out; dbg pointers are host pointers. */
+ * b and info host out (n_sv and the dual objective are reduced on the device); dbg:
+ * alpha0 / f0 / f_out device pointers, pair_trace host. */
 int svm_train_dev(const float* X, const int8_t* y, int64_t n, int64_t d, const svm_params* p,
                   double* alpha, double* b, svm_info* info, const svm_debug* dbg,
                   void* cuda_stream);
@@ -171,19 +183,44 @@ int svm_predict_dev_ex(const float* X_sv, const double* coef, int64_t n_sv, int6
                        int kernel, double gamma, const float* X_test, int64_t m, double* dec,
                        int mode, void* cuda_stream);
 
+/* The support set of a trained model, compacted on the device (row a10):
+ * {i : alpha_i > sv_epsilon} (sv_epsilon <= 0 -> 1e-8) in ascending i.  Device pointers:
+ * X [n][d] float32, y int8, alpha [n] fp64 in; X_sv [n_sv][d] float32, coef [n_sv] fp64
+ * (coef_i = alpha_i y_i, exact), sv_index [n_sv] int64 out (sv_index nullable; X_sv
+ * nullable).  With coef == NULL only *n_sv (host) is written, so a caller can size the
+ * outputs first; otherwise the outputs must hold n_sv entries.  Synchronises the stream. */
+int svm_support_vectors_dev(const float* X, const int8_t* y, const double* alpha, int64_t n,
+                            int64_t d, double sv_epsilon, float* X_sv, double* coef,
+                            int64_t* sv_index, int64_t* n_sv, void* cuda_stream);
+
 /* ---- multi-GPU, one process per GPU (torchrun) -----------------------------------
  * svm_comm_unique_id fills 128 bytes on rank 0 that the caller broadcasts (e.g. with
- * torch.distributed); every rank then calls svm_comm_init.  svm_train_shard trains on
- * the rank's contiguous row block [row_offset, row_offset + n_local) of an n_global-row
- * problem; every rank must call it with the same parameters.  Device pointers; alpha_local
- * receives the rank's slice of alpha.  Each iteration exchanges one 48-byte record per CTA
- * with every peer over NVLink (peer stores + a monotonic arrival counter); results are
- * bit-identical for any number of ranks. */
+ * torch.distributed); every rank then calls svm_comm_init (NCCL bootstrap).  Or every rank
+ * calls svm_comm_init_host with a host all-gather callback (any transport, e.g. gloo;
+ * also the only option for several ranks on ONE device, which NCCL refuses).
+ * svm_train_shard trains on the rank's contiguous row block [row_offset, row_offset +
+ * n_local) of an n_global-row problem; every rank must call it with the same parameters.
+ * Device pointers; alpha_local receives the rank's slice of alpha.  Each iteration, every
+ * CTA stores its 64-byte candidate record into every rank's mailbox (peer stores through
+ * CUDA IPC mappings over NVLink); a record is four 16-byte words whose two 8-byte halves
+ * each carry the exchange's sequence number, so a reader accepts only whole words
+ * (8-byte accesses are single-copy atomic).  Results are bit-identical for any number of
+ * ranks.  dbg: alpha0 / f0 / f_out device pointers of the rank's rows, pair_trace host
+ * (rank 0). */
+typedef struct {
+    void* ctx;
+    /* every rank passes `bytes` bytes in send; recv (host, world * bytes) receives every
+     * rank's bytes in rank order.  Returns 0 on success. */
+    int (*allgather)(void* ctx, const void* send, void* recv, int64_t bytes);
+} svm_host_coll;
+
 int svm_comm_unique_id(uint8_t id[128]);
 int svm_comm_init(void** comm, int rank, int world, const uint8_t id[128], int device);
+int svm_comm_init_host(void** comm, int rank, int world, int device, const svm_host_coll* coll);
 int svm_train_shard(void* comm, const float* X_local, const int8_t* y_local, int64_t n_local,
                     int64_t row_offset, int64_t n_global, int64_t d, const svm_params* p,
-                    double* alpha_local, double* b, svm_info* info, void* cuda_stream);
+                    double* alpha_local, double* b, svm_info* info, const svm_debug* dbg,
+                    void* cuda_stream);
 void svm_comm_destroy(void* comm);
 
 /* ---- projected-gradient dual trainer ------------------------

@@ -323,8 +323,7 @@ __global__ void __launch_bounds__(NTB, 1) smo_bincl(const Params P) {
             uint4 wv = sh.wrec[par][from_u ? wu : wl][h];
             if (h == 2) {                                 // y_up from u's warp, y_low from l's
                 const uint4 w2l = sh.wrec[par][wl][2];
-                wv = rec_pack(sq, (wv.y & 0xffffu) | (w2l.y & 0xffff0000u),
-                              (unsigned long long)wv.z | ((unsigned long long)wv.w << 32));
+                wv = rec_pack(sq, (rec_aux(wv) & 0xffffu) | (rec_aux(w2l) & 0xffff0000u), rec_payload(wv));
             }
             const uint32_t src = smem_u32(cmb + ((size_t)par * G + cta) * RW + h);
             for (int j = warp; j < G; j += NTB / 32) {
@@ -357,7 +356,7 @@ __global__ void __launch_bounds__(NTB, 1) smo_bincl(const Params P) {
         }
         const bool tmo = __any_sync(0xffffffffu, to);
         BPHASE(PH_S_POLL);
-        const unsigned pi = (hl < G) ? w.y : 0xffffffffu;
+        const unsigned pi = (hl < G) ? rec_aux(w) : 0xffffffffu;
         const unsigned long long k0w = pi == 0xffffffffu ? ~0ull : fkey(rec_f64(w));
         const unsigned long long kup = lowh ? ~0ull : k0w;
         const unsigned long long klo = lowh ? (pi == 0xffffffffu ? ~0ull : ~k0w) : ~0ull;
@@ -397,14 +396,16 @@ __global__ void __launch_bounds__(NTB, 1) smo_bincl(const Params P) {
                 if (++spins > (1u << 24)) break;
             }
         }
-        yu = (int)(int16_t)(__shfl_sync(0xffffffffu, wa.y, 0) & 0xffffu);
-        au = __hiloint2double((int)__shfl_sync(0xffffffffu, wa.w, 0), (int)__shfl_sync(0xffffffffu, wa.z, 0));
-        yl = (int)(int16_t)(__shfl_sync(0xffffffffu, wa.y, 1) >> 16);
-        al = __hiloint2double((int)__shfl_sync(0xffffffffu, wa.w, 2), (int)__shfl_sync(0xffffffffu, wa.z, 2));
+        const uint32_t wa_aux = rec_aux(wa), wa_lo = rec_lo(wa), wa_hi = rec_hi(wa);
+        yu = (int)(int16_t)(__shfl_sync(0xffffffffu, wa_aux, 0) & 0xffffu);
+        au = __hiloint2double((int)__shfl_sync(0xffffffffu, wa_hi, 0), (int)__shfl_sync(0xffffffffu, wa_lo, 0));
+        yl = (int)(int16_t)(__shfl_sync(0xffffffffu, wa_aux, 1) >> 16);
+        al = __hiloint2double((int)__shfl_sync(0xffffffffu, wa_hi, 2), (int)__shfl_sync(0xffffffffu, wa_lo, 2));
 #pragma unroll
         for (int k = 0; k < BINCL_MAXW; ++k) {
             const int su = 3 + k / 3, sl = 3 + rw + k / 3;
-            const uint32_t cu_ = (k % 3 == 0) ? wa.y : ((k % 3 == 1) ? wa.z : wa.w);
+            // a row word triple travels as (aux, payload lo, payload hi)
+            const uint32_t cu_ = (k % 3 == 0) ? wa_aux : ((k % 3 == 1) ? wa_lo : wa_hi);
             const uint32_t vu = __shfl_sync(0xffffffffu, cu_, su & 31);
             const uint32_t vl = __shfl_sync(0xffffffffu, cu_, sl & 31);
             pu[k] = k < W ? vu : 0u;

@@ -54,14 +54,19 @@ enum { BAR_A = 1, BAR_B = 2, BAR_C = 3, BAR_D = 4 };
 enum { ST_RUNNING = 0, ST_CONVERGED = 1, ST_MAXITER = 2, ST_LIMIT = 3, ST_TIMEOUT = -8 };
 enum { FL_POS = 1, FL_UP = 2, FL_LOW = 4 };
 
-// One CTA's candidate record: four 16-byte words, each {seq:16 | chk:16, payload[3]},
-// written by one vector store and read by one vector load.  A word whose sequence number
-// (low 16 bits of the exchange number; the stale content of a slot is exchange seq - 2)
-// and checksum of its payload both match is taken as written by exchange seq, so a reader
-// needs no fence, counter or flag ordering (the checksum also rejects a word observed
-// half-written, should a 16-byte access ever be split).  Payloads:
-//   w0 = (i_up, f_up lo, f_up hi)    w1 = (i_low, f_low lo, f_low hi)
-//   w2 = (y_up | y_low << 16, a_up lo, a_up hi)    w3 = (0, a_low lo, a_low hi)
+// One CTA's candidate record: four 16-byte words.  A word carries a 32-bit aux field a and
+// a 64-bit payload v in two 8-byte halves, each tagged with the 16-bit sequence number sq
+// of the exchange that wrote it (the low 16 bits of the exchange number; the stale
+// content of a slot is exchange sq - 2):
+//     half 0 = v[31:0] | (a[15:0] << 32) | (sq << 48)
+//     half 1 = v[63:32] | (a[31:16] << 32) | (sq << 48)
+// Words are written and read as two 64-bit elements (st/ld .v2.u64, relaxed): each
+// naturally aligned 64-bit element is single-copy atomic, so a reader that sees sq in
+// both halves has read one whole word of exchange sq -- however the 16-byte access is
+// split on its way (NVLink, L2) -- and needs no fence, counter or flag ordering.
+// Payloads:
+//   w0 = (a: i_up, v: f_up)    w1 = (i_low, f_low)
+//   w2 = (y_up | y_low << 16, a_up)    w3 = (0, a_low)
 // (i = global row, 0xffffffff = empty set).  The mailbox stores the words transposed,
 // word[parity][h][g], so one warp load of word h covers 32 consecutive records; the
 // selection polls w0/w1 only and fetches w2/w3 of the two winning records afterwards.
@@ -85,6 +90,7 @@ struct Ctl {                       // per rank solver control, persists across l
     int pad;
     double b_up, b_low;
     long long i_up, i_low;
+    long long cache_hits, cache_misses;   // row-cache lookups (a8), accumulated over launches
 };
 
 struct Params {
@@ -233,15 +239,18 @@ __device__ __forceinline__ uint32_t cluster_map(const void* p, int cta) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(cta));
     return r;
 }
+// record words (see Mailbox) move as two 64-bit elements: {x, y} and {z, w}
 __device__ __forceinline__ void st_cluster_v4(uint32_t addr, uint4 v) {
-    asm volatile("st.shared::cluster.v4.u32 [%0], {%1, %2, %3, %4};"
-                 :: "r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+    const unsigned long long h0 = (unsigned long long)v.x | ((unsigned long long)v.y << 32);
+    const unsigned long long h1 = (unsigned long long)v.z | ((unsigned long long)v.w << 32);
+    asm volatile("st.relaxed.cluster.shared::cluster.v2.u64 [%0], {%1, %2};"
+                 :: "r"(addr), "l"(h0), "l"(h1) : "memory");
 }
 __device__ __forceinline__ uint4 ld_volatile_shared_v4(const uint4* p) {
-    uint4 v;
-    asm volatile("ld.volatile.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(smem_u32(p)) : "memory");
-    return v;
+    unsigned long long h0, h1;
+    asm volatile("ld.relaxed.cluster.shared::cta.v2.u64 {%0, %1}, [%2];"
+                 : "=l"(h0), "=l"(h1) : "r"(smem_u32(p)) : "memory");
+    return make_uint4((uint32_t)h0, (uint32_t)(h0 >> 32), (uint32_t)h1, (uint32_t)(h1 >> 32));
 }
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -276,7 +285,7 @@ struct Shared {
     int red_i[2][16];
     int c_hit, c_su, c_sl;         // row cache: both rows cached / their slots
     int c_fill_u, c_fill_l;        // row cache: the slot this iteration fills (miss), else -1
-    int c_fifo;                    // next FIFO victim slot
+    int lru_head, lru_tail;        // row cache: most / least recently used slot
     int kul_cnt;                   // compacted terms of K(x_u, x_l) (cache mode)
     int timeout;
     unsigned long long bars[2 * MAX_STAGES];
@@ -324,14 +333,8 @@ struct Cand {
     double fu, fl, au, al;
     int iu, il, yu, yl;
 };
-__device__ __forceinline__ uint32_t rec_chk(uint32_t a, uint32_t b, uint32_t c) {
-    // high half of a multiplicative hash: any change of one payload word changes it with
-    // probability ~1 - 2^-16
-    return (a * 0x9E3779B1u + b * 0x85EBCA77u + c * 0xC2B2AE3Du) >> 16;
-}
 __device__ __forceinline__ uint4 rec_pack(uint32_t sq, uint32_t a, unsigned long long v) {
-    const uint32_t lo = (uint32_t)v, hi = (uint32_t)(v >> 32);
-    return make_uint4((sq << 16) | rec_chk(a, lo, hi), a, lo, hi);
+    return make_uint4((uint32_t)v, (sq << 16) | (a & 0xffffu), (uint32_t)(v >> 32), (sq << 16) | (a >> 16));
 }
 // word h (0..3) of the record of candidate c for exchange sq
 __device__ __forceinline__ uint4 rec_word(const Cand& c, int h, uint32_t sq) {
@@ -340,28 +343,38 @@ __device__ __forceinline__ uint4 rec_word(const Cand& c, int h, uint32_t sq) {
     if (h == 2) return rec_pack(sq, (uint32_t)((c.yu & 0xffff) | (c.yl << 16)), (unsigned long long)__double_as_longlong(c.au));
     return rec_pack(sq, 0u, (unsigned long long)__double_as_longlong(c.al));
 }
+// both 8-byte halves were written by exchange sq
 __device__ __forceinline__ bool rec_ok(const uint4& v, uint32_t sq) {
-    return v.x == ((sq << 16) | rec_chk(v.y, v.z, v.w));
+    return (((v.y ^ (sq << 16)) | (v.w ^ (sq << 16))) >> 16) == 0u;
+}
+__device__ __forceinline__ uint32_t rec_aux(const uint4& v) { return (v.y & 0xffffu) | (v.w << 16); }
+__device__ __forceinline__ uint32_t rec_lo(const uint4& v) { return v.x; }
+__device__ __forceinline__ uint32_t rec_hi(const uint4& v) { return v.z; }
+__device__ __forceinline__ unsigned long long rec_payload(const uint4& v) {
+    return (unsigned long long)v.x | ((unsigned long long)v.z << 32);
 }
 __device__ __forceinline__ double rec_f64(const uint4& v) {
-    return __longlong_as_double((long long)(((unsigned long long)v.w << 32) | v.z));
+    return __longlong_as_double((long long)rec_payload(v));
 }
 __device__ __forceinline__ int rec_idx(const uint4& v) {
-    return v.y == 0xffffffffu ? INT_MAX : (int)v.y;
+    const uint32_t a = rec_aux(v);
+    return a == 0xffffffffu ? INT_MAX : (int)a;
 }
 __device__ __forceinline__ void rec_store(uint4* p, uint4 v, int sys) {
+    const unsigned long long h0 = (unsigned long long)v.x | ((unsigned long long)v.y << 32);
+    const unsigned long long h1 = (unsigned long long)v.z | ((unsigned long long)v.w << 32);
     if (sys)
-        asm volatile("st.relaxed.sys.global.v4.u32 [%0], {%1, %2, %3, %4};" :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+        asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1, %2};" :: "l"(p), "l"(h0), "l"(h1) : "memory");
     else
-        asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %4};" :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+        asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" :: "l"(p), "l"(h0), "l"(h1) : "memory");
 }
 __device__ __forceinline__ uint4 rec_load(const uint4* p, int sys) {
-    uint4 v;
+    unsigned long long h0, h1;
     if (sys)
-        asm volatile("ld.relaxed.sys.global.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+        asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(h0), "=l"(h1) : "l"(p) : "memory");
     else
-        asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
-    return v;
+        asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(h0), "=l"(h1) : "l"(p) : "memory");
+    return make_uint4((uint32_t)h0, (uint32_t)(h0 >> 32), (uint32_t)h1, (uint32_t)(h1 >> 32));
 }
 
 #define SVM_PHASE(on, ph)                                                    \
@@ -595,8 +608,11 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
     if (m_isbin) off += (size_t)(32 * P.bin_words + 1) * 8;
     off = (off + 7) & ~size_t(7);
     // row-cache directory: owner (global row) of every slot + an open-addressing hash
-    // row -> slot (cache_hash entries, a power of two >= 2 slots), FIFO replacement
+    // row -> slot (cache_hash entries, a power of two >= 2 slots), LRU replacement through a
+    // doubly linked recency list of the slots (lru_prev / lru_next)
     int* dir_owner = reinterpret_cast<int*>(smem_raw + off); off += (size_t)m_cache * 4;
+    int* lru_prev = reinterpret_cast<int*>(smem_raw + off); off += (size_t)m_cache * 4;
+    int* lru_next = reinterpret_cast<int*>(smem_raw + off); off += (size_t)m_cache * 4;
     off = (off + 7) & ~size_t(7);
     int2* dir_hash = reinterpret_cast<int2*>(smem_raw + off); off += (size_t)P.cache_hash * 8;
     // cache mode: the scalar warp compacts the k with a non-zero term of K(x_u, x_l) here
@@ -634,12 +650,16 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     for (int e = t; e < svmexp::EXP_TABLE_DOUBLES; e += NTHREADS_) sh.exp_tab[e] = svmexp::table_entry(e);
-    for (int e = t; e < m_cache; e += NTHREADS_) dir_owner[e] = -1;
+    for (int e = t; e < m_cache; e += NTHREADS_) {
+        dir_owner[e] = -1;
+        lru_prev[e] = e - 1;
+        lru_next[e] = e + 1 < m_cache ? e + 1 : -1;
+    }
     if (m_dict) for (int e = t; e < 256; e += NTHREADS_) dict_s[e] = e < P.dict_n ? P.dict[e] : 0.0;
     for (int e = t; e < P.cache_hash; e += NTHREADS_) dir_hash[e] = make_int2(-1, -1);
     if (m_cluster)
         for (int e = t; e < 2 * P.ctas_per_rank * P.crw; e += NTHREADS_) cmb[e] = make_uint4(0u, 0u, 0u, 0u);
-    if (t == 0) sh.c_fifo = 0;
+    if (t == 0) { sh.lru_head = 0; sh.lru_tail = m_cache - 1; }
     for (int j = t; j < R; j += NTHREADS_) {
         f_s[j] = P.f[rank][r0 + j];
         if (A_SMEM) a_s[j] = alpha_g[j];
@@ -726,6 +746,7 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
     long long seq = ctl->seq;
     const long long it_start = it;
     unsigned int cslot = 0, cpar = 0, consumed = 0;
+    long long c_hits = 0, c_misses = 0;     // row-cache lookups (scalar lane 0)
     const double INF = __longlong_as_double(0x7ff0000000000000ll);
 
     if (m_resident && !m_gram && n_tiles > 0 && !is_scalar) mbar_wait(&full[0], 0);
@@ -968,7 +989,7 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
                 break;
             }
             // ---- row cache (a8): every CTA runs the same directory operations on the same
-            // pair sequence (hash lookup, FIFO replacement), so every CTA agrees
+            // pair sequence (hash lookup, LRU replacement), so every CTA agrees
             int c_hit = 0, su = -1, sl = -1;
             double kul_pre = 0.0;                   // lane 0: K_ul read early from the row cache
             if (m_cache > 0) {
@@ -1002,18 +1023,32 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
                         }
                         dir_hash[h] = make_int2(-1, -1);
                     };
+                    // LRU: the recency list runs from lru_head (most recent) to lru_tail;
+                    // a lookup moves its slot to the head, the victim is the tail (or the
+                    // slot before it when the tail holds the other row of the pair)
+                    auto touch = [&](int sl_) {
+                        if (sh.lru_head == sl_) return;
+                        const int pv = lru_prev[sl_], nx = lru_next[sl_];
+                        lru_next[pv] = nx;                          // pv >= 0: sl_ is not the head
+                        if (nx >= 0) lru_prev[nx] = pv; else sh.lru_tail = pv;
+                        lru_prev[sl_] = -1; lru_next[sl_] = sh.lru_head;
+                        lru_prev[sh.lru_head] = sl_; sh.lru_head = sl_;
+                    };
                     auto victim = [&](int avoid) {
-                        int v = sh.c_fifo;
-                        if (v == avoid) v = (v + 1) % m_cache;
-                        sh.c_fifo = (v + 1) % m_cache;
+                        int v = sh.lru_tail;
+                        if (v == avoid) v = lru_prev[v];
                         if (dir_owner[v] >= 0) erase(dir_owner[v]);
                         return v;
                     };
                     su = find(iu); sl = find(il);
                     c_hit = (su >= 0 && sl >= 0) ? 1 : 0;
+                    c_hits += (su >= 0) + (sl >= 0);
+                    c_misses += (su < 0) + (sl < 0);
                     int fu_ = -1, fl_ = -1;
                     if (su < 0) { fu_ = victim(sl); dir_owner[fu_] = iu; insert(iu, fu_); }
+                    touch(su >= 0 ? su : fu_);
                     if (sl < 0) { fl_ = victim(su >= 0 ? su : fu_); dir_owner[fl_] = il; insert(il, fl_); }
+                    touch(sl >= 0 ? sl : fl_);
                     sh.c_hit = c_hit; sh.c_su = su; sh.c_sl = sl; sh.c_fill_u = fu_; sh.c_fill_l = fl_;
                     // both rows cached: start the load of K_ul (column l of u's row) now, so its
                     // latency overlaps the winners' words and barrier A
@@ -1064,10 +1099,12 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
                     const int k = k0 + lane;
                     const int kk = k < nu ? k : 0;
                     const int src_u = 3 + kk / 3, src_l = 3 + rwc + kk / 3, m = kk % 3;
-                    const uint32_t vu_y = __shfl_sync(0xffffffffu, wa.y, src_u), vu_z = __shfl_sync(0xffffffffu, wa.z, src_u),
-                                   vu_w = __shfl_sync(0xffffffffu, wa.w, src_u);
-                    const uint32_t vl_y = __shfl_sync(0xffffffffu, wa.y, src_l), vl_z = __shfl_sync(0xffffffffu, wa.z, src_l),
-                                   vl_w = __shfl_sync(0xffffffffu, wa.w, src_l);
+                    // a row word triple travels as (aux, payload lo, payload hi)
+                    const uint32_t e0 = rec_aux(wa), e1 = rec_lo(wa), e2 = rec_hi(wa);
+                    const uint32_t vu_y = __shfl_sync(0xffffffffu, e0, src_u), vu_z = __shfl_sync(0xffffffffu, e1, src_u),
+                                   vu_w = __shfl_sync(0xffffffffu, e2, src_u);
+                    const uint32_t vl_y = __shfl_sync(0xffffffffu, e0, src_l), vl_z = __shfl_sync(0xffffffffu, e1, src_l),
+                                   vl_w = __shfl_sync(0xffffffffu, e2, src_l);
                     const uint32_t xu = m == 0 ? vu_y : (m == 1 ? vu_z : vu_w);
                     const uint32_t xl = m == 0 ? vl_y : (m == 1 ? vl_z : vl_w);
                     if (m_isbin) {
@@ -1127,10 +1164,11 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
                     if (++spins > (1u << 24)) { sh.timeout = 1; break; }
                 }
             }
-            const int yu = (int)(int16_t)(__shfl_sync(0xffffffffu, wa.y, 0) & 0xffffu);
-            const double au = __hiloint2double((int)__shfl_sync(0xffffffffu, wa.w, 0), (int)__shfl_sync(0xffffffffu, wa.z, 0));
-            const int yl = (int)(int16_t)(__shfl_sync(0xffffffffu, wa.y, 1) >> 16);
-            const double al = __hiloint2double((int)__shfl_sync(0xffffffffu, wa.w, 2), (int)__shfl_sync(0xffffffffu, wa.z, 2));
+            const uint32_t wa_aux = rec_aux(wa);
+            const int yu = (int)(int16_t)(__shfl_sync(0xffffffffu, wa_aux, 0) & 0xffffu);
+            const double au = __hiloint2double((int)__shfl_sync(0xffffffffu, rec_hi(wa), 0), (int)__shfl_sync(0xffffffffu, rec_lo(wa), 0));
+            const int yl = (int)(int16_t)(__shfl_sync(0xffffffffu, wa_aux, 1) >> 16);
+            const double al = __hiloint2double((int)__shfl_sync(0xffffffffu, rec_hi(wa), 2), (int)__shfl_sync(0xffffffffu, rec_lo(wa), 2));
             SVM_PHASE(timing, PH_S_PIVOT);
             const int u = iu, l = il;
             if (m_cache > 0 && !c_hit) {
@@ -1561,6 +1599,8 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
         ctl->b_low = sh.f_low;
         ctl->i_up = sh.u == INT_MAX ? -1 : sh.u;
         ctl->i_low = sh.l == INT_MAX ? -1 : sh.l;
+        ctl->cache_hits += c_hits;
+        ctl->cache_misses += c_misses;
     }
     __syncwarp();
     if (m_cluster) cluster_sync_all();

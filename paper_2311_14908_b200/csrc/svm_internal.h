@@ -31,6 +31,7 @@ struct SolveOut {
     double b_up = 0, b_low = 0;
     double seconds_solve = 0;
     long long launches = 0;
+    long long cache_hits = 0, cache_misses = 0;
     bool gram = false;
 };
 
@@ -51,8 +52,9 @@ struct SolveArgs {
     double* alpha_out[svmk::MAXR] = {};        // device alpha of rank r's rows
     svmk::Mailbox* mbox[svmk::MAXR] = {};      // all ranks (peer pointers) unless local alloc
     bool mbox_local_alloc = true;
-    const double* alpha0 = nullptr;            // device, global indexing (warm start)
-    const double* f0 = nullptr;
+    const double* alpha0 = nullptr;            // device warm start: global indexing if warm_global,
+    const double* f0 = nullptr;                //   else the served rank's rows
+    bool warm_global = true;
     double* f_out = nullptr;                   // destination of f (global indexing if f_out_global)
     cudaMemcpyKind f_out_kind = cudaMemcpyDeviceToHost;
     bool f_out_global = true;
@@ -83,6 +85,10 @@ int solve(SolveArgs& a);
 // gram.cu: K[i][j] for all i, j < n (fp64, row-major), same arithmetic as the row pass
 int gram_device(const float* X, long long n, long long d, int kernel, double gamma, double* K,
                 cudaStream_t st, long long ld = 0, int blk = 0);
+
+// finalize.cu: out_host = {sum alpha_i (1 - y_i f_i), n_sv} over n rows (device pointers)
+int info_device(const double* alpha, const double* f, const int8_t* y, long long n, double eps,
+                cudaStream_t st, double out_host[2]);
 
 // predict.cu
 int predict_device(const float* X_sv, const double* coef, long long n_sv, long long d, double b,

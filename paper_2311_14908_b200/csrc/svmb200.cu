@@ -434,7 +434,7 @@ int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl, bool bina
     fixed += 2 * (size_t)pl.dp * 8 + mix_bytes + (size_t)pl.state_cap * (pl.alpha_smem ? 17 : 9);  // pivots + state
     int hash = 0;
     if (cache_slots > 0) { hash = 1; while (hash < 2 * cache_slots) hash <<= 1; }
-    fixed = ((fixed + 7) & ~size_t(7)) + (size_t)cache_slots * 4;                       // cache directory
+    fixed = ((fixed + 7) & ~size_t(7)) + (size_t)cache_slots * 12;                      // cache directory + LRU list
     fixed = ((fixed + 7) & ~size_t(7)) + (size_t)hash * 8 + (cache_slots > 0 ? (size_t)pl.dp * 16 + 8 : 0);
     pl.cache_hash = hash;
     fixed += cl_bytes;
@@ -859,8 +859,9 @@ int solve(SolveArgs& a) {
             counted(2);   // build + init_state below
             k_build_xblk<<<bg, 256, 0, st>>>(a.x_rank[r], nr, (int)a.d, pl.d_pad, pl.G, pl.rt, pl.cta_stride, xb);
         }
-        k_init_state<<<256, 256, 0, st>>>(a.y_rank[r], nr, p.C, a.alpha0 ? a.alpha0 + a.row_off[r] : nullptr,
-                                          a.f0 ? a.f0 + a.row_off[r] : nullptr, f, al, fl);
+        const long long woff = a.warm_global ? a.row_off[r] : 0;
+        k_init_state<<<256, 256, 0, st>>>(a.y_rank[r], nr, p.C, a.alpha0 ? a.alpha0 + woff : nullptr,
+                                          a.f0 ? a.f0 + woff : nullptr, f, al, fl);
         CKR(cudaGetLastError());
         P.xblk[r] = xb; P.f[r] = f; P.alpha[r] = al; P.flags[r] = fl; P.ctl[r] = ctl;
         if (a.mbox_local_alloc) {
@@ -943,6 +944,7 @@ int solve(SolveArgs& a) {
         SolveOut& o = a.out_rank[r];
         o.seconds_solve = ms * 1e-3; o.launches = launches; o.iterations = hcr[r].it;
         o.state = hcr[r].state; o.b_up = hcr[r].b_up; o.b_low = hcr[r].b_low;
+        o.cache_hits = hcr[r].cache_hits; o.cache_misses = hcr[r].cache_misses;
     }
     a.out.seconds_solve = ms * 1e-3;
     a.out.launches = launches;
@@ -950,6 +952,8 @@ int solve(SolveArgs& a) {
     a.out.state = hc.state;
     a.out.b_up = hc.b_up;
     a.out.b_low = hc.b_low;
+    a.out.cache_hits = hc.cache_hits;
+    a.out.cache_misses = hc.cache_misses;
     if (a.f_out) {
         for (int r = a.rank_base; r < a.rank_base + a.nranks_here; ++r)
             CKR(cudaMemcpyAsync(a.f_out + (a.f_out_global ? a.row_off[r] : 0), P.f[r],
@@ -1035,9 +1039,12 @@ double now_s() {
     return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
-void fill_info(svm_info* info, const SolveOut& o, const svm_params& p, const double* alpha,
-               const double* f, const int8_t* y, long long n, double t_total) {
-    if (!info) return;
+// info (a10): iterations, state, b_up / b_low from the solve; n_sv and the dual objective
+// W = 1/2 sum alpha_i (1 - y_i f_i) reduced on the device (finalize.cu) from device alpha, f, y
+int fill_info(svm_info* info, const SolveOut& o, const svm_params& p, const double* alpha_dev,
+              const double* f_dev, const int8_t* y_dev, long long n, cudaStream_t st, double t0,
+              double h2d_s = 0.0) {
+    if (!info) return SVM_OK;
     memset(info, 0, sizeof(*info));
     info->iterations = o.iterations;
     info->converged = (o.state == ST_CONVERGED);
@@ -1045,18 +1052,17 @@ void fill_info(svm_info* info, const SolveOut& o, const svm_params& p, const dou
     info->b_low = o.b_low;
     info->gap = o.b_low - o.b_up;
     info->seconds_solve = o.seconds_solve;
-    info->seconds_total = t_total;
     info->launches = o.launches;
-    if (alpha) {
-        int nsv = 0;
-        double w = 0.0;
-        for (long long j = 0; j < n; ++j) {
-            nsv += alpha[j] > p.sv_epsilon;
-            if (f && y) w += alpha[j] * (1.0 - (double)y[j] * f[j]);
-        }
-        info->n_sv = nsv;
-        info->dual_objective = 0.5 * w;               // W = 1/2 sum a_i (1 - y_i f_i)
-    }
+    info->cache_hits = o.cache_hits;
+    info->cache_misses = o.cache_misses;
+    info->seconds_h2d = h2d_s;
+    double s[2];
+    int rc = info_device(alpha_dev, f_dev, y_dev, n, p.sv_epsilon, st, s);
+    if (rc) return rc;
+    info->n_sv = (int)s[1];
+    info->dual_objective = 0.5 * s[0];
+    info->seconds_total = now_s() - t0;
+    return SVM_OK;
 }
 
 }  // namespace
@@ -1074,20 +1080,29 @@ extern "C" int svm_train_ex(const float* X, const int8_t* y, int64_t n, int64_t 
     cudaStream_t st;
     CKR(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     float* dX = nullptr; int8_t* dy = nullptr; double* dA = nullptr; double* dA0 = nullptr; double* dF0 = nullptr;
-    std::vector<double> fbuf;
+    double* dF = nullptr;
+    cudaEvent_t h0 = nullptr, h1 = nullptr;
+    float h2d_ms = 0.f;
     SolveOut o;
     do {
         if (cudaMallocAsync(&dX, (size_t)n * d * 4, st) != cudaSuccess ||
             cudaMallocAsync(&dy, (size_t)n, st) != cudaSuccess ||
-            cudaMallocAsync(&dA, (size_t)n * 8, st) != cudaSuccess) {
+            cudaMallocAsync(&dA, (size_t)n * 8, st) != cudaSuccess ||
+            cudaMallocAsync(&dF, (size_t)n * 8, st) != cudaSuccess) {
             rc = fail(SVM_ENOMEM, "device allocation of the training set failed");
             break;
         }
+        if (cudaEventCreate(&h0) != cudaSuccess || cudaEventCreate(&h1) != cudaSuccess) {
+            rc = fail(SVM_ECUDA, "event creation failed");
+            break;
+        }
+        cudaEventRecord(h0, st);
         if (cudaMemcpyAsync(dX, X, (size_t)n * d * 4, cudaMemcpyHostToDevice, st) != cudaSuccess ||
             cudaMemcpyAsync(dy, y, (size_t)n, cudaMemcpyHostToDevice, st) != cudaSuccess) {
             rc = fail(SVM_ECUDA, "H2D copy failed");
             break;
         }
+        cudaEventRecord(h1, st);
         if (dbg && dbg->alpha0) {
             if (cudaMallocAsync(&dA0, (size_t)n * 8, st) != cudaSuccess ||
                 cudaMallocAsync(&dF0, (size_t)n * 8, st) != cudaSuccess) {
@@ -1098,11 +1113,13 @@ extern "C" int svm_train_ex(const float* X, const int8_t* y, int64_t n, int64_t 
             cudaMemcpyAsync(dF0, dbg->f0, (size_t)n * 8, cudaMemcpyHostToDevice, st);
         }
         if ((rc = validate_device(dX, dy, n, d, st, nullptr))) break;
-        fbuf.resize((size_t)n);
-        rc = train_device(dX, dy, n, d, p, dA, dA0, dF0, fbuf.data(), cudaMemcpyDeviceToHost,
+        cudaEventElapsedTime(&h2d_ms, h0, h1);
+        rc = train_device(dX, dy, n, d, p, dA, dA0, dF0, dF, cudaMemcpyDeviceToDevice,
                           dbg ? (long long*)dbg->pair_trace : nullptr, dbg ? dbg->pair_trace_cap : 0, st, o);
         if (rc) break;
-        if (cudaMemcpyAsync(alpha, dA, (size_t)n * 8, cudaMemcpyDeviceToHost, st) != cudaSuccess) {
+        if ((rc = fill_info(info, o, p, dA, dF, dy, n, st, t0, h2d_ms * 1e-3))) break;
+        if (cudaMemcpyAsync(alpha, dA, (size_t)n * 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            (dbg && dbg->f_out && cudaMemcpyAsync(dbg->f_out, dF, (size_t)n * 8, cudaMemcpyDeviceToHost, st) != cudaSuccess)) {
             rc = fail(SVM_ECUDA, "D2H copy failed");
             break;
         }
@@ -1110,15 +1127,17 @@ extern "C" int svm_train_ex(const float* X, const int8_t* y, int64_t n, int64_t 
     if (dX) cudaFreeAsync(dX, st);
     if (dy) cudaFreeAsync(dy, st);
     if (dA) cudaFreeAsync(dA, st);
+    if (dF) cudaFreeAsync(dF, st);
     if (dA0) cudaFreeAsync(dA0, st);
     if (dF0) cudaFreeAsync(dF0, st);
     cudaError_t se = cudaStreamSynchronize(st);
+    if (h0) cudaEventDestroy(h0);
+    if (h1) cudaEventDestroy(h1);
     cudaStreamDestroy(st);
     if (rc) return rc;
     if (se != cudaSuccess) return fail(SVM_ECUDA, cudaGetErrorString(se));
     *b = -(o.b_up + o.b_low) / 2.0;
-    if (dbg && dbg->f_out) memcpy(dbg->f_out, fbuf.data(), (size_t)n * 8);
-    fill_info(info, o, p, alpha, fbuf.data(), y, n, now_s() - t0);
+    if (info) info->seconds_total = now_s() - t0;
     return SVM_OK;
 }
 
@@ -1138,27 +1157,24 @@ extern "C" int svm_train_dev(const float* X, const int8_t* y, int64_t n, int64_t
     svm_params p;
     int rc = check_params(n, d, p_in, &p);
     if (rc) return rc;
-    if (dbg && (dbg->alpha0 || dbg->f0)) return fail(SVM_EINVAL, "warm start is a host-API hook");
+    if (dbg && ((dbg->alpha0 == nullptr) != (dbg->f0 == nullptr)))
+        return fail(SVM_EINVAL, "warm start needs both alpha0 and f0");
     cudaStream_t st = (cudaStream_t)cuda_stream;
     if ((rc = validate_device(X, y, n, d, st, nullptr))) return rc;
     SolveOut o;
-    double* f_dev = nullptr;
-    CKR(cudaMallocAsync(&f_dev, (size_t)n * 8, st));
-    rc = train_device(X, y, n, d, p, alpha, nullptr, nullptr, f_dev, cudaMemcpyDeviceToDevice,
-                      dbg ? (long long*)dbg->pair_trace : nullptr, dbg ? dbg->pair_trace_cap : 0, st, o);
-    if (rc) { cudaFreeAsync(f_dev, st); return rc; }
-    *b = -(o.b_up + o.b_low) / 2.0;
-    if (info || (dbg && dbg->f_out)) {
-        std::vector<double> ha((size_t)n), hf((size_t)n);
-        std::vector<int8_t> hy((size_t)n);
-        CKR(cudaMemcpyAsync(ha.data(), alpha, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
-        CKR(cudaMemcpyAsync(hf.data(), f_dev, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
-        CKR(cudaMemcpyAsync(hy.data(), y, (size_t)n, cudaMemcpyDeviceToHost, st));
-        CKR(cudaStreamSynchronize(st));
-        if (dbg && dbg->f_out) memcpy(dbg->f_out, hf.data(), (size_t)n * 8);
-        fill_info(info, o, p, ha.data(), hf.data(), hy.data(), n, now_s() - t0);
+    double* f_dev = (dbg && dbg->f_out) ? dbg->f_out : nullptr;
+    double* f_tmp = nullptr;
+    if (!f_dev) {
+        CKR(cudaMallocAsync(&f_tmp, (size_t)n * 8, st));
+        f_dev = f_tmp;
     }
-    CKR(cudaFreeAsync(f_dev, st));
+    rc = train_device(X, y, n, d, p, alpha, dbg ? dbg->alpha0 : nullptr, dbg ? dbg->f0 : nullptr, f_dev,
+                      cudaMemcpyDeviceToDevice, dbg ? (long long*)dbg->pair_trace : nullptr,
+                      dbg ? dbg->pair_trace_cap : 0, st, o);
+    if (!rc) rc = fill_info(info, o, p, alpha, f_dev, y, n, st, t0);
+    if (f_tmp) cudaFreeAsync(f_tmp, st);
+    if (rc) return rc;
+    *b = -(o.b_up + o.b_low) / 2.0;                   // S:L215
     return SVM_OK;
 }
 
@@ -1191,6 +1207,9 @@ extern "C" int svm_train_batch_dev(int B, const float* const* X, const int8_t* c
         int ctas = p.ctas > 0 ? p.ctas : n_sm;
         if (ctas > n_sm) ctas = n_sm;
         a.ctas_per_rank = ctas / nb;
+        if (a.ctas_per_rank < 1)
+            return fail(SVM_EINVAL, "fewer CTAs (" + std::to_string(ctas) + ") than problems in a launch (" +
+                                        std::to_string(nb) + ")");
         a.n_sm = n_sm; a.max_smem = max_smem;
         a.independent = true;
         for (int k = 0; k < nb; ++k) {
@@ -1212,6 +1231,7 @@ extern "C" int svm_train_batch_dev(int B, const float* const* X, const int8_t* c
                 in.iterations = o.iterations; in.converged = o.state == ST_CONVERGED;
                 in.b_up = o.b_up; in.b_low = o.b_low; in.gap = o.b_low - o.b_up;
                 in.seconds_solve = o.seconds_solve; in.launches = o.launches;
+                in.cache_hits = o.cache_hits; in.cache_misses = o.cache_misses;
                 in.seconds_total = now_s() - t0;
             }
         }

@@ -32,8 +32,8 @@ def declared_functions():
 def test_header_declares_the_boundary():
     names = declared_functions()
     for n in ("svm_train", "svm_train_ex", "svm_train_dev", "svm_predict", "svm_predict_dev",
-              "svm_comm_unique_id", "svm_comm_init", "svm_train_shard", "svm_comm_destroy",
-              "svm_last_error", "svm_version"):
+              "svm_comm_unique_id", "svm_comm_init", "svm_comm_init_host", "svm_train_shard",
+              "svm_comm_destroy", "svm_support_vectors_dev", "svm_last_error", "svm_version"):
         assert n in names
 
 
@@ -54,7 +54,9 @@ def test_library_is_sm100a(S):
 def test_struct_layouts_match_header(S):
     # svm_params: 3 doubles, int64, int32, int32, double, int32, int32, int64, 4 x int32 = 80 bytes
     assert ctypes.sizeof(S.Params) == 80
-    assert ctypes.sizeof(S.Info) == 72
+    # svm_info: int64, 2 x int32, 4 doubles, 2 doubles, int64, 2 x int64, double = 96 bytes
+    assert ctypes.sizeof(S.Info) == 96
+    assert ctypes.sizeof(S.Debug) == 40
     assert S.version().startswith("svmb200")
 
 
@@ -131,3 +133,36 @@ def test_cuda_path_exp_matches_oracle_exp_bulk(exp_host):
     exp_host.svm_exp_host_batch(xs.ctypes.data, out.ctypes.data, xs.size)
     ref = np.array([O.exp_cr(x) for x in xs[:200000]])
     np.testing.assert_array_equal(out[:200000], ref)
+
+
+def test_binding_validates_before_the_library(S):
+    """Host-side argument checks of the binding: a warm start needs both
+    alpha0 and f0 of shape (n,); a support-vector / test dimension mismatch raises
+     instead of being reshaped."""
+    X = np.zeros((4, 2), np.float32)
+    y = np.array([1, -1, 1, -1], np.int8)
+    with pytest.raises(ValueError, match="both"):
+        S.svm_train_ex(X, y, 1.0, S.LINEAR, alpha0=np.zeros(4))
+    with pytest.raises(ValueError, match="shape"):
+        S.svm_train_ex(X, y, 1.0, S.LINEAR, alpha0=np.zeros(3), f0=np.zeros(3))
+    with pytest.raises(ValueError, match="X_sv"):
+        S.svm_predict(np.zeros((3, 3), np.float32), np.ones(3), 0.0, S.LINEAR, 0.0, X)
+    with pytest.raises(ValueError, match="coef"):
+        S.svm_predict(np.zeros((3, 2), np.float32), np.ones(2), 0.0, S.LINEAR, 0.0, X)
+
+
+def test_gamma_defaults_to_one_over_d(S):
+    """the RBF width defaults to 1/d in the Python layer (the C ABI has none)."""
+    from paper_2311_14908_b200 import _gamma
+    assert _gamma(None, S.RBF, 256) == 1.0 / 256
+    assert _gamma(None, S.LINEAR, 256) == 0.0
+    assert _gamma(0.5, S.RBF, 256) == 0.5
+
+
+def test_support_vector_call_validates(S):
+    n = ctypes.c_int64()
+    assert S.lib().svm_support_vectors_dev(None, None, None, 4, 2, 0.0, None, None, None, ctypes.byref(n), None) == -1
+    a = np.zeros(4)
+    # coef requested without y
+    assert S.lib().svm_support_vectors_dev(None, None, a.ctypes.data, 4, 2, 0.0, None, a.ctypes.data, None,
+                                           ctypes.byref(n), None) == -1

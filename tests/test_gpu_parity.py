@@ -429,8 +429,9 @@ def test_gram_path_parity(S, name, n, kern):
 
 
 def test_full_size_w3_streaming_prefix(S):
-    """W3 at full size uses the Gram path by default; this keeps the streaming path
-    covered at full size too."""
+    """W3 at full size runs with the automatic row cache by default (the Gram path is
+    opt-in); this keeps the plain streaming path (gram=-1, no cache decision
+    forced) covered at full size too."""
     w = W.get("W3")
     X, y = w.train()
     k = 40

@@ -89,3 +89,21 @@ def test_ovo_matches_oracle(batch):
         assert got["b"] == r.b
     pred = predict_ovo(model, X, Xt, mode=S.PREDICT_EXACT)
     np.testing.assert_array_equal(pred, _oracle_predict(ref, X, m, w, Xt))
+
+
+@pytest.mark.gpu
+def test_batch_with_fewer_ctas_than_problems_is_an_error():
+    """ctas < problems per launch is rejected with SVM_EINVAL (it used to divide by zero
+    in the planner)."""
+    import torch
+    import paper_2311_14908_b200 as S
+    X, labels = W.pavia_like(10, seed=3)
+    probs = []
+    for c in range(4):
+        sel = (labels == c) | (labels == c + 1)
+        yy = np.where(labels[sel] == c, 1, -1).astype(np.int8)
+        probs.append((torch.from_numpy(np.ascontiguousarray(X[sel])).cuda(), torch.from_numpy(yy).cuda()))
+    with pytest.raises(S.SvmError, match="EINVAL"):
+        S.svm_train_batch_dev(probs, 1.0, S.RBF, 0.01, ctas=2)
+    out = S.svm_train_batch_dev(probs, 1.0, S.RBF, 0.01, ctas=4)      # one CTA each: fine
+    assert len(out) == 4 and all(o["info"]["converged"] for o in out)

@@ -47,6 +47,62 @@ def test_two_point_linear_box_optimum():
     assert abs(r.b) <= 1e-12
 
 
+def _int_problem():
+    """Integer linear data: K = X X^T and every g below are exact small integers times a
+    power of two, so the expected biases are exact in fp64."""
+    X = np.array([[2, 0], [1, 1], [0, 3], [-1, 2], [3, -1], [1, -2]], np.float32)
+    y = np.array([1, 1, -1, -1, 1, -1], np.int8)
+    K = X.astype(np.int64) @ X.astype(np.int64).T
+    return X, y, K
+
+
+def test_bias_interior_svs_after_one_epoch():
+    """Bias with free multipliers away from the optimum (R25): one epoch from
+    alpha = 0 gives alpha = lr < C everywhere (all interior), g = lr K y, and
+    b = mean_i (y_i - g_i), written out here from the definition.  The data make that
+    mean clearly non-zero, so a sign slip (g - y) or a wrong set fails."""
+    X, y, K = _int_problem()
+    lr = 0.125
+    r = O.gd_train(X, y, 10.0, O.LINEAR, 0.0, lr, 1)
+    assert np.all(r.alpha == lr)
+    g = lr * (K @ y.astype(np.int64))
+    np.testing.assert_array_equal(r.g, g)
+    b_def = float(np.mean(y.astype(np.float64) - g))
+    assert abs(b_def) > 0.1
+    assert r.b == b_def
+
+
+def test_bias_fallback_all_at_bound():
+    """No interior multiplier: one epoch with lr > C puts every alpha at C, and the bias
+    falls back to the midpoint -(max g + min g)/2 over the SVs (S:L307 fallback), with
+    g = C K y."""
+    X, y, K = _int_problem()
+    C = 0.5
+    r = O.gd_train(X, y, C, O.LINEAR, 0.0, 4.0, 1)
+    assert np.all(r.alpha == C)
+    g = C * (K @ y.astype(np.int64))
+    b_mid = -(g.max() + g.min()) / 2.0
+    assert b_mid != 0.0 and b_mid != -float(np.mean(y - g))
+    assert r.b == b_mid
+
+
+def test_bias_fallback_mixed_bounds():
+    """Multipliers at 0 and at C but none interior: the fallback ranges over the SVs
+    (alpha > 1e-8) only.  Two epochs with lr = 4, C = 1 on two well-separated pairs:
+    epoch 1 sets alpha = C; epoch 2 gives y g >> 1 for the far pair (alpha -> 0) and
+    y g < 1 for the overlapping pair (alpha stays at C)."""
+    X = np.array([[0.0], [0.25], [5.0], [-5.0]], np.float32)
+    y = np.array([1, -1, 1, -1], np.int8)
+    r = O.gd_train(X, y, 1.0, O.LINEAR, 0.0, 4.0, 2)
+    # hand computation: alpha1 = (1, 1, 1, 1); g1 = K y with K = x x^T:
+    #   v = (1, -1, 1, -1); K v = x * (0 - 0.25 + 5 + 5) = 9.75 x
+    #   grad = 1 - y * 9.75 x = (1, 1 + 2.4375, 1 - 48.75, 1 - 48.75) -> alpha2 = (1, 1, 0, 0)
+    np.testing.assert_array_equal(r.alpha, [1.0, 1.0, 0.0, 0.0])
+    # final g = K (alpha2 o y) = x * (0 - 0.25) = (0, -0.0625, -1.25, 1.25); SVs = {0, 1}
+    np.testing.assert_array_equal(r.g, [0.0, -0.0625, -1.25, 1.25])
+    assert r.b == -(0.0 + -0.0625) / 2.0          # over the SVs only (all-i midpoint would be 0)
+
+
 def _box_qp_bruteforce(Q, C):
     """max 1'a - a'Qa/2 over [0, C]^n: every (0 / C / free) pattern whose free block
     solves Q_FF a_F = 1 - Q_FB a_B inside (0, C) with the bounded gradients pointing out."""
