@@ -96,7 +96,13 @@ typedef struct {
                                cluster's shared memory).  Auto picks a cluster when the rows fit
                                (<= 2048 rows per CTA, or <= 8192 with 16 CTAs).  The exchange
                                computes the same lexicographic winner, so results are identical. */
-    int32_t reserved0;      /* 0 */
+    int32_t wss;            /* working-set selection: <= 1 the maximal violating pair (DESIGN
+                               reading R1); 2 second order (Fan, Chen & Lin 2005, cited at P:L140):
+                               u as in 1, then l = argmax over t in I_low with f_t > f_u of
+                               (f_t - f_u)^2 / (K_uu + K_tt - 2 K_ut), lowest index on ties; the
+                               stopping test stays b_low - b_up <= 2 tol.  Each iteration then
+                               takes two row passes and two exchanges.  Not for
+                               svm_train_batch_dev. */
 } svm_params;
 
 typedef struct {

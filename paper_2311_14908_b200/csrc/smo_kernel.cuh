@@ -157,6 +157,14 @@ struct Params {
     // so the arithmetic is the dense path's.  dict_n = 0: not dictionary-coded.
     int dict_n;
     const double* dict;
+    // Working-set selection: 1 = the maximal violating pair (reading
+    // R1); 2 = second order (Fan, Chen & Lin 2005, cited at P:L140): u as in R1, then
+    // l = argmax over t in I_low with f_t > f_u of (f_t - f_u)^2 / a_t,
+    // a_t = K_uu + K_tt - 2 K_ut (<= 1e-12 -> 1e-12), lowest index on ties.  An iteration
+    // is then two row passes: a gain pass over K(x_u, .) and its exchange, then the update
+    // pass over K(x_u, .), K(x_l, .).
+    int wss;
+    const double* qself;           // wss 2, linear kernel: x_t . x_t of every global row (R13 order)
     int l2_keep_chunks;            // streamed X: the first l2_keep_chunks stages (tile-major) of
                                    // every CTA block are copied with an L2 evict_last policy, the
                                    // rest evict_first, so that part of X stays in L2 across
@@ -281,6 +289,8 @@ struct Shared {
     int u, l;                      // global winners of this iteration
     double f_up, f_low;
     double cu, cl;                 // written by the scalar warp before barrier B
+    int pass;                      // wss 2: 1 = this row pass is the gain pass of u (barrier A)
+    double gain_kuu, gain_fu;      // wss 2 gain pass: K(x_u, x_u) and f_u (barrier B)
     double red_f[2][16];           // per consumer warp candidates (local row index; <= 16 warps)
     int red_i[2][16];
     int c_hit, c_su, c_sl;         // row cache: both rows cached / their slots
@@ -582,6 +592,7 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
     const double* const m_gram = BINCL ? nullptr : P.gram;
     const int m_cache = BINCL ? 0 : P.cache_slots;
     const bool m_resident = BINCL || P.resident != 0;
+    const bool m_wss2 = !BINCL && P.wss == 2;               // second-order working set (NEXT-2)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Shared& sh = *reinterpret_cast<Shared*>(smem_raw);
     size_t off = (sizeof(Shared) + 127) & ~size_t(127);
@@ -747,6 +758,11 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
     const long long it_start = it;
     unsigned int cslot = 0, cpar = 0, consumed = 0;
     long long c_hits = 0, c_misses = 0;     // row-cache lookups (scalar lane 0)
+    // wss 2 (scalar warp): wphase 0 = the exchange carries first-order candidates (then
+    // the gain pass of u follows), 1 = it carries gain candidates (then the update pass);
+    // u's index, f, alpha and label are kept from phase 0 for the update
+    int wphase = 0, sv_u = 0, sv_l = 0, sv_yu = 0;
+    double sv_fu = 0.0, sv_au = 0.0;
     const double INF = __longlong_as_double(0x7ff0000000000000ll);
 
     if (m_resident && !m_gram && n_tiles > 0 && !is_scalar) mbar_wait(&full[0], 0);
@@ -925,6 +941,11 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
                     c.al = (jl == INT_MAX) ? 0.0 : (A_SMEM ? a_s[jl] : alpha_g[jl]);
                     c.yu = (ju == INT_MAX) ? 0 : ((fl_s[ju] & FL_POS) ? 1 : -1);
                     c.yl = (jl == INT_MAX) ? 0 : ((fl_s[jl] & FL_POS) ? 1 : -1);
+                    if (m_wss2 && wphase == 1) {
+                        // gain candidates: w1 = (t, gain), w2 = (y_t << 16, f_t), w3 = (0, alpha_t)
+                        c.au = (jl == INT_MAX) ? 0.0 : f_s[jl];
+                        c.yu = 0;
+                    }
                 }
                 Sel best;
                 const int gcta = (rank - xbase) * P.ctas_per_rank + cta;
@@ -973,11 +994,20 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
                 rec_l = __shfl_sync(0xffffffffu, best.gl, ml ? __ffs(ml) - 1 : 0);
             }
             int dec = ST_RUNNING;
-            if (tmo) dec = ST_TIMEOUT;
-            else if (iu == INT_MAX || il == INT_MAX) dec = ST_CONVERGED;
-            else if (fl - fu <= 2.0 * P.tol) dec = ST_CONVERGED;
-            else if (it == max_iter) dec = ST_MAXITER;
-            else if (P.iter_limit > 0 && it - it_start == P.iter_limit) dec = ST_LIMIT;
+            const bool gainA = m_wss2 && wphase == 0;          // wss 2: the gain pass of u follows
+            if (m_wss2 && wphase == 1) {
+                // the second-order l (the stopping test was taken on the first-order pair);
+                // some t always qualifies (the first-order l has f_l > f_u), else keep it
+                if (tmo) dec = ST_TIMEOUT;
+                if (il == INT_MAX) il = sv_l;
+                iu = sv_u; fu = sv_fu;
+            } else {
+                if (tmo) dec = ST_TIMEOUT;
+                else if (iu == INT_MAX || il == INT_MAX) dec = ST_CONVERGED;
+                else if (fl - fu <= 2.0 * P.tol) dec = ST_CONVERGED;
+                else if (it == max_iter) dec = ST_MAXITER;
+                else if (P.iter_limit > 0 && it - it_start == P.iter_limit) dec = ST_LIMIT;
+            }
             if (dec != ST_RUNNING) {
                 final_state = dec;
                 if (lane == 0) {
@@ -988,6 +1018,7 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
                 named_arrive<NSYNC_>(BAR_A);
                 break;
             }
+            if (gainA) { sv_u = iu; sv_l = il; sv_fu = fu; il = iu; }   // the gain pass streams K(x_u, .) only
             // ---- row cache (a8): every CTA runs the same directory operations on the same
             // pair sequence (hash lookup, LRU replacement), so every CTA agrees
             int c_hit = 0, su = -1, sl = -1;
@@ -1040,19 +1071,29 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
                         if (dir_owner[v] >= 0) erase(dir_owner[v]);
                         return v;
                     };
+                    int fu_ = -1, fl_ = -1;
+                    if (gainA) {
+                        // wss 2 gain pass: only u's row (then cached for the update pass)
+                        su = find(iu);
+                        c_hits += su >= 0; c_misses += su < 0;
+                        if (su < 0) { fu_ = victim(-1); dir_owner[fu_] = iu; insert(iu, fu_); }
+                        touch(su >= 0 ? su : fu_);
+                        sl = su;
+                        c_hit = su >= 0 ? 1 : 0;
+                    } else {
                     su = find(iu); sl = find(il);
                     c_hit = (su >= 0 && sl >= 0) ? 1 : 0;
                     c_hits += (su >= 0) + (sl >= 0);
                     c_misses += (su < 0) + (sl < 0);
-                    int fu_ = -1, fl_ = -1;
                     if (su < 0) { fu_ = victim(sl); dir_owner[fu_] = iu; insert(iu, fu_); }
                     touch(su >= 0 ? su : fu_);
                     if (sl < 0) { fl_ = victim(su >= 0 ? su : fu_); dir_owner[fl_] = il; insert(il, fl_); }
                     touch(sl >= 0 ? sl : fl_);
+                    }
                     sh.c_hit = c_hit; sh.c_su = su; sh.c_sl = sl; sh.c_fill_u = fu_; sh.c_fill_l = fl_;
                     // both rows cached: start the load of K_ul (column l of u's row) now, so its
                     // latency overlaps the winners' words and barrier A
-                    if (c_hit && kul_cache_ok(P, iu, il)) kul_pre = kcache_at(P, su, il);
+                    if (c_hit && !gainA && kul_cache_ok(P, iu, il)) kul_pre = kcache_at(P, su, il);
                 }
                 c_hit = __shfl_sync(0xffffffffu, c_hit, 0);
                 su = __shfl_sync(0xffffffffu, su, 0);
@@ -1154,7 +1195,7 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
                     }
                 }
             }
-            if (lane == 0) { sh.decision = ST_RUNNING; sh.u = iu; sh.l = il; }
+            if (lane == 0) { sh.decision = ST_RUNNING; sh.u = iu; sh.l = il; sh.pass = gainA ? 1 : 0; }
             __syncwarp();
             named_arrive<NSYNC_>(BAR_A);
             if (lane < 3 && !m_cluster) {
@@ -1165,13 +1206,21 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
                 }
             }
             const uint32_t wa_aux = rec_aux(wa);
-            const int yu = (int)(int16_t)(__shfl_sync(0xffffffffu, wa_aux, 0) & 0xffffu);
-            const double au = __hiloint2double((int)__shfl_sync(0xffffffffu, rec_hi(wa), 0), (int)__shfl_sync(0xffffffffu, rec_lo(wa), 0));
+            int yu = (int)(int16_t)(__shfl_sync(0xffffffffu, wa_aux, 0) & 0xffffu);
+            double au = __hiloint2double((int)__shfl_sync(0xffffffffu, rec_hi(wa), 0), (int)__shfl_sync(0xffffffffu, rec_lo(wa), 0));
             const int yl = (int)(int16_t)(__shfl_sync(0xffffffffu, wa_aux, 1) >> 16);
             const double al = __hiloint2double((int)__shfl_sync(0xffffffffu, rec_hi(wa), 2), (int)__shfl_sync(0xffffffffu, rec_lo(wa), 2));
+            if (m_wss2) {
+                // phase 0: keep u's alpha and label for the update; phase 1: word 2 of l's gain
+                // record carries f_l (the pair's gap is f_l - f_u, not the first-order gap)
+                const double f_rec = __hiloint2double((int)__shfl_sync(0xffffffffu, rec_hi(wa), 1),
+                                                      (int)__shfl_sync(0xffffffffu, rec_lo(wa), 1));
+                if (gainA) { sv_au = au; sv_yu = yu; }
+                else { au = sv_au; yu = sv_yu; fl = f_rec; }
+            }
             SVM_PHASE(timing, PH_S_PIVOT);
             const int u = iu, l = il;
-            if (m_cache > 0 && !c_hit) {
+            if (m_cache > 0 && !c_hit && !gainA) {
                 // compact the non-zero terms of K(x_u, x_l) (RBF: x_u - x_l; linear: pairs
                 // with x_u or x_l non-zero) in ascending k
                 int cnt = 0;
@@ -1192,6 +1241,19 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
                 __syncwarp();
             }
         // ---- pair update (a2): eta, clipped step, snapped alphas (lane 0)
+            if (gainA) {
+                // wss 2 gain pass: K(x_u, x_u) and f_u for the consumers' gains; no update
+                if (lane == 0) {
+                    sh.gain_kuu = KERNEL == 1 ? 1.0 : __ldg(&P.qself[u]);
+                    sh.gain_fu = fu;
+                    sh.cu = 0.0; sh.cl = 0.0;
+                }
+                __syncwarp();
+                named_arrive<NSYNC_>(BAR_B);
+                wphase = 1;
+                continue;
+            }
+            if (m_wss2) wphase = 0;
             if (lane == 0) {
                 double Kuu, Kll, Kul;
                 if (m_gram) {
@@ -1290,6 +1352,7 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
         }
         // ================= consumers: row pass (a3-a5)
         const int u = sh.u, l = sh.l;
+        const bool gain = m_wss2 && sh.pass != 0;      // wss 2: gain pass over K(x_u, .)
         const bool c_hit = m_cache > 0 && sh.c_hit;
         const int su = sh.c_su, sl = sh.c_sl;
         bool rows_ready = m_gram != nullptr;
@@ -1510,7 +1573,8 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
 #pragma unroll
                     for (int q = 0; q < RPT; ++q) {
                         ku[q] = svmexp::exp_cr_fast(-(P.gamma * du[q]), tab, su[q]);
-                        kl[q] = svmexp::exp_cr_fast(-(P.gamma * dl[q]), tab, sl[q]);
+                        if (gain) { kl[q] = ku[q]; sl[q] = true; }
+                        else kl[q] = svmexp::exp_cr_fast(-(P.gamma * dl[q]), tab, sl[q]);
                         all_safe = all_safe && su[q] && sl[q];
                     }
                     if (!all_safe) {
@@ -1527,6 +1591,28 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
                         if (jg == l) kl[q] = 1.0;
                     }
                 }
+                if (gain) {
+                    // wss 2 gain pass: candidates t in I_low with f_t > f_u, gain
+                    // (f_t - f_u)^2 / a_t, a_t = K_uu + K_tt - 2 K_ut (<= 1e-12 -> 1e-12); the
+                    // maximum with the lowest index (rows in increasing j, strict >)
+                    const double gfu = sh.gain_fu, gkuu = sh.gain_kuu;
+#pragma unroll
+                    for (int q = 0; q < RPT; ++q) {
+                        const int j = tile * P.rt + t * RPT + q;
+                        if (j < R) {
+                            if (fill_u) fill_u[j] = ku[q];
+                            const double fj = f_s[j];
+                            if ((fl_s[j] & FL_LOW) && fj > gfu) {
+                                const double bb = fj - gfu;
+                                const double ktt = KERNEL == 1 ? 1.0 : __ldg(&P.qself[gbase + j]);
+                                double aa = gkuu + ktt - 2.0 * ku[q];
+                                if (!(aa > 1e-12)) aa = 1e-12;
+                                const double gg = (bb * bb) / aa;
+                                if (gg > bfl) { bfl = gg; bjl = j; }
+                            }
+                        }
+                    }
+                } else
 #pragma unroll
                 for (int q = 0; q < RPT; ++q) {
                     const int j = tile * P.rt + t * RPT + q;

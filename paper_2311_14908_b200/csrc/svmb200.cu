@@ -57,6 +57,15 @@ __global__ void k_build_xblk(const float* __restrict__ X, long long n_r, int d, 
     }
 }
 
+// x_t . x_t of every row, ascending k, one fma per term (R13; wss 2 gains, linear kernel)
+__global__ void k_self_dot(const float* __restrict__ X, long long n, int d, double* __restrict__ q) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    double acc = 0.0;
+    for (int k = 0; k < d; ++k) { const double x = X[t * d + k]; acc = fma(x, x, acc); }
+    q[t] = acc;
+}
+
 // counts values of X that are not exactly 0 or 1
 __global__ void k_count_nonbinary(const float* __restrict__ X, long long nx, unsigned long long* out) {
     unsigned long long c = 0;
@@ -289,6 +298,8 @@ int check_params(long long n, long long d, const svm_params* p, svm_params* q) {
     if (q->sv_epsilon <= 0.0) q->sv_epsilon = 1e-8;
     if (q->virtual_ranks <= 1) q->virtual_ranks = 1;
     if (q->virtual_ranks > MAXR) return fail(SVM_EINVAL, "virtual_ranks > 8");
+    if (q->wss <= 0) q->wss = 1;
+    if (q->wss > 2) return fail(SVM_EINVAL, "wss must be 1 (first order) or 2 (second order)");
     return SVM_OK;
 }
 
@@ -502,7 +513,8 @@ int solve(SolveArgs& a) {
     Plan pl;
     int rc = SVM_OK;
     bool binary = false;
-    if (!a.independent && getenv("SVMB200_NO_BINARY") == nullptr && a.d <= 1024) {
+    // (wss 2 runs on fp32 / dictionary / mixed rows: the resident bit-row loop has no gain pass)
+    if (!a.independent && p.wss != 2 && getenv("SVMB200_NO_BINARY") == nullptr && a.d <= 1024) {
         unsigned long long* dc = nullptr;
         CKR(cudaMallocAsync(&dc, 8, a.stream));
         CKR(cudaMemsetAsync(dc, 0, 8, a.stream));
@@ -664,6 +676,7 @@ int solve(SolveArgs& a) {
     // rows travel in the records.  Auto: the smallest power-of-two cluster with <= 2048 rows
     // per CTA (else 16 CTAs if <= 8192 rows each), when it is resident.
     const bool cl_allowed = gram == nullptr && pl.cache_slots == 0 && pl.mix_nseg == 0 && pl.esz == 4 && a.p.cluster != -1 &&
+                            p.wss != 2 &&
                             a.world == a.nranks_here && (a.world == 1 || a.independent) &&
                             (a.p.ctas <= 0 || a.p.cluster > 0) && getenv("SVMB200_NO_CLUSTER") == nullptr;
     if (a.p.cluster > 16 || a.p.cluster < -1) return fail(SVM_EINVAL, "cluster must be -1, 0 or 1..16");
@@ -782,6 +795,7 @@ int solve(SolveArgs& a) {
         P.max_iter_rank[r] = a.independent ? a.max_iter_rank[r] : p.max_iter;
     }
     P.timeout_ns = a.timeout_ns;
+    P.wss = p.wss;
     if (const char* e = getenv("SVMB200_POLL_NS")) P.poll_ns = atoi(e);
     // L2 residency of streamed X: keep the first tiles of every CTA block in L2
     // (SVMB200_L2_KEEP_MB, per GPU; tuning)
@@ -870,6 +884,14 @@ int solve(SolveArgs& a) {
             CKR(cudaMemsetAsync(mb, 0, mbox_bytes, st));
             P.mbox[r] = mb;
         }
+    }
+    if (p.wss == 2 && p.kernel == SVM_LINEAR) {
+        // K(x_t, x_t) of every row for the second-order gains (R13 order, as the oracle's dot)
+        double* qs;
+        if ((rc = dalloc((void**)&qs, (size_t)a.n_global * 8))) { release(); return rc; }
+        k_self_dot<<<(unsigned)((a.n_global + 255) / 256), 256, 0, st>>>(a.xr, a.n_global, (int)a.d, qs);
+        counted();
+        P.qself = qs;
     }
     long long* dtrace = nullptr;
     if (a.trace && a.trace_cap > 0) {
@@ -1196,6 +1218,7 @@ extern "C" int svm_train_batch_dev(int B, const float* const* X, const int8_t* c
         for (int k = 0; k < nb; ++k) {
             if (!X[b0 + k] || !y[b0 + k] || !alpha[b0 + k]) return fail(SVM_EINVAL, "null problem pointer");
             if ((rc = check_params(n[b0 + k], d, p_in, &p))) return rc;
+            if (p.wss == 2) return fail(SVM_EINVAL, "wss = 2 is not supported by svm_train_batch_dev");
             if ((rc = validate_device(X[b0 + k], y[b0 + k], n[b0 + k], d, st, nullptr))) return rc;
             a.max_iter_rank[k] = p.max_iter;
             if (p_in->max_iter <= 0) a.max_iter_rank[k] = (10 * n[b0 + k] > 10000) ? 10 * n[b0 + k] : 10000;

@@ -1,0 +1,171 @@
+"""Full-size parity of the largest configs (SURVEY §8(c) "Large configs" row; VERDICT r1
+item 1): the oracle cannot run W4 / W5 to convergence (days of CPU time), so
+
+  * segment parity -- the GPU solve is stopped at k in {10^4, 10^5, ~final - 1000} (the
+    bench's launch configuration, one GPU); the oracle resumes from the GPU's (alpha, f)
+    snapshot and runs the next 50 SMO steps; the GPU resumed from the same snapshot must
+    take the identical 50 pairs and reach bit-identical alpha and f over all n rows;
+  * converged-state properties on the GPU's final state at any size -- KKT at
+    tol' = 2 tau on every row, box and equality constraints, gap <= 2 tau,
+    and f on sampled rows equal to the oracle's from-scratch sum_j alpha_j y_j K_ij - y_i
+    (S:L176);
+  * tensor-core prediction at scale -- the 3xTF32 path over all held-out rows in the
+    bench's configuration, sampled rows against the oracle's decision values
+    (BASELINE.json tolerance 1e-4, identical labels).
+
+Marked `gpu`; ~6 minutes on a B200 box with 16 host cores."""
+import numpy as np
+import pytest
+
+from gen import workloads as W
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+SEG = 50
+
+
+@pytest.fixture(scope="module")
+def S():
+    import paper_2311_14908_b200 as S
+    S.lib()
+    return S
+
+
+def _chain(S, name, bounds):
+    """GPU solve stopped at the given iteration counts (warm-started segments, each a
+    device solve in the default launch configuration), then run to convergence."""
+    import torch
+    w = W.get(name)
+    X, y = w.train()
+    Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    snaps = {}
+    a = f = None
+    done = 0
+    for k in bounds:
+        r = S.svm_train_dev(Xd, yd, w.C, w.kernel, w.gamma, w.tol, max_iter=k - done, alpha0=a, f0=f,
+                            want_f=True)
+        assert r["info"]["iterations"] == k - done and r["info"]["converged"] == 0
+        a, f = r["alpha"], r["f"]
+        done = k
+        snaps[k] = (a.cpu().numpy(), f.cpu().numpy())
+    r = S.svm_train_dev(Xd, yd, w.C, w.kernel, w.gamma, w.tol, alpha0=a, f0=f, want_f=True)
+    final = dict(alpha=r["alpha"].cpu().numpy(), f=r["f"].cpu().numpy(), b=r["b"], info=r["info"],
+                 total=done + r["info"]["iterations"])
+    return w, X, y, Xd, yd, snaps, final
+
+
+@pytest.fixture(scope="module")
+def w5(S):
+    return _chain(S, "W5", (10_000, 100_000, 410_000))
+
+
+@pytest.fixture(scope="module")
+def w4(S):
+    return _chain(S, "W4", (10_000, 100_000, 132_900))
+
+
+def _segment(S, chain, k):
+    w, X, y, Xd, yd, snaps, final = chain
+    import torch
+    a0, f0 = snaps[k]
+    ref = O.train(X, y, w.C, w.kernel, w.gamma, w.tol, max_iter=SEG, alpha0=a0, f0=f0, trace_cap=SEG)
+    r = S.svm_train_dev(Xd, yd, w.C, w.kernel, w.gamma, w.tol, max_iter=SEG, alpha0=torch.from_numpy(a0).cuda(),
+                        f0=torch.from_numpy(f0).cuda(), want_f=True, trace_cap=SEG)
+    assert r["info"]["iterations"] == ref.iterations == SEG
+    np.testing.assert_array_equal(r["trace"], ref.trace)
+    np.testing.assert_array_equal(r["alpha"].cpu().numpy(), ref.alpha)
+    np.testing.assert_array_equal(r["f"].cpu().numpy(), ref.f)
+    assert r["info"]["b_up"] == ref.b_up and r["info"]["b_low"] == ref.b_low
+
+
+def _converged(chain, n_f_rows):
+    w, X, y, Xd, yd, snaps, final = chain
+    a, f, b, info = final["alpha"], final["f"], final["b"], final["info"]
+    C, tol = w.C, w.tol
+    assert info["converged"] == 1 and info["gap"] <= 2 * tol
+    assert np.all(a >= 0) and np.all(a <= C)
+    yd_ = y.astype(np.float64)
+    assert abs(np.dot(a, yd_)) <= 1e-9 * max(1.0, C * np.sqrt(len(y)))
+    # KKT at tol' = 2 tau on every row: y dec(x_i) = y_i f_i + 1 + y_i b
+    m = yd_ * f + 1.0 + yd_ * b
+    t2 = 2 * tol
+    assert np.all(m[a == 0] >= 1 - t2)
+    free = (a > 0) & (a < C)
+    assert np.all(np.abs(m[free] - 1) <= t2)
+    assert np.all(m[a == C] <= 1 + t2)
+    # f on sampled rows against the oracle's from-scratch sum
+    sv = a > 0
+    rows = np.random.default_rng(1).choice(len(y), n_f_rows, replace=False)
+    f_ref = O.decision(X[sv], (a * y)[sv], 0.0, w.kernel, w.gamma, X[rows]) - y[rows]
+    np.testing.assert_allclose(f[rows], f_ref, rtol=0, atol=1e-6)
+    # the dual objective from the device reduction (S:L176 f form) against numpy's
+    W_np = 0.5 * float(np.sum(a * (1.0 - yd_ * f)))
+    assert abs(info["dual_objective"] - W_np) <= 1e-10 * abs(W_np)
+
+
+@pytest.mark.parametrize("k", [10_000, 100_000, 410_000])
+def test_w5_segment_parity(S, w5, k):
+    _segment(S, w5, k)
+
+
+def test_w5_converged_state(w5):
+    final = w5[-1]
+    assert 410_000 + SEG <= final["total"] <= 410_000 + 3000      # the last snapshot is ~final - 1000
+    _converged(w5, 200)
+
+
+@pytest.mark.parametrize("k", [10_000, 100_000, 132_900])
+def test_w4_segment_parity(S, w4, k):
+    _segment(S, w4, k)
+
+
+def test_w4_converged_state(w4):
+    final = w4[-1]
+    assert 132_900 + SEG <= final["total"] <= 132_900 + 3000
+    _converged(w4, 300)
+
+
+def _predict_at_scale(S, Xsv, coef, b, w, Xt_all, rows):
+    import torch
+    dec = S.svm_predict_dev(torch.from_numpy(Xsv).cuda(), torch.from_numpy(coef).cuda(), b, w.kernel, w.gamma,
+                            torch.from_numpy(Xt_all).cuda(), mode=S.PREDICT_TENSOR).cpu().numpy()
+    ref = O.decision(Xsv, coef, b, w.kernel, w.gamma, Xt_all[rows])
+    err = np.max(np.abs(dec[rows] - ref))
+    assert err <= 1e-4, err
+    clear = np.abs(ref) > 1e-4
+    assert np.array_equal(np.sign(dec[rows][clear]), np.sign(ref[clear]))
+    return err
+
+
+def test_predict_tensor_w2_bench_model(S):
+    """The W2 bench prediction: the oracle's converged W2 model (tests/golden, 27k SVs)
+    over all 16,281 held-out rows on the tensor cores; 4,000 sampled rows against the
+    oracle."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "W2_oracle.npz"))
+    w = W.get("W2")
+    X, y = w.train()
+    sv = g["alpha"] > 1e-8
+    assert sv.sum() > 20000
+    Xt, _ = w.test()
+    rows = np.random.default_rng(2).choice(len(Xt), 4000, replace=False)
+    _predict_at_scale(S, np.ascontiguousarray(X[sv]), (g["alpha"] * y)[sv], float(g["b"]), w, Xt, rows)
+
+
+def test_predict_tensor_w5_scale(S):
+    """BASELINE.json configs[4] prediction size: 10^6 held-out rows against 450,000
+    support vectors (W5 training rows; coefficients drawn like alpha y with C = 1, 40% at
+    the bound) in one tensor-core launch; 1,000 sampled rows against the oracle."""
+    w = W.get("W5")
+    X, _ = w.train()
+    nsv = 450_000
+    rng = np.random.default_rng(55)
+    coef = rng.uniform(0.0, 1.0, nsv)
+    coef[rng.random(nsv) < 0.4] = 1.0
+    coef *= np.where(rng.random(nsv) < 0.5, 1.0, -1.0)
+    Xsv = np.ascontiguousarray(X[:nsv])
+    del X
+    Xt, _ = w.test()
+    rows = np.random.default_rng(3).choice(len(Xt), 1000, replace=False)
+    _predict_at_scale(S, Xsv, coef, 0.037, w, Xt, rows)

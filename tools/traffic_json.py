@@ -10,7 +10,7 @@ import json
 import sys
 
 
-def main(src, workload, out):
+def main(src, workload, out, iterations=None):
     vals, kernel = {}, None
     with open(src) as fh:
         lines = [ln for ln in fh if ln.startswith('"')]
@@ -27,12 +27,14 @@ def main(src, workload, out):
     rd, wr = vals.get("dram__bytes_read.sum", 0.0), vals.get("dram__bytes_write.sum", 0.0)
     short = kernel.split("(")[0].replace("void ", "").replace("svmk::", "").replace(" ", "") if kernel else None
     res = {"kernel": short, "workload": workload, "dram_bytes_per_launch": int(rd + wr),
+           "iterations": int(iterations) if iterations else None,
+           "dram_bytes_per_iter": (rd + wr) / int(iterations) if iterations else None,
            "dram_read": int(rd), "dram_write": int(wr), "duration_ms": vals.get("gpu__time_duration.sum"),
-           "note": "ncu --metrics dram__bytes_{read,write}.sum; one launch = one whole solve", "source": src}
+           "note": "ncu --metrics dram__bytes_{read,write}.sum of one solver launch (the given iterations)", "source": src}
     with open(out, "w") as fh:
         json.dump(res, fh, indent=1)
     print(json.dumps(res))
 
 
 if __name__ == "__main__":
-    main(*sys.argv[1:4])
+    main(*sys.argv[1:5])
