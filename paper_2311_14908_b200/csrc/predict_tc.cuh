@@ -20,8 +20,9 @@
 //     thread); two 128-column TMEM accumulators so the epilogue of tile j overlaps the
 //     MMAs of tile j + 1
 //   * epilogue in fp64: D = |t|^2 + |s|^2 - 2 (t.s) from exact fp64 norms, K = exp(-gamma D)
-//     (CUDA's fp64 exp), dec accumulated with fp64 fma -- fp32 there would cost up to
-//     1e-3 on Adult-like data (C = 100, 15 distinct kernel values, correlated rounding).
+//     (a table-driven fp64 exp good to a few ulp, exp_nonpos), dec accumulated with fp64
+//     fma -- fp32 there would cost up to 1e-3 on Adult-like data (C = 100, 15 distinct
+//     kernel values, correlated rounding).
 // Not bit-exact (tensor cores); parity vs the oracle is BASELINE.json's 1e-4 absolute.
 #pragma once
 
@@ -91,6 +92,30 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                  :: "r"(smem_u32(bar)) : "memory");
 }
 
+// exp(x) for x <= 0 in fp64 to a few ulp, for the epilogue (the decision values are
+// checked to 1e-4 absolute, the tf32 products are good to ~2^-21, so a correctly rounded
+// exp is not needed here -- the exact path has one).  x = (n / 64) ln 2 + r, |r| <= ln 2 / 128:
+// exp(x) = 2^(n >> 6) * 2^((n & 63) / 64) * exp(r), exp(r) by its degree-5 Taylor
+// polynomial (truncation r^6 / 720 < 4e-17), 2^(j / 64) from a 64-entry table in shared
+// memory; x < -708 gives 0 (the kernel value is below 3.3e-308).  About 11 fp64
+// operations against ~25 for the libdevice exp, which bounded the epilogue.
+__device__ __forceinline__ double exp_nonpos(double x, const double* __restrict__ t64) {
+    if (x < -708.0) return 0.0;
+    const double sh = 6755399441055744.0;                    // 1.5 * 2^52: round to integer
+    const double kk = fma(x, 92.33248261689366, sh);     // x * 64 / ln 2 + shift
+    const int n = __double2loint(kk);
+    const double nd = kk - sh;
+    double r = fma(nd, -0.010830424695996044, x);           // ln 2 / 64, high part (35 bits:
+    r = fma(nd, -2.5310172166650877e-13, r);                 // nd * hi exact) and low part
+    double q = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+    q = fma(q, r, 1.0 / 6.0);
+    q = fma(q, r, 0.5);
+    q = fma(q, r, 1.0);
+    q = fma(q, r, 1.0);
+    const double v = t64[n & 63] * q;
+    return __hiloint2double(__double2hiint(v) + (n >> 6) * (1 << 20), __double2loint(v));
+}
+
 template <int KERNEL>
 __global__ void __launch_bounds__(NTHREADS, 1)
 k_predict_tc(const float* __restrict__ A,   // packed test rows [m_tiles][k_chunks][2][BM*BK]
@@ -105,6 +130,8 @@ k_predict_tc(const float* __restrict__ A,   // packed test rows [m_tiles][k_chun
     __shared__ uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
     __shared__ uint32_t tmem_base_sh;
     __shared__ double part_sh[NPART][BM];           // the column parts' partial sums
+    __shared__ double t64[64];                      // 2^(j / 64), j = 0..63 (exp_nonpos)
+    if (threadIdx.x < 64) t64[threadIdx.x] = exp2((double)threadIdx.x / 64.0);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int mt = blockIdx.x;
@@ -211,7 +238,7 @@ k_predict_tc(const float* __restrict__ A,   // packed test rows [m_tiles][k_chun
                     double kv;
                     if (KERNEL == 1) {
                         const double dist = fmax(q_t + __ldg(&qs_t[c0 + j]) - 2.0 * dot, 0.0);
-                        kv = exp(-gamma * dist);
+                        kv = exp_nonpos(-gamma * dist, t64);
                     } else {
                         kv = dot;
                     }
