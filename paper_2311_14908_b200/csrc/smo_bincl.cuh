@@ -220,8 +220,11 @@ __global__ void __launch_bounds__(NTB, 1) smo_bincl(const Params P) {
                 for (int q = 0; q < BT; ++q) {
                     ku[q] = ktab[du[q]];      // RBF: K(x_j, x_j) = ktab[0] = 1 (R16)
                     kl[q] = ktab[dl[q]];
-                    fj[q] = f_s[jq[q]];
-                    gq[q] = fl_s[jq[q]];
+                    // rows past the end (clamped to R - 1, whose owner may be updating it)
+                    // are not read: their results are discarded anyway
+                    const bool in = (q0 + q) * NTB + t < R;
+                    fj[q] = in ? f_s[jq[q]] : 0.0;
+                    gq[q] = in ? fl_s[jq[q]] : (uint8_t)0;
                 }
 #pragma unroll
                 for (int q = 0; q < BT; ++q) {
@@ -230,7 +233,11 @@ __global__ void __launch_bounds__(NTB, 1) smo_bincl(const Params P) {
                 }
             } else {
 #pragma unroll
-                for (int q = 0; q < BT; ++q) { fj[q] = f_s[jq[q]]; gq[q] = fl_s[jq[q]]; }
+                for (int q = 0; q < BT; ++q) {
+                    const bool in = (q0 + q) * NTB + t < R;
+                    fj[q] = in ? f_s[jq[q]] : 0.0;
+                    gq[q] = in ? fl_s[jq[q]] : (uint8_t)0;
+                }
             }
             double cfu[BT], cfl[BT];
             int cju[BT], cjl[BT];
