@@ -103,6 +103,16 @@ typedef struct {
                                stopping test stays b_low - b_up <= 2 tol.  Each iteration then
                                takes two row passes and two exchanges.  Not for
                                svm_train_batch_dev. */
+    int32_t shrink_window;  /* window shrinking (DESIGN reading R29): 0 off; H > 0 runs the solve in
+                               windows of H updates; at each window start (every row selected
+                               over, stopping test taken) the rows that cannot form a violating
+                               pair -- i in I_up only with f_i > b_low, i in I_low only with
+                               f_i < b_up -- are set aside for the window: only the active rows
+                               are streamed and selected over, and the window's updates are
+                               replayed on the rows set aside at its end (their f stays the exact
+                               incremental value).  A window also ends when the active rows'
+                               gap reaches 2 tol.  svm_train_dev / svm_train_ex, one rank. */
+    int32_t reserved1;      /* 0 */
 } svm_params;
 
 typedef struct {

@@ -54,6 +54,8 @@ def lib():
             L.oracle_svm_train.restype = i32
             L.oracle_svm_train_wss.argtypes = L.oracle_svm_train.argtypes + [i32]
             L.oracle_svm_train_wss.restype = i32
+            L.oracle_svm_train_full.argtypes = L.oracle_svm_train.argtypes + [i32, i64]
+            L.oracle_svm_train_full.restype = i32
             L.oracle_select_second_order.argtypes = [P, P, P, P, f64, i64, i64, i32, f64, i64]
             L.oracle_select_second_order.restype = i64
             L.oracle_decision.argtypes = [P, P, i64, i64, f64, i32, f64, P, i64, P]
@@ -115,9 +117,11 @@ class TrainResult(dict):
 
 
 def train(X, y, C: float, kernel: int, gamma: float = 0.0, tol: float = 1e-3,
-          max_iter: int = 0, alpha0=None, f0=None, trace_cap: int = 0, wss: int = 1) -> TrainResult:
+          max_iter: int = 0, alpha0=None, f0=None, trace_cap: int = 0, wss: int = 1,
+          shrink: int = 0) -> TrainResult:
     """The oracle SMO solve (smo_oracle.c).  wss: 1 maximal violating pair (reading R1,
-    default), 2 second-order selection of the second index (Fan et al.)."""
+    default), 2 second-order selection of the second index (Fan et al.).
+    shrink: window length H of window shrinking (reading R29), 0 = off."""
     X = _f32(X)
     y = np.ascontiguousarray(y, dtype=np.int8)
     n, d = X.shape
@@ -129,11 +133,11 @@ def train(X, y, C: float, kernel: int, gamma: float = 0.0, tol: float = 1e-3,
     b, it = ctypes.c_double(), ctypes.c_int64()
     conv = ctypes.c_int()
     bu, bl = ctypes.c_double(), ctypes.c_double()
-    rc = lib().oracle_svm_train_wss(_p(X), _p(y), n, d, float(C), int(kernel), float(gamma),
-                                    float(tol), int(max_iter), _p(a0), _p(g0), _p(alpha), _p(f),
-                                    ctypes.byref(b), ctypes.byref(it), ctypes.byref(conv),
-                                    ctypes.byref(bu), ctypes.byref(bl), _p(trace),
-                                    trace_cap if trace_cap > 0 else 0, int(wss))
+    rc = lib().oracle_svm_train_full(_p(X), _p(y), n, d, float(C), int(kernel), float(gamma),
+                                     float(tol), int(max_iter), _p(a0), _p(g0), _p(alpha), _p(f),
+                                     ctypes.byref(b), ctypes.byref(it), ctypes.byref(conv),
+                                     ctypes.byref(bu), ctypes.byref(bl), _p(trace),
+                                     trace_cap if trace_cap > 0 else 0, int(wss), int(shrink))
     if rc != 0:
         raise ValueError(f"oracle_svm_train failed with status {rc}")
     res = TrainResult(alpha=alpha, f=f, b=b.value, iterations=it.value,

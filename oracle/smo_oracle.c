@@ -192,14 +192,26 @@ int oracle_select(const double* f, const int8_t* y, const double* alpha, double 
  * the unconstrained pair step,
  *     g_t = (f_t - f_u)^2 / a_t,   a_t = K_uu + K_tt - 2 K_ut  (a_t <= 1e-12 -> 1e-12),
  * ties to the lowest index (reading R4).  Returns -1 when no t qualifies. */
+static int64_t select_second_order_masked(const float* X, const int8_t* y, const double* alpha,
+                                          const double* f, double C, int64_t n, int64_t d,
+                                          int kernel, double gamma, int64_t u, const uint8_t* active);
+
 int64_t oracle_select_second_order(const float* X, const int8_t* y, const double* alpha,
                                    const double* f, double C, int64_t n, int64_t d,
                                    int kernel, double gamma, int64_t u) {
+    return select_second_order_masked(X, y, alpha, f, C, n, d, kernel, gamma, u, NULL);
+}
+
+/* the same over the rows with active[t] != 0 (NULL: all rows; R29 windows) */
+static int64_t select_second_order_masked(const float* X, const int8_t* y, const double* alpha,
+                                          const double* f, double C, int64_t n, int64_t d,
+                                          int kernel, double gamma, int64_t u, const uint8_t* active) {
     const float* xu = X + u * d;
     const double Kuu = oracle_kernel(kernel, gamma, xu, xu, d, 1);
     int64_t best = -1;
     double best_g = 0.0;
     for (int64_t t = 0; t < n; ++t) {
+        if (active && !active[t]) continue;
         const int pos = y[t] == 1;
         const int low = pos ? (alpha[t] > 0.0) : (alpha[t] < C);
         if (!low) continue;
@@ -223,6 +235,49 @@ int oracle_svm_train(const float* X, const int8_t* y, int64_t n, int64_t d, doub
                      int* converged_out, double* b_up_out, double* b_low_out,
                      int64_t* pair_trace, int64_t trace_cap);
 
+/* Window shrinking (reading R29; the shrinking heuristic of the SMO
+ * improvements P:L140 cites, "keerthi2001improvements" / "fan2005working", in the form of
+ * Joachims / LIBSVM, with f kept exact): the solve runs in windows of H updates.  At a
+ * window start every row is active; the pair is selected over all rows and the stopping
+ * test taken; then the rows that cannot form a violating pair are set aside for the
+ * window -- i in I_up only with f_i > b_low, and i in I_low only with f_i < b_up.  Inside
+ * the window the pair is selected over the active rows only; when their gap falls to
+ * 2 tol, or after H updates, the window ends (the next selection is over all rows
+ * again).  Every update is applied to every row's f (rows set aside are only excluded
+ * from the selection), so f stays the exact incremental value. */
+static void shrink_mark(const double* f, const int8_t* y, const double* alpha, double C, int64_t n,
+                        double b_up, double b_low, uint8_t* active) {
+    for (int64_t j = 0; j < n; ++j) {
+        int in_up = (y[j] == 1 && alpha[j] < C) || (y[j] == -1 && alpha[j] > 0.0);
+        int in_low = (y[j] == 1 && alpha[j] > 0.0) || (y[j] == -1 && alpha[j] < C);
+        int out = (in_up && !in_low && f[j] > b_low) || (in_low && !in_up && f[j] < b_up);
+        active[j] = (uint8_t)!out;
+    }
+}
+
+/* S:L194-202 selection restricted to the rows with active[j] != 0 (NULL: all rows). */
+static int select_active(const double* f, const int8_t* y, const double* alpha, double C, int64_t n,
+                         const uint8_t* active, int64_t* i_up, int64_t* i_low, double* b_up, double* b_low) {
+    int64_t u = -1, l = -1;
+    double fu = 0.0, fl = 0.0;
+    for (int64_t j = 0; j < n; ++j) {
+        if (active && !active[j]) continue;
+        int in_up = (y[j] == 1 && alpha[j] < C) || (y[j] == -1 && alpha[j] > 0.0);
+        int in_low = (y[j] == 1 && alpha[j] > 0.0) || (y[j] == -1 && alpha[j] < C);
+        if (in_up && (u < 0 || f[j] < fu)) { u = j; fu = f[j]; }
+        if (in_low && (l < 0 || f[j] > fl)) { l = j; fl = f[j]; }
+    }
+    *i_up = u; *i_low = l; *b_up = fu; *b_low = fl;
+    return (u >= 0 && l >= 0);
+}
+
+int oracle_svm_train_full(const float* X, const int8_t* y, int64_t n, int64_t d, double C,
+                          int kernel, double gamma, double tol, int64_t max_iter,
+                          const double* alpha0, const double* f0,
+                          double* alpha, double* f, double* b_out, int64_t* iters_out,
+                          int* converged_out, double* b_up_out, double* b_low_out,
+                          int64_t* pair_trace, int64_t trace_cap, int wss, int64_t shrink_window);
+
 /* The SMO solve with working-set rule wss (1: maximal violating pair, S:L197 -- the
  * default reading R1; 2: second-order selection of l above).  The stopping test is the
  * first-order gap in both. */
@@ -232,6 +287,17 @@ int oracle_svm_train_wss(const float* X, const int8_t* y, int64_t n, int64_t d, 
                          double* alpha, double* f, double* b_out, int64_t* iters_out,
                          int* converged_out, double* b_up_out, double* b_low_out,
                          int64_t* pair_trace, int64_t trace_cap, int wss) {
+    return oracle_svm_train_full(X, y, n, d, C, kernel, gamma, tol, max_iter, alpha0, f0, alpha, f, b_out,
+                                 iters_out, converged_out, b_up_out, b_low_out, pair_trace, trace_cap, wss, 0);
+}
+
+/* wss as above; shrink_window H > 0 turns on window shrinking (R29), 0 = off. */
+int oracle_svm_train_full(const float* X, const int8_t* y, int64_t n, int64_t d, double C,
+                          int kernel, double gamma, double tol, int64_t max_iter,
+                          const double* alpha0, const double* f0,
+                          double* alpha, double* f, double* b_out, int64_t* iters_out,
+                          int* converged_out, double* b_up_out, double* b_low_out,
+                          int64_t* pair_trace, int64_t trace_cap, int wss, int64_t shrink_window) {
     oracle_init();
     if (n < 2 || d < 1 || !(C > 0.0) || !(tol > 0.0)) return -1;
     if (kernel == ORACLE_RBF && !(gamma > 0.0)) return -1;
@@ -249,12 +315,25 @@ int oracle_svm_train_wss(const float* X, const int8_t* y, int64_t n, int64_t d, 
     int64_t it = 0;
     int converged = 0;
     double b_up = 0.0, b_low = 0.0;
+    uint8_t* active = shrink_window > 0 ? (uint8_t*)malloc((size_t)n) : NULL;
+    int64_t window_left = 0;                  /* updates left in the current window (R29) */
     for (;;) {
         int64_t u, l;
-        if (!oracle_select(f, y, alpha, C, n, &u, &l, &b_up, &b_low)) { converged = 1; break; }
-        if (b_low - b_up <= 2.0 * tol) { converged = 1; break; }
-        if (it == max_iter) break;
-        if (wss == 2) l = oracle_select_second_order(X, y, alpha, f, C, n, d, kernel, gamma, u);
+        if (!active || window_left == 0) {
+            /* every row: the selection, the stopping test, then (R29) the rows set aside */
+            if (!oracle_select(f, y, alpha, C, n, &u, &l, &b_up, &b_low)) { converged = 1; break; }
+            if (b_low - b_up <= 2.0 * tol) { converged = 1; break; }
+            if (it == max_iter) break;
+            if (active) { shrink_mark(f, y, alpha, C, n, b_up, b_low, active); window_left = shrink_window; }
+        } else {
+            /* inside a window: the active rows only; their convergence ends the window */
+            if (!select_active(f, y, alpha, C, n, active, &u, &l, &b_up, &b_low) || b_low - b_up <= 2.0 * tol) {
+                window_left = 0;
+                continue;
+            }
+            if (it == max_iter) break;
+        }
+        if (wss == 2) l = select_second_order_masked(X, y, alpha, f, C, n, d, kernel, gamma, u, active);
 
         const float* xu = X + u * d;
         const float* xl = X + l * d;
@@ -284,7 +363,9 @@ int oracle_svm_train_wss(const float* X, const int8_t* y, int64_t n, int64_t d, 
             f[j] = fma(cl, kl, fma(cu, ku, f[j]));
         }
         ++it;
+        if (active) --window_left;
     }
+    free(active);
     *b_out = -(b_up + b_low) / 2.0;
     *iters_out = it;
     *converged_out = converged;

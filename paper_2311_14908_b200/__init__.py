@@ -42,7 +42,8 @@ class Params(ctypes.Structure):
                 ("kernel", ctypes.c_int32), ("sv_epsilon", ctypes.c_double),
                 ("virtual_ranks", ctypes.c_int32), ("ctas", ctypes.c_int32),
                 ("iters_per_launch", ctypes.c_int64), ("gram", ctypes.c_int32), ("cache_rows", ctypes.c_int32),
-                ("cluster", ctypes.c_int32), ("wss", ctypes.c_int32)]
+                ("cluster", ctypes.c_int32), ("wss", ctypes.c_int32),
+                ("shrink_window", ctypes.c_int32), ("reserved1", ctypes.c_int32)]
 
 
 class Info(ctypes.Structure):

@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libsvmb200.so")
-SOURCES = ["svmb200.cu", "predict.cu", "comm.cu", "gram.cu", "gd.cu", "finalize.cu"]
+SOURCES = ["svmb200.cu", "predict.cu", "comm.cu", "gram.cu", "gd.cu", "finalize.cu", "shrink.cu"]
 HEADERS = ["smo_kernel.cuh", "smo_bincl.cuh", "svm_exp.cuh", "exp_table.inc", "svm_internal.h", "predict_tc.cuh"]
 
 

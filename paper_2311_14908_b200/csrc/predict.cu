@@ -8,6 +8,8 @@
 // ascending s -- the oracle's order, so decision values match it bit for bit.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "predict_tc.cuh"
 #include "svm_exp.cuh"
 #include "svm_internal.h"
@@ -100,7 +102,11 @@ int predict_device_tc(const float* X_sv, const double* coef, long long n_sv, lon
     k_pad_coef<<<256, 256, 0, st>>>(coef, n_sv, n_pad, cf);
     counted(3);
     const size_t smem = (size_t)STAGES * STAGE_BYTES;
-    auto fn = kernel == SVM_RBF ? k_predict_tc<1> : k_predict_tc<0>;
+    // the epilogue's exp (tuning switch SVMB200_PREDICT_EXP: 0 CUDA exp, 1 table, 2 polynomial)
+    int expv = 1;
+    if (const char* e = getenv("SVMB200_PREDICT_EXP")) expv = atoi(e);
+    auto fn = kernel != SVM_RBF ? k_predict_tc<0, 0>
+            : expv == 0 ? k_predict_tc<1, 0> : expv == 2 ? k_predict_tc<1, 2> : k_predict_tc<1, 1>;
     CKR(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     fn<<<(unsigned)(m_pad / BM), NTHREADS, smem, st>>>(pa, pb, qt, qs, cf, k_chunks, (int)(n_pad / BN), m, b,
                                                         gamma, dec);

@@ -116,7 +116,36 @@ __device__ __forceinline__ double exp_nonpos(double x, const double* __restrict_
     return __hiloint2double(__double2hiint(v) + (n >> 6) * (1 << 20), __double2loint(v));
 }
 
-template <int KERNEL>
+// the same by a degree-13 polynomial after reduction by ln 2 (no table; |r| <= ln 2 / 2,
+// truncation < 4e-17)
+__device__ __forceinline__ double exp_nonpos_poly(double x) {
+    if (x < -708.0) return 0.0;
+    const double sh = 6755399441055744.0;
+    const double kk = fma(x, 1.4426950408889634, sh);        // x / ln 2 + shift
+    const int n = __double2loint(kk);
+    const double nd = kk - sh;
+    double r = fma(nd, -0.693147180559663, x);               // ln 2, high part (41 bits, |nd| < 2^11:
+    r = fma(nd, -2.8235290563031577e-13, r);                 // exact product) and low part
+    double q = 1.0 / 6227020800.0;
+    q = fma(q, r, 1.0 / 479001600.0);
+    q = fma(q, r, 1.0 / 39916800.0);
+    q = fma(q, r, 1.0 / 3628800.0);
+    q = fma(q, r, 1.0 / 362880.0);
+    q = fma(q, r, 1.0 / 40320.0);
+    q = fma(q, r, 1.0 / 5040.0);
+    q = fma(q, r, 1.0 / 720.0);
+    q = fma(q, r, 1.0 / 120.0);
+    q = fma(q, r, 1.0 / 24.0);
+    q = fma(q, r, 1.0 / 6.0);
+    q = fma(q, r, 0.5);
+    q = fma(q, r, 1.0);
+    q = fma(q, r, 1.0);
+    // 2^n in two halves (n >= -1022 - 1 when x >= -708: the result stays normal)
+    return __hiloint2double(__double2hiint(q) + n * (1 << 20), __double2loint(q));
+}
+
+// EXPV: the epilogue's exp -- 0 CUDA's fp64 exp, 1 table-driven (exp_nonpos), 2 polynomial
+template <int KERNEL, int EXPV>
 __global__ void __launch_bounds__(NTHREADS, 1)
 k_predict_tc(const float* __restrict__ A,   // packed test rows [m_tiles][k_chunks][2][BM*BK]
              const float* __restrict__ B,   // packed SVs       [n_tiles][k_chunks][2][BN*BK]
@@ -238,7 +267,9 @@ k_predict_tc(const float* __restrict__ A,   // packed test rows [m_tiles][k_chun
                     double kv;
                     if (KERNEL == 1) {
                         const double dist = fmax(q_t + __ldg(&qs_t[c0 + j]) - 2.0 * dot, 0.0);
-                        kv = exp_nonpos(-gamma * dist, t64);
+                        if (EXPV == 0) kv = exp(-gamma * dist);
+                        else if (EXPV == 1) kv = exp_nonpos(-gamma * dist, t64);
+                        else kv = exp_nonpos_poly(-gamma * dist);
                     } else {
                         kv = dot;
                     }

@@ -112,6 +112,7 @@ struct Params {
     Ctl* ctl[MAXR];
     long long* trace;
     long long trace_cap;
+    double* hist;                  // optional [2 trace_cap]: (c_u, c_l) of every update (shrinking replay)
     unsigned long long* progress;  // host-mapped, may be null
     int check_interval;
     int state_cap;                 // rows per CTA the shared-memory state can hold
@@ -590,7 +591,7 @@ __device__ __forceinline__ void dict_rows(int kc, const unsigned char* stb, int 
 // BINCL: the kernel specialised for binary rows resident in a thread-block cluster (the
 // latency-bound small-problem path): the other modes compile out, so the per-iteration code
 // is short (instruction-cache resident).
-template <int KERNEL, int RPT, bool A_SMEM, bool BINCL, int NTC = NT>
+template <int KERNEL, int RPT, bool A_SMEM, bool BINCL, int NTC = NT, bool WSS2 = false>
 __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
     // NTC consumer threads (8 or 16 warps), then the scalar and the producer warp
     constexpr int NT_ = NTC, NWC_ = NTC / 32, SCALAR_ = NWC_, PRODUCER_ = NWC_ + 1;
@@ -602,7 +603,9 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
     const double* const m_gram = BINCL ? nullptr : P.gram;
     const int m_cache = BINCL ? 0 : P.cache_slots;
     const bool m_resident = BINCL || P.resident != 0;
-    const bool m_wss2 = !BINCL && P.wss == 2;               // second-order working set (NEXT-2)
+    constexpr bool m_wss2 = WSS2 && !BINCL;                 // second-order working set (NEXT-2):
+                                                            // its own instantiations, so the
+                                                            // first-order kernels carry no gain pass
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Shared& sh = *reinterpret_cast<Shared*>(smem_raw);
     size_t off = (sizeof(Shared) + 127) & ~size_t(127);
@@ -1350,6 +1353,7 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
                 }
                 if (P.trace && rank == 0 && cta == 0 && it < P.trace_cap) {
                     P.trace[2 * it] = u; P.trace[2 * it + 1] = l;
+                    if (P.hist) { P.hist[2 * it] = sh.cu; P.hist[2 * it + 1] = sh.cl; }
                 }
                 if (P.progress && rank == 0 && cta == 0 && (it % P.check_interval) == 0)
                     *(volatile unsigned long long*)P.progress = (unsigned long long)it;

@@ -60,6 +60,9 @@ struct SolveArgs {
     bool f_out_global = true;
     long long* trace = nullptr;                // host
     long long trace_cap = 0;
+    long long* trace_dev = nullptr;            // device pair trace + (c_u, c_l) history, written
+    double* hist_dev = nullptr;                //   by the kernel in place (window shrinking)
+    long long dev_cap = 0;
     cudaStream_t stream = nullptr;
     long long timeout_ns = 20ll * 1000 * 1000 * 1000;
     PreLaunchFn pre_launch = nullptr;
@@ -81,6 +84,15 @@ int validate_device(const float* X, const int8_t* y, long long n, long long d, c
 int device_limits(int* n_sm, int* max_smem);
 void pool_setup();
 int solve(SolveArgs& a);
+int train_device(const float* X, const int8_t* y, long long n, long long d, const svm_params& p,
+                 double* alpha, const double* alpha0, const double* f0, double* f_out,
+                 cudaMemcpyKind f_kind, long long* trace, long long trace_cap, cudaStream_t st,
+                 SolveOut& out, long long* trace_dev = nullptr, double* hist_dev = nullptr,
+                 long long dev_cap = 0);
+// shrink.cu: window shrinking (R29) around train_device, one rank
+int train_shrink(const float* X, const int8_t* y, long long n, long long d, const svm_params& p,
+                 double* alpha, const double* alpha0, const double* f0, double* f_out,
+                 long long* trace, long long trace_cap, cudaStream_t st, SolveOut& out);
 
 // gram.cu: K[i][j] for all i, j < n (fp64, row-major), same arithmetic as the row pass
 int gram_device(const float* X, long long n, long long d, int kernel, double gamma, double* K,

@@ -25,7 +25,7 @@
 using namespace svmk;
 
 namespace svmint {
-static_assert(sizeof(svm_params) == 80, "svm_params layout (binding and tests assume 80 bytes)");
+static_assert(sizeof(svm_params) == 88, "svm_params layout (binding and tests assume 88 bytes)");
 
 thread_local std::string g_err;
 thread_local long long g_launches = 0;
@@ -299,6 +299,7 @@ int check_params(long long n, long long d, const svm_params* p, svm_params* q) {
     if (q->virtual_ranks <= 1) q->virtual_ranks = 1;
     if (q->virtual_ranks > MAXR) return fail(SVM_EINVAL, "virtual_ranks > 8");
     if (q->wss <= 0) q->wss = 1;
+    if (q->shrink_window < 0) return fail(SVM_EINVAL, "shrink_window must be >= 0");
     if (q->wss > 2) return fail(SVM_EINVAL, "wss must be 1 (first order) or 2 (second order)");
     return SVM_OK;
 }
@@ -323,6 +324,9 @@ struct Plan {
     long long cta_stride = 0;
     size_t smem = 0;
 };
+
+// the solve being planned uses the second-order rule (its kernels have 256 consumer threads)
+static thread_local bool t_plan_wss2 = false;
 
 int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl, bool binary = false,
               bool gram = false, int cache_slots = 0, int cl_words = 0, const Plan* mix = nullptr) {
@@ -387,6 +391,7 @@ int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl, bool bina
         const int v = atoi(e);
         if (v == 256 || (v == 512 && cl_words == 0)) pl.ntc = v;
     }
+    if (t_plan_wss2) pl.ntc = NT;
     pl.rpt = pl.state_cap <= pl.ntc ? 1 : (pl.state_cap <= 2 * pl.ntc ? 2 : 4);
     if (const char* e = getenv("SVMB200_RPT")) {          // tuning override: 1, 2 or 4
         const int r = atoi(e);
@@ -475,7 +480,11 @@ int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl, bool bina
 typedef void (*KernelFn)(const Params);
 
 template <int K>
-KernelFn pick_rpt(int rpt, bool a_smem, int ntc) {
+KernelFn pick_rpt(int rpt, bool a_smem, int ntc, bool wss2 = false) {
+    if (wss2) {                                            // second-order selection: 256 consumers
+        if (a_smem) return rpt == 4 ? smo_persistent<K, 4, true, false, NT, true> : rpt == 2 ? smo_persistent<K, 2, true, false, NT, true> : smo_persistent<K, 1, true, false, NT, true>;
+        return rpt == 4 ? smo_persistent<K, 4, false, false, NT, true> : rpt == 2 ? smo_persistent<K, 2, false, false, NT, true> : smo_persistent<K, 1, false, false, NT, true>;
+    }
     if (ntc == 512) {
         if (a_smem) return rpt == 2 ? smo_persistent<K, 2, true, false, 512> : smo_persistent<K, 1, true, false, 512>;
         return rpt == 2 ? smo_persistent<K, 2, false, false, 512> : smo_persistent<K, 1, false, false, 512>;
@@ -487,12 +496,12 @@ KernelFn pick_rpt(int rpt, bool a_smem, int ntc) {
 KernelFn pick_bincl(int kernel) { return kernel == SVM_RBF ? smo_bincl<1> : smo_bincl<0>; }
 
 // bincl: binary rows resident in a cluster (the specialised kernel; rpt is 1 there)
-KernelFn pick_kernel(int kernel, int rpt, bool a_smem, bool bincl = false, int ntc = NT) {
+KernelFn pick_kernel(int kernel, int rpt, bool a_smem, bool bincl = false, int ntc = NT, bool wss2 = false) {
     if (bincl && getenv("SVMB200_NO_SPECIALISE") == nullptr) {
         if (kernel == SVM_RBF) return a_smem ? smo_persistent<1, 1, true, true> : smo_persistent<1, 1, false, true>;
         return a_smem ? smo_persistent<0, 1, true, true> : smo_persistent<0, 1, false, true>;
     }
-    return kernel == SVM_RBF ? pick_rpt<1>(rpt, a_smem, ntc) : pick_rpt<0>(rpt, a_smem, ntc);
+    return kernel == SVM_RBF ? pick_rpt<1>(rpt, a_smem, ntc, wss2) : pick_rpt<0>(rpt, a_smem, ntc, wss2);
 }
 
 int device_limits(int* n_sm, int* max_smem) {
@@ -510,6 +519,7 @@ int device_limits(int* n_sm, int* max_smem) {
 // single-process solve (world == nranks_here) all pointers are local.
 int solve(SolveArgs& a) {
     const svm_params& p = a.p;
+    t_plan_wss2 = (p.wss == 2);
     Plan pl;
     int rc = SVM_OK;
     bool binary = false;
@@ -728,7 +738,8 @@ int solve(SolveArgs& a) {
             return fail(SVM_EINVAL, "cluster mode needs every rank's rows resident in the cluster's shared memory");
     }
     KernelFn fn = pl.bincl ? pick_bincl(p.kernel)
-                           : pick_kernel(p.kernel, pl.rpt, pl.alpha_smem, pl.cluster > 0 && pl.bin_words > 0, pl.ntc);
+                           : pick_kernel(p.kernel, pl.rpt, pl.alpha_smem, pl.cluster > 0 && pl.bin_words > 0, pl.ntc,
+                                         p.wss == 2);
     const int nthreads = pl.bincl ? NTB : pl.ntc + 64;
     {
         const char* mode = gram ? "gram" : pl.bin_words ? "binary-resident"
@@ -898,6 +909,8 @@ int solve(SolveArgs& a) {
         if ((rc = dalloc((void**)&dtrace, (size_t)a.trace_cap * 16))) { release(); return rc; }
         CKR(cudaMemsetAsync(dtrace, 0xff, (size_t)a.trace_cap * 16, st));
         P.trace = dtrace; P.trace_cap = a.trace_cap;
+    } else if (a.trace_dev && a.dev_cap > 0) {
+        P.trace = a.trace_dev; P.hist = a.hist_dev; P.trace_cap = a.dev_cap;
     }
     if (want_timers) {
         unsigned long long* tm;
@@ -1017,11 +1030,15 @@ int solve(SolveArgs& a) {
 int train_device(const float* X, const int8_t* y, long long n, long long d, const svm_params& p,
                  double* alpha, const double* alpha0, const double* f0, double* f_out,
                  cudaMemcpyKind f_kind, long long* trace, long long trace_cap, cudaStream_t st,
-                 SolveOut& out) {
+                 SolveOut& out, long long* trace_dev, double* hist_dev, long long dev_cap) {
+    if (p.shrink_window > 0 && !trace_dev)
+        return train_shrink(X, y, n, d, p, alpha, alpha0, f0, f_kind == cudaMemcpyDeviceToDevice ? f_out : nullptr,
+                            trace, trace_cap, st, out);
     int n_sm = 0, max_smem = 0;
     int rc = device_limits(&n_sm, &max_smem);
     if (rc) return rc;
     const int vr = p.virtual_ranks;
+    if (p.shrink_window > 0 && vr > 1) return fail(SVM_EINVAL, "shrinking runs on one rank (virtual_ranks = 1)");
     int ctas = p.ctas > 0 ? p.ctas : n_sm;
     if (ctas > n_sm) ctas = n_sm;
     const int cpr = ctas / vr;
@@ -1046,6 +1063,7 @@ int train_device(const float* X, const int8_t* y, long long n, long long d, cons
     a.alpha0 = alpha0; a.f0 = f0;
     a.f_out = f_out; a.f_out_kind = f_kind; a.f_out_global = true;
     a.trace = trace; a.trace_cap = trace ? trace_cap : 0;
+    a.trace_dev = trace_dev; a.hist_dev = hist_dev; a.dev_cap = dev_cap;
     rc = solve(a);
     out = a.out;
     return rc;

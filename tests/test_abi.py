@@ -52,8 +52,8 @@ def test_library_is_sm100a(S):
 
 
 def test_struct_layouts_match_header(S):
-    # svm_params: 3 doubles, int64, int32, int32, double, int32, int32, int64, 4 x int32 = 80 bytes
-    assert ctypes.sizeof(S.Params) == 80
+    # svm_params: 3 doubles, int64, int32, int32, double, int32, int32, int64, 6 x int32 = 88 bytes
+    assert ctypes.sizeof(S.Params) == 88
     # svm_info: int64, 2 x int32, 4 doubles, 2 doubles, int64, 2 x int64, double = 96 bytes
     assert ctypes.sizeof(S.Info) == 96
     assert ctypes.sizeof(S.Debug) == 40

@@ -115,6 +115,23 @@ def test_w5_converged_state(w5):
     _converged(w5, 200)
 
 
+def test_w5_shrinking_segment(S, w5):
+    """Window shrinking at full size (reading R29), from the GPU's W5 snapshot at 10^5
+    steps (many multipliers at bounds, so most rows are set aside): three windows of 100
+    steps against the oracle with the same rule -- pairs, alpha and f (all 10^6 rows: the
+    replayed rows included) bit for bit."""
+    import torch
+    w, X, y, Xd, yd, snaps, final = w5
+    a0, f0 = snaps[100_000]
+    ref = O.train(X, y, w.C, w.kernel, w.gamma, w.tol, max_iter=300, alpha0=a0, f0=f0, trace_cap=300, shrink=100)
+    r = S.svm_train_dev(Xd, yd, w.C, w.kernel, w.gamma, w.tol, max_iter=300, alpha0=torch.from_numpy(a0).cuda(),
+                        f0=torch.from_numpy(f0).cuda(), want_f=True, trace_cap=300, shrink_window=100)
+    assert r["info"]["iterations"] == ref.iterations == 300
+    np.testing.assert_array_equal(r["trace"], ref.trace)
+    np.testing.assert_array_equal(r["alpha"].cpu().numpy(), ref.alpha)
+    np.testing.assert_array_equal(r["f"].cpu().numpy(), ref.f)
+
+
 @pytest.mark.parametrize("k", [10_000, 100_000, 132_900])
 def test_w4_segment_parity(S, w4, k):
     _segment(S, w4, k)

@@ -215,3 +215,94 @@ def test_second_order_selection_matches_libsvm(name, n):
     r1 = O.train(X, y, w.C, w.kernel, w.gamma, w.tol, wss=1)
     assert abs(O.dual_objective(X, y, r1.alpha, w.kernel, w.gamma) - w_or) <= 1e-6 * abs(w_or)
     assert 0.5 * clf.n_iter_[0] <= r.iterations <= 2.0 * clf.n_iter_[0]
+
+
+# ---------------------------------------------------------------- window shrinking (R29)
+def _rand_problem(seed):
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(8, 60))
+    d = int(rng.integers(1, 4))
+    X = rng.normal(size=(n, d)).astype(np.float32)
+    y = np.where(X[:, 0] + rng.normal(size=n) * 0.8 > 0, 1, -1).astype(np.int8)
+    y[0], y[1] = 1, -1
+    C = float(rng.choice([0.1, 1.0, 10.0]))
+    kern = int(rng.integers(0, 2))
+    return X, y, C, kern
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_shrinking_matches_brute_force_qp(seed):
+    """Window shrinking (R29) on tiny instances at tight tolerance reaches the brute-force
+    QP optimum (every (0 / C / free) pattern), for several window lengths."""
+    rng = np.random.default_rng(300 + seed)
+    n = int(rng.integers(4, 7))
+    X = (rng.standard_normal((n, 2)) * 1.5).astype(np.float32)
+    y = np.where(rng.random(n) < 0.5, 1, -1).astype(np.int8)
+    y[0], y[1] = 1, -1
+    kind = O.RBF if seed % 2 else O.LINEAR
+    gamma = 0.7 if kind == O.RBF else 0.0
+    C = float(rng.choice([0.5, 1.0, 5.0]))
+    K = np_gram(X, kind, gamma)
+    Wbf, _ = brute_force_qp(K, y, C)
+    for H in (1, 2, 5):
+        r = O.train(X, y, C, kind, gamma, tol=1e-10, max_iter=200000, shrink=H)
+        assert r.converged
+        assert np_W(r.alpha, y.astype(float), K) == pytest.approx(Wbf, rel=1e-11, abs=1e-12)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_shrinking_reaches_the_qp_optimum(seed):
+    """Window shrinking is a heuristic on the selection only: at tight tolerance it
+    reaches the optimum of the plain solve, every row satisfies KKT at tol' = 2 tau at the
+    end (the final stopping test is over all rows), and f is the exact incremental value
+    (equal to the from-scratch sum)."""
+    X, y, C, kern = _rand_problem(seed)
+    gamma = 0.5
+    r0 = O.train(X, y, C, kern, gamma, 1e-9, max_iter=2_000_000)
+    assert r0.converged
+    for H in (1, 3, 7):
+        r = O.train(X, y, C, kern, gamma, 1e-9, max_iter=2_000_000, shrink=H)
+        assert r.converged
+        W0 = O.dual_objective(X, y, r0.alpha, kern, gamma)
+        W1 = O.dual_objective(X, y, r.alpha, kern, gamma)
+        assert abs(W1 - W0) <= 1e-10 * max(1.0, abs(W0))
+        assert abs(np.dot(r.alpha, y.astype(float))) <= 1e-12 * max(1.0, C * len(y))
+        sv = r.alpha > 0
+        f_ref = O.decision(X[sv], (r.alpha * y)[sv], 0.0, kern, gamma, X) - y
+        np.testing.assert_allclose(r.f, f_ref, rtol=0, atol=1e-9 * max(1.0, C))
+        m = y * (r.f + y + r.b)
+        t2 = 2e-9
+        assert np.all(m[r.alpha == 0] >= 1 - t2 - 1e-9)
+        assert np.all(m[r.alpha == C] <= 1 + t2 + 1e-9)
+
+
+def test_shrinking_changes_the_selection_but_not_the_result():
+    """On these instances shrinking takes a different pair sequence (the rows set aside
+    are not selectable inside a window), and still converges (dual objective within the
+    tau-level of the plain solve)."""
+    changed = 0
+    for seed in (1, 2, 3):
+        X, y, C, kern = _rand_problem(seed)
+        r0 = O.train(X, y, C, kern, 0.5, 1e-3, trace_cap=100000)
+        r = O.train(X, y, C, kern, 0.5, 1e-3, trace_cap=100000, shrink=5)
+        changed += (r0.iterations != r.iterations) or not np.array_equal(r0.trace, r.trace)
+        W0 = O.dual_objective_from_f(r0.alpha, y, r0.f)
+        W1 = O.dual_objective_from_f(r.alpha, y, r.f)
+        assert abs(W1 - W0) <= 1e-2 * max(1.0, abs(W0))
+        assert r.converged and r.b_low - r.b_up <= 2e-3
+    assert changed >= 2
+
+
+def test_shrinking_equals_plain_solve_when_nothing_would_be_selected():
+    """When no row set aside would have been selected (the usual case on the workload
+    laws), the trajectory, alpha, f and b equal the plain solve's bit for bit -- the f of
+    the rows set aside is the exact incremental value."""
+    from gen import workloads as W
+    w = W.get("W5")
+    X, y = w.train(1500)
+    r0 = O.train(X, y, w.C, w.kernel, w.gamma, w.tol, trace_cap=100000)
+    r = O.train(X, y, w.C, w.kernel, w.gamma, w.tol, trace_cap=100000, shrink=50)
+    np.testing.assert_array_equal(r.trace, r0.trace)
+    np.testing.assert_array_equal(r.alpha, r0.alpha)
+    np.testing.assert_array_equal(r.f, r0.f)
+    assert r.b == r0.b

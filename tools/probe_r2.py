@@ -1,0 +1,76 @@
+"""Round-2 perf probe (one GPU): per-iteration times of the streamed configs, the tensor-core
+predict epilogue variants at the W5 scale, and window shrinking on the full solves.
+  python tools/probe_r2.py [what ...]   what: iters predict shrink5 shrink4"""
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2311_14908_b200 as S  # noqa: E402
+from gen import workloads as W  # noqa: E402
+
+what = sys.argv[1:] or ["iters", "predict", "shrink5"]
+
+
+def dev(name, n=None):
+    w = W.get(name)
+    X, y = w.train(n)
+    return w, torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+
+
+def timed(fn):
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(); r = fn(); e1.record(); torch.cuda.synchronize()
+    return r, e0.elapsed_time(e1) * 1e-3
+
+
+if "iters" in what:
+    for name, k in (("W3", 0), ("W4", 6000), ("W5", 1500)):
+        w, Xd, yd = dev(name)
+        kw = dict(max_iter=k) if k else {}
+        S.svm_train_dev(Xd, yd, w.C, w.kernel, w.gamma, w.tol, **kw)
+        r, t = timed(lambda: S.svm_train_dev(Xd, yd, w.C, w.kernel, w.gamma, w.tol, **kw))
+        print(json.dumps({"probe": "iters", "workload": name, "iterations": r["info"]["iterations"],
+                          "us_per_iter": 1e6 * r["info"]["seconds_solve"] / r["info"]["iterations"],
+                          "plan": S.last_plan()}), flush=True)
+        del Xd, yd
+        torch.cuda.empty_cache()
+
+if "predict" in what:
+    w, Xd, yd = dev("W5")
+    nsv = 284_028
+    rng = np.random.default_rng(5)
+    coef = torch.from_numpy(rng.uniform(-1, 1, nsv)).cuda()
+    Xsv = Xd[:nsv].contiguous()
+    Xt, _ = w.test()
+    Xt = torch.from_numpy(Xt).cuda()
+    for v in ("0", "1", "2"):
+        os.environ["SVMB200_PREDICT_EXP"] = v
+        S.svm_predict_dev(Xsv, coef, 0.1, w.kernel, w.gamma, Xt[:4096], mode=1)
+        dec, t = timed(lambda: S.svm_predict_dev(Xsv, coef, 0.1, w.kernel, w.gamma, Xt, mode=1))
+        if v == "0":
+            ref = dec.clone()
+        print(json.dumps({"probe": "predict", "exp_variant": int(v), "rows": Xt.shape[0], "n_sv": nsv, "seconds": t,
+                          "tflops_algorithmic": 2.0 * Xt.shape[0] * nsv * 256 / t / 1e12,
+                          "max_diff_vs_variant0": float((dec - ref).abs().max())}), flush=True)
+    os.environ.pop("SVMB200_PREDICT_EXP")
+    del Xd, yd, Xt, Xsv
+    torch.cuda.empty_cache()
+
+for tag, name in (("shrink5", "W5"), ("shrink4", "W4")):
+    if tag not in what:
+        continue
+    w, Xd, yd = dev(name)
+    for H in (0, 1000):
+        r, t = timed(lambda: S.svm_train_dev(Xd, yd, w.C, w.kernel, w.gamma, w.tol, shrink_window=H))
+        print(json.dumps({"probe": "shrink", "workload": name, "H": H, "time_to_converge_s": t,
+                          "iterations": r["info"]["iterations"], "converged": r["info"]["converged"],
+                          "b": r["b"], "n_sv": r["info"]["n_sv"], "W": r["info"]["dual_objective"],
+                          "launches": r["info"]["launches"]}), flush=True)
+    del Xd, yd
+    torch.cuda.empty_cache()
