@@ -103,7 +103,7 @@ int predict_device_tc(const float* X_sv, const double* coef, long long n_sv, lon
     counted(3);
     const size_t smem = (size_t)STAGES * STAGE_BYTES;
     // the epilogue's exp (tuning switch SVMB200_PREDICT_EXP: 0 CUDA exp, 1 table, 2 polynomial)
-    int expv = 1;
+    int expv = 0;            // (measured: all three equal at the W5 scale -- the exp does not bound it)
     if (const char* e = getenv("SVMB200_PREDICT_EXP")) expv = atoi(e);
     auto fn = kernel != SVM_RBF ? k_predict_tc<0, 0>
             : expv == 0 ? k_predict_tc<1, 0> : expv == 2 ? k_predict_tc<1, 2> : k_predict_tc<1, 1>;

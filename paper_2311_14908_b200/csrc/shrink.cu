@@ -20,6 +20,8 @@
 
 #include <climits>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -283,6 +285,104 @@ k_replay(const float* __restrict__ X, int d, const long long* __restrict__ rows,
     if (t < nrows) f[rows[r0 + t]] = fr;
 }
 
+// Replay, rows resident (d_pad <= 256, the HBM-bound configs): a CTA owns R2 = 64 rows,
+// held in shared memory as fp64 for the whole window; the window's steps are taken 32 at a
+// time (64 pivot rows, staged per feature chunk).  Thread (warp w, lane): rows lane and
+// lane + 32, pivots 8 w .. 8 w + 7 -- 16 independent R13 chains, 2 row loads and 4
+// broadcast pivot loads per feature.  Same arithmetic as k_replay.
+constexpr int R2 = 64, S2 = 32, P2 = 2 * S2, D2 = 64, D2MAX = 256;
+constexpr size_t REPLAY2_SMEM = sizeof(double) * ((size_t)D2MAX * R2 + (size_t)D2 * P2 + (size_t)P2 * (R2 + 1) + 96);
+
+template <int KERNEL>
+__global__ void __launch_bounds__(RT, 1)
+k_replay_res(const float* __restrict__ X, int d, const long long* __restrict__ rows, long long nr,
+             const long long* __restrict__ tg, const double* __restrict__ hist, long long k,
+             double gamma, double* __restrict__ f) {
+    extern __shared__ __align__(16) double rsm[];
+    const int dpad = (d + D2 - 1) / D2 * D2;
+    double (*xs)[R2] = reinterpret_cast<double (*)[R2]>(rsm);                                 // [dpad][R2]
+    double (*ps)[P2] = reinterpret_cast<double (*)[P2]>(rsm + (size_t)D2MAX * R2);             // [D2][P2]
+    double (*kv)[R2 + 1] = reinterpret_cast<double (*)[R2 + 1]>(rsm + (size_t)D2MAX * R2 + D2 * P2);  // [P2][R2+1]
+    double* tab = rsm + (size_t)D2MAX * R2 + D2 * P2 + P2 * (R2 + 1);
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    for (int e = t; e < svmexp::EXP_TABLE_DOUBLES; e += RT) tab[e] = svmexp::table_entry(e);
+    const svmexp::PtrTab T{tab};
+    const long long r0 = (long long)blockIdx.x * R2;
+    const int nrows = (int)((nr - r0) < R2 ? (nr - r0) : R2);
+    // the CTA's rows, once: fp32 -> fp64, feature-major, zero padded
+    for (int e = t; e < dpad * R2; e += RT) {
+        const int rr = e / dpad, kk = e - rr * dpad;
+        float v = 0.0f;
+        if (rr < nrows && kk < d) v = X[rows[r0 + rr] * (long long)d + kk];
+        xs[kk][rr] = (double)v;
+    }
+    double fr = 0.0;
+    if (t < nrows) fr = f[rows[r0 + t]];
+    for (long long h0 = 0; h0 < k; h0 += S2) {
+        const int ns = (int)((k - h0) < S2 ? (k - h0) : S2);
+        double acc[2][8];
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+#pragma unroll
+            for (int p = 0; p < 8; ++p) acc[q][p] = 0.0;
+        for (int k0 = 0; k0 < dpad; k0 += D2) {
+            __syncthreads();
+            for (int e = t; e < D2 * P2; e += RT) {
+                const int pp = e / D2, kk = e - pp * D2;
+                float v = 0.0f;
+                if ((pp >> 1) < ns && k0 + kk < d) v = X[tg[2 * (h0 + (pp >> 1)) + (pp & 1)] * (long long)d + k0 + kk];
+                ps[kk][pp] = (double)v;
+            }
+            __syncthreads();
+#pragma unroll 2
+            for (int kk = 0; kk < D2; ++kk) {
+                const double x0 = xs[k0 + kk][lane], x1 = xs[k0 + kk][lane + 32];
+                const double2* pr = reinterpret_cast<const double2*>(&ps[kk][8 * warp]);
+                double pv[8];
+#pragma unroll
+                for (int p = 0; p < 4; ++p) { const double2 v2 = pr[p]; pv[2 * p] = v2.x; pv[2 * p + 1] = v2.y; }
+#pragma unroll
+                for (int p = 0; p < 8; ++p) {
+                    if (KERNEL == 1) {
+                        const double e0 = x0 - pv[p]; acc[0][p] = fma(e0, e0, acc[0][p]);
+                        const double e1 = x1 - pv[p]; acc[1][p] = fma(e1, e1, acc[1][p]);
+                    } else {
+                        acc[0][p] = fma(x0, pv[p], acc[0][p]);
+                        acc[1][p] = fma(x1, pv[p], acc[1][p]);
+                    }
+                }
+            }
+        }
+        // kernel values: all fast phases first (independent), the rare slow ones after
+        bool safe[2][8];
+        bool all_safe = true;
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+#pragma unroll
+            for (int p = 0; p < 8; ++p) {
+                double kvv = acc[q][p];
+                safe[q][p] = true;
+                if (KERNEL == 1) { kvv = svmexp::exp_cr_fast(-(gamma * acc[q][p]), T, safe[q][p]); all_safe = all_safe && safe[q][p]; }
+                kv[8 * warp + p][lane + 32 * q] = kvv;
+            }
+        if (KERNEL == 1 && !all_safe) {
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+#pragma unroll
+                for (int p = 0; p < 8; ++p)
+                    if (!safe[q][p]) kv[8 * warp + p][lane + 32 * q] = svmexp::exp_cr_slow(-(gamma * acc[q][p]), T);
+        }
+        __syncthreads();
+        if (t < nrows) {
+            for (int s2 = 0; s2 < ns; ++s2) {
+                const double cu = hist[2 * (h0 + s2)], cl = hist[2 * (h0 + s2) + 1];
+                fr = fma(cl, kv[2 * s2 + 1][t], fma(cu, kv[2 * s2][t], fr));
+            }
+        }
+    }
+    if (t < nrows) f[rows[r0 + t]] = fr;
+}
+
 }  // namespace svmint
 
 using namespace svmint;
@@ -316,6 +416,26 @@ int train_shrink(const float* X, const int8_t* y, long long n, long long d, cons
     };
     auto release = [&]() { for (void* q : owned) cudaFreeAsync(q, st); owned.clear(); };
     int rc = SVM_OK;
+    // every window allocates the sub-problem's blocked copy of X (up to |X|) from the pool:
+    // keep all of it cached for the solve (a release at the 2 GiB default threshold would
+    // re-map GBs per window -- measured 0.3-0.9 s spikes), restore the threshold after
+    cudaMemPool_t pool = nullptr;
+    unsigned long long thr_old = 0;
+    {
+        int dev = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr_old);
+            unsigned long long keep = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        } else {
+            pool = nullptr;
+        }
+        cudaGetLastError();
+    }
+    struct PoolRestore {
+        cudaMemPool_t p; unsigned long long t;
+        ~PoolRestore() { if (p) cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &t); }
+    } pool_restore{pool, thr_old};
     double* f; double* aa; double* fa; float* Xa; int8_t* ya; uint8_t* act;
     long long *idx, *oidx, *trs, *tg; double* hist; SelPart* part; SelOut* so;
     unsigned long long *cnt, *icnt;
@@ -344,6 +464,8 @@ int train_shrink(const float* X, const int8_t* y, long long n, long long d, cons
     double b_up = 0.0, b_low = 0.0;
     SolveOut so_last;
     long long hits = 0, misses = 0;
+    bool plain_rows = false;
+    const bool slog = getenv("SVMB200_SHRINK_LOG") != nullptr;     // per-window timing (diagnostic)
     for (;;) {
         // ---- window start: the selection over every row and the stopping test
         k_sel_part<<<SEL_BLOCKS, SEL_THREADS, 0, st>>>(f, y, alpha, n, p.C, part);
@@ -376,9 +498,14 @@ int train_shrink(const float* X, const int8_t* y, long long n, long long d, cons
         q.iters_per_launch = 0;
         q.cluster = -1;
         q.shrink_window = 0;
+        if (q.cache_rows == 0) q.cache_rows = -1;     // (auto cache: decided for the whole problem, off here)
         SolveOut o;
+        cudaEvent_t w0 = nullptr, w1 = nullptr, w2 = nullptr;
+        if (slog) { cudaEventCreate(&w0); cudaEventCreate(&w1); cudaEventCreate(&w2); cudaEventRecord(w0, st); }
         rc = train_device(Xa, ya, na, d, q, aa, aa, fa, fa, cudaMemcpyDeviceToDevice, nullptr, 0, st, o,
-                          trs, hist, H);
+                          trs, hist, H, plain_rows);
+        plain_rows = plain_rows || o.plain_rows;      // an fp32-row problem stays one: skip the probes
+        if (slog) cudaEventRecord(w1, st);
         if (rc) { release(); return rc; }
         launches += o.launches;
         solve_s += o.seconds_solve;
@@ -392,7 +519,16 @@ int train_shrink(const float* X, const int8_t* y, long long n, long long d, cons
             if (ni > 0) {
                 const unsigned grid = (unsigned)((ni + RB - 1) / RB);
                 static_assert(svmexp::EXP_TABLE_DOUBLES == 96, "replay table size");
-                if (p.kernel == SVM_RBF) {
+                if (d <= D2MAX && getenv("SVMB200_REPLAY_V1") == nullptr) {
+                    const unsigned g2 = (unsigned)((ni + R2 - 1) / R2);
+                    if (p.kernel == SVM_RBF) {
+                        CKR(cudaFuncSetAttribute((const void*)k_replay_res<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)REPLAY2_SMEM));
+                        k_replay_res<1><<<g2, RT, REPLAY2_SMEM, st>>>(X, (int)d, oidx, ni, tg, hist, kk, p.gamma, f);
+                    } else {
+                        CKR(cudaFuncSetAttribute((const void*)k_replay_res<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)REPLAY2_SMEM));
+                        k_replay_res<0><<<g2, RT, REPLAY2_SMEM, st>>>(X, (int)d, oidx, ni, tg, hist, kk, p.gamma, f);
+                    }
+                } else if (p.kernel == SVM_RBF) {
                     CKR(cudaFuncSetAttribute((const void*)k_replay<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)REPLAY_SMEM));
                     k_replay<1><<<grid, RT, REPLAY_SMEM, st>>>(X, (int)d, oidx, ni, tg, hist, kk, p.gamma, f);
                 } else {
@@ -407,6 +543,16 @@ int train_shrink(const float* X, const int8_t* y, long long n, long long d, cons
             }
         }
         CKR(cudaGetLastError());
+        if (slog) {
+            cudaEventRecord(w2, st);
+            cudaEventSynchronize(w2);
+            float ms_s = 0.f, ms_r = 0.f;
+            cudaEventElapsedTime(&ms_s, w0, w1);
+            cudaEventElapsedTime(&ms_r, w1, w2);
+            fprintf(stderr, "[svmb200 shrink] it=%lld window=%lld active=%lld aside=%lld solve_ms=%.2f replay_ms=%.2f\n",
+                    it, kk, na, ni, ms_s, ms_r);
+            cudaEventDestroy(w0); cudaEventDestroy(w1); cudaEventDestroy(w2);
+        }
         it += kk;
         if (o.state == ST_MAXITER && kk == remaining && remaining < H) {
             // the run's max_iter inside the window: the active rows' selection stands

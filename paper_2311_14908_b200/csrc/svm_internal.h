@@ -33,6 +33,7 @@ struct SolveOut {
     long long launches = 0;
     long long cache_hits = 0, cache_misses = 0;
     bool gram = false;
+    bool plain_rows = false;                   // the solve streamed plain fp32 rows (no encoding)
 };
 
 struct SolveArgs;
@@ -63,6 +64,7 @@ struct SolveArgs {
     long long* trace_dev = nullptr;            // device pair trace + (c_u, c_l) history, written
     double* hist_dev = nullptr;                //   by the kernel in place (window shrinking)
     long long dev_cap = 0;
+    bool skip_detect = false;                  // plain fp32 rows without probing X for encodings
     cudaStream_t stream = nullptr;
     long long timeout_ns = 20ll * 1000 * 1000 * 1000;
     PreLaunchFn pre_launch = nullptr;
@@ -88,7 +90,7 @@ int train_device(const float* X, const int8_t* y, long long n, long long d, cons
                  double* alpha, const double* alpha0, const double* f0, double* f_out,
                  cudaMemcpyKind f_kind, long long* trace, long long trace_cap, cudaStream_t st,
                  SolveOut& out, long long* trace_dev = nullptr, double* hist_dev = nullptr,
-                 long long dev_cap = 0);
+                 long long dev_cap = 0, bool skip_detect = false);
 // shrink.cu: window shrinking (R29) around train_device, one rank
 int train_shrink(const float* X, const int8_t* y, long long n, long long d, const svm_params& p,
                  double* alpha, const double* alpha0, const double* f0, double* f_out,

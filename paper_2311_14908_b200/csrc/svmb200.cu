@@ -524,7 +524,7 @@ int solve(SolveArgs& a) {
     int rc = SVM_OK;
     bool binary = false;
     // (wss 2 runs on fp32 / dictionary / mixed rows: the resident bit-row loop has no gain pass)
-    if (!a.independent && p.wss != 2 && getenv("SVMB200_NO_BINARY") == nullptr && a.d <= 1024) {
+    if (!a.independent && !a.skip_detect && p.wss != 2 && getenv("SVMB200_NO_BINARY") == nullptr && a.d <= 1024) {
         unsigned long long* dc = nullptr;
         CKR(cudaMallocAsync(&dc, 8, a.stream));
         CKR(cudaMemsetAsync(dc, 0, 8, a.stream));
@@ -571,7 +571,7 @@ int solve(SolveArgs& a) {
         // them, at most MIX_MAXSEG runs of the column order)
         Plan mix;
         std::vector<int> mix_map;
-        if (!a.independent && getenv("SVMB200_NO_MIXED") == nullptr && a.d >= 32) {
+        if (!a.independent && !a.skip_detect && getenv("SVMB200_NO_MIXED") == nullptr && a.d >= 32) {
             int* dnb = nullptr;
             CKR(cudaMallocAsync(&dnb, (size_t)a.d * 4, a.stream));
             CKR(cudaMemsetAsync(dnb, 0, (size_t)a.d * 4, a.stream));
@@ -606,7 +606,7 @@ int solve(SolveArgs& a) {
         std::vector<double> dict_vals;
         std::vector<unsigned char> dict_code((size_t)DICT_SLOTS, 0);
         std::vector<unsigned> dict_keys((size_t)DICT_SLOTS, DICT_EMPTY);
-        if (!a.independent && getenv("SVMB200_NO_DICT") == nullptr && a.d >= 8 &&
+        if (!a.independent && !a.skip_detect && getenv("SVMB200_NO_DICT") == nullptr && a.d >= 8 &&
             (mix.mix_nseg == 0 || a.d < 4 * (mix.mix_nc + mix.mix_nbw))) {
             unsigned* dk = nullptr;
             int* dcnt = nullptr;
@@ -1016,6 +1016,7 @@ int solve(SolveArgs& a) {
     CKR(cudaStreamSynchronize(st));
     if (progress_h) cudaFreeHost(progress_h);
     a.out.gram = gram != nullptr;
+    a.out.plain_rows = !gram && pl.bin_words == 0 && pl.mix_nseg == 0 && pl.esz == 4;
     for (int r = a.rank_base; r < a.rank_base + a.nranks_here; ++r) {
         if (hcr[r].state == ST_TIMEOUT) return fail(SVM_ETIMEOUT, "device wait for the candidate exchange timed out");
         if (hcr[r].state != ST_CONVERGED && hcr[r].state != ST_MAXITER)
@@ -1030,10 +1031,12 @@ int solve(SolveArgs& a) {
 int train_device(const float* X, const int8_t* y, long long n, long long d, const svm_params& p,
                  double* alpha, const double* alpha0, const double* f0, double* f_out,
                  cudaMemcpyKind f_kind, long long* trace, long long trace_cap, cudaStream_t st,
-                 SolveOut& out, long long* trace_dev, double* hist_dev, long long dev_cap) {
-    if (p.shrink_window > 0 && !trace_dev)
+                 SolveOut& out, long long* trace_dev, double* hist_dev, long long dev_cap, bool skip_detect) {
+    if (p.shrink_window > 0 && !trace_dev) {
+        if (p.virtual_ranks > 1) return fail(SVM_EINVAL, "shrinking runs on one rank (virtual_ranks = 1)");
         return train_shrink(X, y, n, d, p, alpha, alpha0, f0, f_kind == cudaMemcpyDeviceToDevice ? f_out : nullptr,
                             trace, trace_cap, st, out);
+    }
     int n_sm = 0, max_smem = 0;
     int rc = device_limits(&n_sm, &max_smem);
     if (rc) return rc;
@@ -1064,6 +1067,7 @@ int train_device(const float* X, const int8_t* y, long long n, long long d, cons
     a.f_out = f_out; a.f_out_kind = f_kind; a.f_out_global = true;
     a.trace = trace; a.trace_cap = trace ? trace_cap : 0;
     a.trace_dev = trace_dev; a.hist_dev = hist_dev; a.dev_cap = dev_cap;
+    a.skip_detect = skip_detect;
     rc = solve(a);
     out = a.out;
     return rc;
