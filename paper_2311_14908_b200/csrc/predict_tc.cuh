@@ -247,22 +247,22 @@ k_predict_tc(const float* __restrict__ A,   // packed test rows [m_tiles][k_chun
             const double* qs_t = qs + (size_t)nt * BN;
             const double* cf_t = cf + (size_t)nt * BN;
 #pragma unroll 1
-            for (int c0 = half * (BN / NPART); c0 < (half + 1) * (BN / NPART); c0 += 32) {
-                uint32_t v[32];
+            for (int c0 = half * (BN / NPART); c0 < (half + 1) * (BN / NPART); c0 += 16) {
+                // 16 accumulator columns per load (x16)
+                uint32_t v[16];
                 const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN + c0;
                 asm volatile(
-                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-                    "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+                    "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
                       "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-                      "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),
-                      "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),
-                      "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                      "=r"(v[14]), "=r"(v[15])
                     : "r"(taddr));
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll 8
-                for (int j = 0; j < 32; ++j) {
+                // fully unrolled: v[j] must index registers (a partial unroll put v in local
+                // memory -- STL/LDL per element)
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
                     const double dot = (double)__uint_as_float(v[j]);
                     double kv;
                     if (KERNEL == 1) {
