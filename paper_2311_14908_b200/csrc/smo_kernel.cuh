@@ -166,6 +166,10 @@ struct Params {
     // pass over K(x_u, .), K(x_l, .).
     int wss;
     const double* qself;           // wss 2, linear kernel: x_t . x_t of every global row (R13 order)
+    int l2_prefetch;               // streamed X: the producer also prefetches into L2 the stage
+                                   // l2_prefetch stages beyond the ring (cp.async.bulk.prefetch.L2),
+                                   // so HBM keeps streaming while the ring is full -- during the
+                                   // exchange, when the consumers wait (0 = off)
     int l2_keep_chunks;            // streamed X: the first l2_keep_chunks stages (tile-major) of
                                    // every CTA block are copied with an L2 evict_last policy, the
                                    // rest evict_first, so that part of X stays in L2 across
@@ -226,6 +230,9 @@ __device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32
                                               uint64_t policy) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
                  :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy) : "memory");
+}
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ uint64_t l2_policy(bool keep) {
     uint64_t p;
@@ -717,6 +724,12 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
             bool wrapped = false;
             const uint64_t pol_keep = l2_policy(true), pol_stream = l2_policy(false);
             int tile = 0, chunk = 0;
+            // L2 prefetch cursor: l2_prefetch stages beyond the copy cursor plus the ring
+            const int pf_ahead = P.l2_prefetch > 0 ? P.l2_prefetch + P.stages : 0;
+            int ptile = 0, pchunk = 0;
+            for (int q = 0; q < pf_ahead; ++q) {
+                if (++pchunk == P.n_chunks) { pchunk = 0; if (++ptile == n_tiles) ptile = 0; }
+            }
             for (;;) {
                 if (wrapped) {
                     while (!mbar_try_wait(&empty[slot], par ^ 1u)) {
@@ -735,6 +748,13 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
                                   tile * P.n_chunks + chunk < P.l2_keep_chunks ? pol_keep : pol_stream);
                 else
                     bulk_g2s(dst, src, bytes, &full[slot]);
+                if (pf_ahead > 0) {
+                    const int prows = min(P.rt, R - ptile * P.rt);
+                    const int prp = (prows + 3) & ~3;
+                    const unsigned char* psrc = xcta_b + ((long long)ptile * P.d_pad * P.rt + (long long)pchunk * P.kc * prp) * esz;
+                    bulk_prefetch_l2(psrc, (uint32_t)P.kc * prp * (uint32_t)esz);
+                    if (++pchunk == P.n_chunks) { pchunk = 0; if (++ptile == n_tiles) ptile = 0; }
+                }
                 ++s;
                 sh.issued = s;
                 if (++slot == (unsigned)P.stages) { slot = 0; par ^= 1u; wrapped = true; }

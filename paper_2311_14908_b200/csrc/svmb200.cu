@@ -818,6 +818,8 @@ int solve(SolveArgs& a) {
         const long long stage_bytes = (long long)pl.kc * pl.rt * 4;
         const long long ctas_here = (long long)a.ctas_per_rank * a.nranks_here;
         if (keep_mb > 0 && stage_bytes > 0) P.l2_keep_chunks = (int)((keep_mb << 20) / (stage_bytes * ctas_here));
+        // L2 prefetch beyond the ring (tuning switch SVMB200_L2_PF, stages; default 0)
+        if (const char* e = getenv("SVMB200_L2_PF")) P.l2_prefetch = atoi(e);
     }
     P.sys_scope = a.mbox_local_alloc ? 0 : 1;
     const bool want_timers = getenv("SVMB200_PHASE_TIMERS") != nullptr;

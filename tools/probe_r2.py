@@ -74,3 +74,41 @@ for tag, name in (("shrink5", "W5"), ("shrink4", "W4")):
                           "launches": r["info"]["launches"]}), flush=True)
     del Xd, yd
     torch.cuda.empty_cache()
+
+if "wss5" in what:
+    # the second-order rule on W5 (report both rules on the bench config)
+    w, Xd, yd = dev("W5")
+    for wss in (1, 2):
+        r, t = timed(lambda: S.svm_train_dev(Xd, yd, w.C, w.kernel, w.gamma, w.tol, wss=wss))
+        print(json.dumps({"probe": "wss", "workload": "W5", "wss": wss, "time_to_converge_s": t,
+                          "iterations": r["info"]["iterations"], "us_per_iter": 1e6 * t / r["info"]["iterations"],
+                          "b": r["b"], "n_sv": r["info"]["n_sv"], "W": r["info"]["dual_objective"]}), flush=True)
+    del Xd, yd
+    torch.cuda.empty_cache()
+
+if "cache4" in what:
+    # the kernel-row cache on W4 (auto-off for n > 200k: replayed LRU hit rate ~11%)
+    w, Xd, yd = dev("W4")
+    for slots in (-1, 2048):
+        r, t = timed(lambda: S.svm_train_dev(Xd, yd, w.C, w.kernel, w.gamma, w.tol, cache_rows=slots))
+        print(json.dumps({"probe": "cache", "workload": "W4", "cache_rows": slots, "time_to_converge_s": t,
+                          "iterations": r["info"]["iterations"], "cache_hits": r["info"]["cache_hits"],
+                          "cache_misses": r["info"]["cache_misses"], "plan": S.last_plan()}), flush=True)
+    del Xd, yd
+    torch.cuda.empty_cache()
+
+if "pf5" in what:
+    # L2 prefetch beyond the ring x L2 keep window, W5 prefix (SVMB200_L2_PF / _L2_KEEP_MB)
+    w, Xd, yd = dev("W5")
+    for pf, keep in (("0", "48"), ("2", "48"), ("4", "48"), ("4", "16"), ("6", "0"), ("8", "0"), ("0", "48")):
+        os.environ["SVMB200_L2_PF"] = pf
+        os.environ["SVMB200_L2_KEEP_MB"] = keep
+        S.svm_train_dev(Xd, yd, w.C, w.kernel, w.gamma, w.tol, max_iter=200)
+        ts = []
+        for rep in range(2):
+            r, t = timed(lambda: S.svm_train_dev(Xd, yd, w.C, w.kernel, w.gamma, w.tol, max_iter=2000))
+            ts.append(1e6 * r["info"]["seconds_solve"] / r["info"]["iterations"])
+        print(json.dumps({"probe": "l2pf", "workload": "W5", "pf": int(pf), "keep_mb": int(keep), "us_per_iter": ts}), flush=True)
+    os.environ.pop("SVMB200_L2_PF"); os.environ.pop("SVMB200_L2_KEEP_MB")
+    del Xd, yd
+    torch.cuda.empty_cache()
