@@ -72,6 +72,11 @@ __global__ void __launch_bounds__(TI) k_predict_exact(const float* __restrict__ 
     if (i < m) dec[i] = acc + b;
 }
 
+__global__ void k_scale_norms(double* __restrict__ q, long long n, double s) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        q[i] = s * q[i];
+}
+
 __global__ void k_pad_coef(const double* __restrict__ coef, long long n, long long n_pad, double* __restrict__ out) {
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad; i += (long long)gridDim.x * blockDim.x)
         out[i] = i < n ? coef[i] : 0.0;
@@ -101,6 +106,10 @@ int predict_device_tc(const float* X_sv, const double* coef, long long n_sv, lon
     k_pack_3xtf32<<<1184, 256, 0, st>>>(X_sv, n_sv, (int)d, k_chunks, n_pad, pb, qs);
     k_pad_coef<<<256, 256, 0, st>>>(coef, n_sv, n_pad, cf);
     counted(3);
+    if (kernel == SVM_RBF) {                       // the epilogue takes -gamma |s|^2 per SV
+        k_scale_norms<<<256, 256, 0, st>>>(qs, n_pad, -gamma);
+        counted();
+    }
     const size_t smem = (size_t)STAGES * STAGE_BYTES;
     // the epilogue's exp (tuning switch SVMB200_PREDICT_EXP: 0 CUDA exp, 1 table, 2 polynomial)
     int expv = 0;            // (measured: all three equal at the W5 scale -- the exp does not bound it)

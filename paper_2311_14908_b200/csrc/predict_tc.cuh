@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 k_predict_tc(const float* __restrict__ A,   // packed test rows [m_tiles][k_chunks][2][BM*BK]
              const float* __restrict__ B,   // packed SVs       [n_tiles][k_chunks][2][BN*BK]
              const double* __restrict__ qt, // |t_i|^2 [m_pad]
-             const double* __restrict__ qs, // |s|^2   [n_pad]
+             const double* __restrict__ qs, // RBF: -gamma |s|^2 [n_pad] (unused for linear)
              const double* __restrict__ cf, // coef    [n_pad] (0 for padding)
              int k_chunks, int n_tiles, long long m, double b, double gamma,
              double* __restrict__ dec) {
@@ -238,7 +238,12 @@ k_predict_tc(const float* __restrict__ A,   // packed test rows [m_tiles][k_chun
         const int half = (warp - 2) >> 2;                 // column part
         const int row = quarter * 32 + lane;
         const long long gi = (long long)mt * BM + row;
+        // x = -gamma (|t|^2 + |s|^2 - 2 t.s) = (a_t + b_s) + 2 gamma (t.s), a_t = -gamma |t|^2,
+        // b_s = -gamma |s|^2 (precomputed per SV, qs holds b_s for RBF): two fp64 operations
+        // per (row, SV) instead of four -- they share the pipe with the tensor cores
         const double q_t = qt[(long long)mt * BM + row];
+        const double a_t = -gamma * q_t;
+        const double g2 = 2.0 * gamma;
         double acc_d = 0.0;
         for (int nt = 0; nt < n_tiles; ++nt) {
             const int acc = nt & 1;
@@ -266,10 +271,10 @@ k_predict_tc(const float* __restrict__ A,   // packed test rows [m_tiles][k_chun
                     const double dot = (double)__uint_as_float(v[j]);
                     double kv;
                     if (KERNEL == 1) {
-                        const double dist = fmax(q_t + __ldg(&qs_t[c0 + j]) - 2.0 * dot, 0.0);
-                        if (EXPV == 0) kv = exp(-gamma * dist);
-                        else if (EXPV == 1) kv = exp_nonpos(-gamma * dist, t64);
-                        else kv = exp_nonpos_poly(-gamma * dist);
+                        const double x = fmin(fma(g2, dot, a_t + __ldg(&qs_t[c0 + j])), 0.0);
+                        if (EXPV == 0) kv = exp(x);
+                        else if (EXPV == 1) kv = exp_nonpos(x, t64);
+                        else kv = exp_nonpos_poly(x);
                     } else {
                         kv = dot;
                     }
