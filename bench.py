@@ -47,7 +47,7 @@ METRIC = "SVM train time-to-converge (s) & SMO iters/s at 1/2/4/8 B200; kernel-r
 # Iteration counts of the deterministic trajectories (the oracle and the GPU
 # take the same steps).  Used only to size the windows of a step; if a solve takes a
 # different count, the number of launches (reported as `launches`) differs from K.
-PLAN_ITERS = {"W2": 42790, "W3": 11659, "W4": 133952, "W5": 411469}
+PLAN_ITERS = {"W1": 150, "W2": 42790, "W3": 11659, "W4": 133952, "W5": 411469}
 WINDOWED = ("W4", "W5")
 
 
@@ -204,10 +204,20 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook (SVMB200_BENCH_HOSTCOMM=1): several ranks on the GPUs there are (possibly
+    # one), bootstrapped over gloo + svm_comm_init_host instead of NCCL, to exercise the N > 1
+    # path of this script where NCCL refuses to run (two ranks on one device)
+    hostcomm = os.environ.get("SVMB200_BENCH_HOSTCOMM") == "1"
+    if hostcomm:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    cdev = torch.device("cpu") if hostcomm else dev       # the collectives' device
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if hostcomm:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     S.lib()
     hbm, bf16, peak_kind = peaks()
     w = W.get(args.workload)
@@ -223,11 +233,14 @@ def run_ours(args):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > L2 (126 MB)
     comm = None
     if world > 1:
-        from paper_2311_14908_b200.dist import broadcast_uid
-        uid = broadcast_uid(S.svm_comm_unique_id() if rank == 0 else None, dev)
-        comm = S.svm_comm_init(rank, world, uid, local)
+        if hostcomm:
+            comm = S.svm_comm_init_host(rank, world, local)
+        else:
+            from paper_2311_14908_b200.dist import broadcast_uid
+            uid = broadcast_uid(S.svm_comm_unique_id() if rank == 0 else None, dev)
+            comm = S.svm_comm_init(rank, world, uid, local)
 
-    windowed = w.name in WINDOWED and w.name in PLAN_ITERS
+    windowed = (w.name in WINDOWED or args.windowed) and w.name in PLAN_ITERS
     window = math.ceil(PLAN_ITERS[w.name] / args.steps) if windowed else 0
 
     def train(**kw):
@@ -243,7 +256,7 @@ def run_ours(args):
     def gmax(v):
         if world > 1:
             from paper_2311_14908_b200.dist import max_over_ranks
-            return max_over_ranks(v, dev)
+            return max_over_ranks(v, cdev)
         return v
 
     # ---- warm-up: the first W windows of a solve (windowed) / W whole solves
@@ -376,7 +389,7 @@ def run_ours(args):
     if not args.no_predict:
         if world > 1:
             from paper_2311_14908_b200.dist import gather_rows
-            alpha_full = gather_rows(alpha_last.contiguous(), blocks, dev)
+            alpha_full = gather_rows(alpha_last.contiguous().to(cdev), blocks, cdev).to(dev)
         else:
             alpha_full = alpha_last
         Xsv, coef, _ = S.svm_support_vectors_dev(Xd_full, yd_full, alpha_full, stream=stream)
@@ -523,6 +536,7 @@ def main():
     ap.add_argument("--no-predict", action="store_true")
     ap.add_argument("--no-others", action="store_true", help="skip the W2-W4 time-to-converge entries")
     ap.add_argument("--no-gd", action="store_true", help="skip the projected-GD trainer measurement")
+    ap.add_argument("--windowed", action="store_true", help="time one solve in K windows for any workload")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

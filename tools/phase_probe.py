@@ -1,6 +1,6 @@
 """Per-phase cycle breakdown of the persistent SMO kernel (profiling aid).
 
-  SVMB200_PHASE_TIMERS=1 python tools/phase_probe.py W2 W3:0 W4:20000 W5:3000
+  SVMB200_PHASE_TIMERS=1 python tools/phase_probe.py W2 W3:0 W4:20000 W5:3000 W5@125000:3000
 (workload[:max_iter]; 0 = run to convergence)."""
 import os
 import sys
@@ -19,12 +19,13 @@ from gen import workloads as W  # noqa: E402
 
 for spec in sys.argv[1:]:
     name, _, rest = spec.partition(":")
+    name, _, nrows = name.partition("@")          # W5@125000:3000 -> the first 125,000 rows (a P = 8 shard)
     mi, _, kern = rest.partition(":")          # W4:20000:lin -> the linear kernel on W4's data
     w = W.get(name)
     if kern == "lin":
         import dataclasses
         w = dataclasses.replace(w, kernel=0)
-    X, y = w.train()
+    X, y = w.train(int(nrows) if nrows else None)
     Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
     kw = dict(max_iter=int(mi)) if mi and int(mi) > 0 else {}
     for extra in ({},):
