@@ -112,3 +112,18 @@ if "pf5" in what:
     os.environ.pop("SVMB200_L2_PF"); os.environ.pop("SVMB200_L2_KEEP_MB")
     del Xd, yd
     torch.cuda.empty_cache()
+
+if "shards" in what:
+    # the per-GPU work of a P-way W5 shard, on one GPU (rows 1M / P, the launch configuration
+    # of a rank: row cache off as for n_global = 1M)
+    w = W.get("W5")
+    for n in (125_000, 250_000, 500_000, 1_000_000):
+        X, y = w.train(n)
+        Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+        S.svm_train_dev(Xd, yd, w.C, w.kernel, w.gamma, w.tol, max_iter=300, cache_rows=-1)
+        r, t = timed(lambda: S.svm_train_dev(Xd, yd, w.C, w.kernel, w.gamma, w.tol, max_iter=3000, cache_rows=-1))
+        print(json.dumps({"probe": "shard", "workload": "W5", "rows": n, "P_equiv": 1_000_000 // n,
+                          "us_per_iter": 1e6 * r["info"]["seconds_solve"] / r["info"]["iterations"],
+                          "plan": S.last_plan()}), flush=True)
+        del Xd, yd
+        torch.cuda.empty_cache()
