@@ -300,6 +300,8 @@ struct Shared {
     int pass;                      // wss 2: 1 = this row pass is the gain pass of u (barrier A)
     double gain_kuu, gain_fu;      // wss 2 gain pass: K(x_u, x_u) and f_u (barrier B)
     double red_f[2][16];           // per consumer warp candidates (local row index; <= 16 warps)
+    double red_a[2][16];           // ... and their alpha when alpha lives in HBM (read by the
+                                   // consumer warps, off the scalar warp's critical path)
     int red_i[2][16];
     int c_hit, c_su, c_sl;         // row cache: both rows cached / their slots
     int c_fill_u, c_fill_l;        // row cache: the slot this iteration fills (miss), else -1
@@ -502,6 +504,13 @@ __device__ __forceinline__ void load_slot(const float* st, int rp, int i, int t,
 // walks the binade crossings instead of the c additions measured slower on W4: the common
 // c is 0, 2 or 4.)
 __device__ __forceinline__ double add_ones(double acc, int c) {
+    if (c <= 4) {
+        // the common case (W4's one-hot groups give c = 0, 2 or 4): the four sequential
+        // additions, branch-free, and the c-th result (ncu: the data-dependent loop below
+        // was the most executed line of the W4 row pass)
+        const double a1 = acc + 1.0, a2 = a1 + 1.0, a3 = a2 + 1.0, a4 = a3 + 1.0;
+        return c == 0 ? acc : c == 1 ? a1 : c == 2 ? a2 : c == 3 ? a3 : a4;
+    }
     const double cd = (double)c;
     const double s = acc + cd;
     const double bb = s - acc;
@@ -806,6 +815,10 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
         if (lane == 0) {
             sh.red_f[0][warp] = fu; sh.red_i[0][warp] = ju;
             sh.red_f[1][warp] = fl; sh.red_i[1][warp] = jl;
+            if (!A_SMEM) {
+                sh.red_a[0][warp] = ju == INT_MAX ? 0.0 : alpha_g[ju];
+                sh.red_a[1][warp] = jl == INT_MAX ? 0.0 : alpha_g[jl];
+            }
         }
     }
 
@@ -962,8 +975,16 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
                     c.fu = fu; c.fl = fl;
                     c.iu = (ju == INT_MAX) ? INT_MAX : (int)(gbase + ju);
                     c.il = (jl == INT_MAX) ? INT_MAX : (int)(gbase + jl);
-                    c.au = (ju == INT_MAX) ? 0.0 : (A_SMEM ? a_s[ju] : alpha_g[ju]);
-                    c.al = (jl == INT_MAX) ? 0.0 : (A_SMEM ? a_s[jl] : alpha_g[jl]);
+                    if (A_SMEM) {
+                        c.au = (ju == INT_MAX) ? 0.0 : a_s[ju];
+                        c.al = (jl == INT_MAX) ? 0.0 : a_s[jl];
+                    } else {
+                        // the winning warps' alpha, read by them (local rows are unique)
+                        const unsigned wu = __ballot_sync(0xffffffffu, lane < NWC_ && wju != INT_MAX && wju == ju);
+                        const unsigned wl = __ballot_sync(0xffffffffu, lane < NWC_ && wjl != INT_MAX && wjl == jl);
+                        c.au = (ju == INT_MAX || !wu) ? 0.0 : sh.red_a[0][__ffs(wu) - 1];
+                        c.al = (jl == INT_MAX || !wl) ? 0.0 : sh.red_a[1][__ffs(wl) - 1];
+                    }
                     c.yu = (ju == INT_MAX) ? 0 : ((fl_s[ju] & FL_POS) ? 1 : -1);
                     c.yl = (jl == INT_MAX) ? 0 : ((fl_s[jl] & FL_POS) ? 1 : -1);
                     if (m_wss2 && wphase == 1) {
@@ -1672,6 +1693,10 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
         if (lane == 0) {
             sh.red_f[0][warp] = bfu; sh.red_i[0][warp] = bju;
             sh.red_f[1][warp] = bfl; sh.red_i[1][warp] = bjl;
+            if (!A_SMEM) {
+                sh.red_a[0][warp] = bju == INT_MAX ? 0.0 : alpha_g[bju];
+                sh.red_a[1][warp] = bjl == INT_MAX ? 0.0 : alpha_g[bjl];
+            }
         }
         ++it;
     }
