@@ -127,3 +127,19 @@ if "shards" in what:
                           "plan": S.last_plan()}), flush=True)
         del Xd, yd
         torch.cuda.empty_cache()
+
+if "keep" in what:
+    # L2 evict_last window size for W5 shards (the per-GPU work of a P-way run)
+    w = W.get("W5")
+    for n in (125_000, 250_000):
+        X, y = w.train(n)
+        Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+        for keep in ("0", "48", "64", "80", "96", "112"):
+            os.environ["SVMB200_L2_KEEP_MB"] = keep
+            S.svm_train_dev(Xd, yd, w.C, w.kernel, w.gamma, w.tol, max_iter=300, cache_rows=-1)
+            r, t = timed(lambda: S.svm_train_dev(Xd, yd, w.C, w.kernel, w.gamma, w.tol, max_iter=3000, cache_rows=-1))
+            print(json.dumps({"probe": "keep", "rows": n, "keep_mb": int(keep),
+                              "us_per_iter": 1e6 * r["info"]["seconds_solve"] / r["info"]["iterations"]}), flush=True)
+        os.environ.pop("SVMB200_L2_KEEP_MB")
+        del Xd, yd
+        torch.cuda.empty_cache()
