@@ -157,6 +157,7 @@ extern "C" int svm_train_shard(void* comm, const float* X_local, const int8_t* y
         return fail(SVM_EINVAL, "row block outside [0, n_global)");
     if (dbg && ((dbg->alpha0 == nullptr) != (dbg->f0 == nullptr)))
         return fail(SVM_EINVAL, "warm start needs both alpha0 and f0");
+    if (p.shrink_window > 0) return fail(SVM_EINVAL, "shrinking runs on one rank (svm_train_dev / svm_train_ex)");
     cudaStream_t st = cuda_stream ? (cudaStream_t)cuda_stream : c->st;
     CKR(cudaSetDevice(c->device));
     const int W = c->world;

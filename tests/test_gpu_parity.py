@@ -580,3 +580,31 @@ def test_consumer_warp_counts(S, monkeypatch, nt):
         r_g, r_or = _run_pair(S, w, X, y, cluster=-1, cache_rows=-1)
         _assert_exact(r_g, r_or)
         assert S.last_plan()["threads"] == int(nt) + 64
+
+
+def test_l2_prefetch_switch_keeps_results(S, monkeypatch):
+    """SVMB200_L2_PF (L2 prefetch of the stages beyond the ring, a tuning switch) and the L2
+    keep window change only where bytes come from: the trajectory stays the oracle's."""
+    monkeypatch.setenv("SVMB200_NO_RESIDENT", "1")
+    w = W.get("W5")
+    X, y = w.train(3000)
+    for pf, keep in (("2", "48"), ("6", "0")):
+        monkeypatch.setenv("SVMB200_L2_PF", pf)
+        monkeypatch.setenv("SVMB200_L2_KEEP_MB", keep)
+        r_g, r_or = _run_pair(S, w, X, y, cluster=-1, cache_rows=-1)
+        _assert_exact(r_g, r_or)
+
+
+@pytest.mark.parametrize("expv", ["0", "1", "2"])
+def test_predict_tensor_exp_variants(S, monkeypatch, expv):
+    """The tensor-core epilogue's exp variants (SVMB200_PREDICT_EXP) all stay within
+    BASELINE.json's 1e-4 of the oracle."""
+    monkeypatch.setenv("SVMB200_PREDICT_EXP", expv)
+    w = W.get("W5")
+    X, y = w.train(3000)
+    r = O.train(X, y, w.C, w.kernel, w.gamma, w.tol)
+    sv = r.alpha > 1e-8
+    Xt, _ = w.test(700)
+    d_o = O.decision(X[sv], (r.alpha * y)[sv], r.b, w.kernel, w.gamma, Xt)
+    d_t = S.svm_predict(X[sv], (r.alpha * y)[sv], r.b, w.kernel, w.gamma, Xt, mode=S.PREDICT_TENSOR)
+    assert np.max(np.abs(d_t - d_o)) <= 1e-4

@@ -42,6 +42,7 @@ def test_two_processes_one_gpu(tmp_path):
         {"workload": "W1", "n": 200},
         {"workload": "W5", "n": 1200, "params": {"iters_per_launch": 97}},
         {"workload": "W5", "n": 1200, "warm": warm},
+        {"workload": "W3", "n": 900, "params": {"wss": 2}},
     ]
     cj = str(tmp_path / "cases.json")
     json.dump(cases, open(cj, "w"))
@@ -52,7 +53,10 @@ def test_two_processes_one_gpu(tmp_path):
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
     X1, y1 = w1.train(200)
     ref1 = O.train(X1, y1, w1.C, w1.kernel, w1.gamma, w1.tol, trace_cap=100000)
-    expect = [(ref5, 0), (ref1, 0), (ref5, 0), (ref5, k)]
+    w3 = W.get("W3")
+    X3, y3 = w3.train(900)
+    ref3 = O.train(X3, y3, w3.C, w3.kernel, w3.gamma, w3.tol, trace_cap=100000, wss=2)
+    expect = [(ref5, 0), (ref1, 0), (ref5, 0), (ref5, k), (ref3, 0)]
     for c, (ref, k0) in enumerate(expect):
         parts = [np.load(tmp_path / f"case{c}_rank{r}.npz") for r in range(2)]
         alpha = np.concatenate([q["alpha"] for q in parts])
