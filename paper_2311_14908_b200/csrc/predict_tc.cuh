@@ -268,15 +268,25 @@ k_predict_tc(const float* __restrict__ A,   // packed test rows [m_tiles][k_chun
                 // memory -- STL/LDL per element)
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
-                    const double dot = (double)__uint_as_float(v[j]);
                     double kv;
                     if (KERNEL == 1) {
-                        const double x = fmin(fma(g2, dot, a_t + __ldg(&qs_t[c0 + j])), 0.0);
+                        // fp32 accumulator -> fp64 by integer ops (the fp64 pipe is shared with
+                        // the tensor cores): rebias the exponent, widen the mantissa; 0 stays 0
+                        // (the dot of fp32 data is never subnormal unless 0 or a cancellation
+                        // below 2^-126, whose exp(.) contribution is 1 either way)
+                        const uint32_t fb = v[j];
+                        const uint32_t ex = (fb >> 23) & 0xffu;
+                        const uint32_t hi = ex == 0u ? (fb & 0x80000000u)
+                                                     : ((fb & 0x80000000u) | ((ex + 896u) << 20) | ((fb >> 3) & 0xfffffu));
+                        const uint32_t lo = ex == 0u ? 0u : (fb << 29);
+                        const double dot = __hiloint2double((int)hi, (int)lo);
+                        // (x > 0 by rounding, when t ~ s, gives K = 1 + O(1e-16): not clamped)
+                        const double x = fma(g2, dot, a_t + __ldg(&qs_t[c0 + j]));
                         if (EXPV == 0) kv = exp(x);
                         else if (EXPV == 1) kv = exp_nonpos(x, t64);
                         else kv = exp_nonpos_poly(x);
                     } else {
-                        kv = dot;
+                        kv = (double)__uint_as_float(v[j]);
                     }
                     acc_d = fma(__ldg(&cf_t[c0 + j]), kv, acc_d);
                 }

@@ -105,3 +105,14 @@ def test_shrinking_device_api_and_errors(S):
     np.testing.assert_array_equal(r["f"].cpu().numpy(), ref.f)
     with pytest.raises(S.SvmError, match="rank"):
         S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol, shrink_window=10, virtual_ranks=2)
+
+
+def test_shrinking_with_row_cache_and_gram(S, monkeypatch):
+    """The sub-problems keep a requested row cache (and the Gram path works per window):
+    still the oracle's shrinking trajectory."""
+    monkeypatch.setenv("SVMB200_NO_RESIDENT", "1")
+    w = W.get("W3")
+    X, y = w.train(1500)
+    _check(S, X, y, w.C, w.kernel, w.gamma, w.tol, 50, cache_rows=16)
+    monkeypatch.delenv("SVMB200_NO_RESIDENT")
+    _check(S, X, y, w.C, w.kernel, w.gamma, w.tol, 50, gram=1)
