@@ -204,6 +204,18 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
                  : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
     return ok != 0;
 }
+// the same with a suspend-time hint: the thread sleeps until the phase completes (or the
+// hint elapses) instead of spinning -- the producer lane and waiting consumers then leave
+// the issue slots to the warps doing row work (ncu on W4: the producer's spin loop was ~6%
+// of the instructions issued)
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+    uint32_t ok;
+    asm volatile("{\n\t.reg .pred p;\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity), "r"(ns) : "memory");
+    return ok != 0;
+}
 __device__ __forceinline__ long long globaltimer() {
     long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -214,7 +226,7 @@ __device__ __forceinline__ long long globaltimer() {
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     unsigned int spins = 0;
     long long t0 = 0;
-    while (!mbar_try_wait(bar, parity)) {
+    while (!mbar_try_wait_sleep(bar, parity, 2000u)) {
         if ((++spins & 4095u) == 0) {
             const long long now = globaltimer();
             if (t0 == 0) t0 = now;
@@ -525,6 +537,44 @@ template <int KERNEL, int RPT>
 __device__ __forceinline__ void mixed_rows(const Params& P, const float* st, int rp, int t,
                                            const double2* pivm, const uint32_t* pbits,
                                            double (&du)[RPT], double (&dl)[RPT]) {
+    if (P.mix_nseg == 2 && P.mix_seg[0] > 0) {
+        // the common layout (W4): the continuous columns, then one run of every binary
+        // column -- no run bookkeeping, and no bit masks (the padding bits of the last
+        // word are 0 in the rows and in the pivots)
+        const int nc = P.mix_nc;
+#pragma unroll 2
+        for (int i = 0; i < nc; ++i) {
+            uint32_t v[RPT];
+            load_slot<RPT>(st, rp, i, t, v);
+            const double2 pv = pivm[i];
+#pragma unroll
+            for (int q = 0; q < RPT; ++q) {
+                const double x = (double)__uint_as_float(v[q]);
+                if (KERNEL == 1) {
+                    double e = x - pv.x; du[q] = fma(e, e, du[q]);
+                    e = x - pv.y; dl[q] = fma(e, e, dl[q]);
+                } else {
+                    du[q] = fma(x, pv.x, du[q]); dl[q] = fma(x, pv.y, dl[q]);
+                }
+            }
+        }
+        int cu[RPT], cl[RPT];
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) { cu[q] = 0; cl[q] = 0; }
+        for (int w = 0; w < P.mix_nbw; ++w) {
+            uint32_t v[RPT];
+            load_slot<RPT>(st, rp, nc + w, t, v);
+            const uint32_t pu = pbits[w], pl = pbits[P.mix_nbw + w];
+#pragma unroll
+            for (int q = 0; q < RPT; ++q) {
+                if (KERNEL == 1) { cu[q] += __popc(v[q] ^ pu); cl[q] += __popc(v[q] ^ pl); }
+                else { cu[q] += __popc(v[q] & pu); cl[q] += __popc(v[q] & pl); }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) { du[q] = add_ones(du[q], cu[q]); dl[q] = add_ones(dl[q], cl[q]); }
+        return;
+    }
     int ci = 0, bb = 0;
     for (int sg = 0; sg < P.mix_nseg; ++sg) {
         const int len = P.mix_seg[sg];
@@ -741,7 +791,7 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
             }
             for (;;) {
                 if (wrapped) {
-                    while (!mbar_try_wait(&empty[slot], par ^ 1u)) {
+                    while (!mbar_try_wait_sleep(&empty[slot], par ^ 1u, 2000u)) {
                         if (sh.stop) break;
                     }
                 }
