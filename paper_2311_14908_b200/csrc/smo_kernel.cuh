@@ -152,6 +152,10 @@ struct Params {
     int mix_nseg, mix_nc, mix_nbw;
     int mix_seg[MIX_MAXSEG];
     const int* mix_map;
+    const uint32_t* xcomp;         // mixed rows, no row cache: every row of the problem in its
+                                   // compact form, row-major [n_global][mix_nc + mix_nbw], so the
+                                   // two pivots are gathered compact (one load per word) and
+                                   // K(x_u, x_l) is computed from them
     // Dictionary-coded rows (SURVEY §8(f) compact encodings: uint8 pixels): when X holds at
     // most 256 distinct fp32 values, xblk stores one byte per element, the index of its
     // value in dict (the values widened to fp64 exactly); the row pass looks the value up,
@@ -620,6 +624,40 @@ __device__ __forceinline__ void mixed_rows(const Params& P, const float* st, int
     }
 }
 
+// Mixed compact rows: the pivots' own sums from their compact forms (pivm: continuous
+// pairs (x_u, x_l), pbits: x_u's bit words then x_l's), run by run in the original column
+// order -- the R13 recurrence, a binary run adding 1.0 popcount times (add_ones), exactly
+// as mixed_rows does for a row.  RBF: D(x_u, x_l); linear: x_u.x_u, x_l.x_l, x_u.x_l.
+__device__ __forceinline__ void mixed_pivot_sums(const Params& P, const double2* pivm, const uint32_t* pbits,
+                                                 int kernel, double& d_ul, double& s_uu, double& s_ll, double& s_ul) {
+    int ci = 0, bb = 0;
+    d_ul = 0.0; s_uu = 0.0; s_ll = 0.0; s_ul = 0.0;
+    for (int sg = 0; sg < P.mix_nseg; ++sg) {
+        const int len = P.mix_seg[sg];
+        if (len > 0) {
+#pragma unroll 4
+            for (int i = ci; i < ci + len; ++i) {
+                const double2 pv = pivm[i];
+                if (kernel == 1) { const double e = pv.x - pv.y; d_ul = fma(e, e, d_ul); }
+                else { s_uu = fma(pv.x, pv.x, s_uu); s_ll = fma(pv.y, pv.y, s_ll); s_ul = fma(pv.x, pv.y, s_ul); }
+            }
+            ci += len;
+        } else {
+            const int nb = -len;
+            int cx = 0, cuu = 0, cll = 0, cul = 0;
+            for (int w = bb >> 5; w <= (bb + nb - 1) >> 5; ++w) {
+                const int lo = max(bb, 32 * w) - 32 * w, hi = min(bb + nb, 32 * w + 32) - 32 * w;
+                const uint32_t m = (hi - lo == 32) ? 0xffffffffu : (((1u << (hi - lo)) - 1u) << lo);
+                const uint32_t pu = pbits[w] & m, pl = pbits[P.mix_nbw + w] & m;
+                cx += __popc(pu ^ pl); cuu += __popc(pu); cll += __popc(pl); cul += __popc(pu & pl);
+            }
+            if (kernel == 1) d_ul = add_ones(d_ul, cx);
+            else { s_uu = add_ones(s_uu, cuu); s_ll = add_ones(s_ll, cll); s_ul = add_ones(s_ul, cul); }
+            bb += nb;
+        }
+    }
+}
+
 // Dictionary-coded rows (Params::dict_n): the R13 recurrence of RPT rows over the kc
 // features of one stage [kc][rp] of byte codes; values from the fp64 dictionary.
 template <int KERNEL, int RPT>
@@ -1050,7 +1088,13 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
                               rec_word(c, lane & 3, sq), P.sys_scope);
                 // warm L2 with this CTA's candidate rows: the two winners' rows are gathered
                 // from the row-major replica right after the selection (the critical path)
-                if (!m_gram && !m_isbin) {
+                if (m_mixed && P.xcomp && m_cache == 0) {
+                    const int ncw = P.mix_nc + P.mix_nbw;
+                    if (lane < 2) {
+                        const int jj = lane == 0 ? ju : jl;
+                        if (jj != INT_MAX) asm volatile("prefetch.global.L2 [%0];" :: "l"(P.xcomp + (gbase + jj) * (long long)ncw));
+                    }
+                } else if (!m_gram && !m_isbin) {
                     const int span = P.d * 4;
                     const int lines = (span + 127) / 128 + 1;
                     for (int q = lane; q < 2 * lines; q += 32) {
@@ -1260,6 +1304,16 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
                     const int w = lane < Wp ? lane : lane - Wp;
                     pw[lane] = w < P.bin_words ? __ldg(&P.xrbits[(long long)(lane < Wp ? iu : il) * P.bin_words + w]) : 0u;
                 }
+            } else if (m_mixed && P.xcomp && m_cache == 0) {
+                // compact pivots straight from the compact row-major copy: one load per word
+                const int nc = P.mix_nc, ncw = nc + P.mix_nbw;
+                for (int w0 = 0; w0 < ncw; w0 += 32) {
+                    const int w = w0 + lane;
+                    const uint32_t uw = w < ncw ? __ldg(&P.xcomp[(long long)iu * ncw + w]) : 0u;
+                    const uint32_t lw = w < ncw ? __ldg(&P.xcomp[(long long)il * ncw + w]) : 0u;
+                    if (w < nc) pivm[w] = make_double2((double)__uint_as_float(uw), (double)__uint_as_float(lw));
+                    else if (w < ncw) { pbits[w - nc] = uw; pbits[P.mix_nbw + w - nc] = lw; }
+                }
             } else {
                 const float* xu_g = xr + (long long)iu * P.d;
                 const float* xl_g = xr + (long long)il * P.d;
@@ -1393,6 +1447,16 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
                             const double2 pv = kul_t[i];
                             s_uu = fma(pv.x, pv.x, s_uu); s_ll = fma(pv.y, pv.y, s_ll); s_ul = fma(pv.x, pv.y, s_ul);
                         }
+                        Kuu = s_uu; Kll = s_ll; Kul = s_ul;
+                    }
+                } else if (m_mixed && P.xcomp) {
+                    // (the pivots were gathered compact: the same sums from their compact forms)
+                    double d_ul, s_uu, s_ll, s_ul;
+                    mixed_pivot_sums(P, pivm, pbits, KERNEL, d_ul, s_uu, s_ll, s_ul);
+                    if (KERNEL == 1) {
+                        Kuu = 1.0; Kll = 1.0;
+                        Kul = (u == l) ? 1.0 : svmexp::exp_cr_t(-(P.gamma * d_ul), tab);
+                    } else {
                         Kuu = s_uu; Kll = s_ll; Kul = s_ul;
                     }
                 } else if (KERNEL == 1) {

@@ -117,6 +117,30 @@ __global__ void k_build_xblk_mixed(const float* __restrict__ X, long long n_r, i
     }
 }
 
+// Mixed compact rows, row-major: row r = the nc continuous columns (fp32 bits, map order)
+// then nbw bit words of the binary columns -- the pivots' compact forms (Params::xcomp).
+__global__ void k_build_compact_rows(const float* __restrict__ X, long long n, int d, const int* __restrict__ map,
+                                     int nc, int nbw, uint32_t* __restrict__ out) {
+    const int ncw = nc + nbw, nbin = d - nc;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n * ncw;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long r = e / ncw;
+        const int k = (int)(e - r * ncw);
+        const float* row = X + r * d;
+        uint32_t v = 0u;
+        if (k < nc) {
+            v = __float_as_uint(row[map[k]]);
+        } else {
+            const int w = k - nc;
+            for (int b = 0; b < 32; ++b) {
+                const int i = 32 * w + b;
+                if (i < nbin && row[map[nc + i]] != 0.0f) v |= 1u << b;
+            }
+        }
+        out[e] = v;
+    }
+}
+
 // Dictionary of X's distinct fp32 values (bit patterns): an open-addressing set of 1024
 // slots; per-block sets in shared memory merged into the global one.  *count ends > 256 if
 // X has more than 256 distinct values (then the build stops early).
@@ -843,6 +867,15 @@ int solve(SolveArgs& a) {
         if ((rc = dalloc((void**)&dm, a.mix_map.size() * 4))) { release(); return rc; }
         CKR(cudaMemcpyAsync(dm, a.mix_map.data(), a.mix_map.size() * 4, cudaMemcpyHostToDevice, st));
         P.mix_map = dm;
+        if (pl.cache_slots == 0 && getenv("SVMB200_NO_COMPACT_PIVOTS") == nullptr) {
+            // the compact form of every row (pivot gathers; 4 (nc + nbw) bytes per row)
+            uint32_t* xc;
+            const long long ncw = pl.mix_nc + pl.mix_nbw;
+            if ((rc = dalloc((void**)&xc, (size_t)a.n_global * ncw * 4))) { release(); return rc; }
+            k_build_compact_rows<<<1184, 256, 0, st>>>(a.xr, a.n_global, (int)a.d, dm, pl.mix_nc, pl.mix_nbw, xc);
+            counted();
+            P.xcomp = xc;
+        }
     }
     for (int r = a.rank_base; r < a.rank_base + a.nranks_here; ++r) {
         const long long nr = a.n_rows[r];

@@ -515,6 +515,10 @@ def test_mixed_rows_parity(S, monkeypatch, runs, kern, gamma):
     assert S.last_plan()["mode"] == "mixed-streamed"
     _assert_exact(r6, r_or)
     monkeypatch.delenv("SVMB200_NO_RESIDENT")
+    monkeypatch.setenv("SVMB200_NO_COMPACT_PIVOTS", "1")          # pivots gathered dense
+    r7 = S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol, want_f=True, cluster=-1)
+    _assert_exact(r7, r_or)
+    monkeypatch.delenv("SVMB200_NO_COMPACT_PIVOTS")
     monkeypatch.setenv("SVMB200_NO_MIXED", "1")
     r5 = S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol, want_f=True, cluster=-1)
     assert not S.last_plan()["mode"].startswith("mixed")
