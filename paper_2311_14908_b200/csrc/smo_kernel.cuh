@@ -1238,18 +1238,6 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
                 c_hit = __shfl_sync(0xffffffffu, c_hit, 0);
                 su = __shfl_sync(0xffffffffu, su, 0);
                 sl = __shfl_sync(0xffffffffu, sl, 0);
-                if (c_hit) {
-                    // both rows cached: pull this CTA's columns of the two slots into L2 while
-                    // the winners' words and barrier A go by (the consumers read them next)
-                    const char* bu = reinterpret_cast<const char*>(P.cache[rank] + r0 + (long long)su * P.n_rows[rank]);
-                    const char* bl = reinterpret_cast<const char*>(P.cache[rank] + r0 + (long long)sl * P.n_rows[rank]);
-                    const int lines = (R * 8 + 127) / 128 + 1;
-                    for (int q = lane; q < 2 * lines; q += 32) {
-                        const char* base = q < lines ? bu : bl;
-                        const int o = min((q % lines) * 128, R * 8 - 1);
-                        if (R > 0) asm volatile("prefetch.global.L2 [%0];" :: "l"(base + o));
-                    }
-                }
             }
             SVM_PHASE(timing, PH_S_READ);
             // alpha and label of the two winners: words 2 / 3 of their records, in flight

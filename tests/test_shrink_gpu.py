@@ -116,3 +116,13 @@ def test_shrinking_with_row_cache_and_gram(S, monkeypatch):
     _check(S, X, y, w.C, w.kernel, w.gamma, w.tol, 50, cache_rows=16)
     monkeypatch.delenv("SVMB200_NO_RESIDENT")
     _check(S, X, y, w.C, w.kernel, w.gamma, w.tol, 50, gram=1)
+
+
+def test_shrinking_replay_wide_rows(S):
+    """d = 784 > 256: the rows set aside are replayed by the feature-chunked replay kernel
+    (the row-resident one covers d <= 256); from a state far into the W3 solve."""
+    w = W.get("W3")
+    X, y = w.train(2000)
+    full = O.train(X, y, w.C, w.kernel, w.gamma, w.tol)
+    part = O.train(X, y, w.C, w.kernel, w.gamma, w.tol, max_iter=(2 * full.iterations) // 3)
+    _check(S, X, y, w.C, w.kernel, w.gamma, w.tol, 29, alpha0=part.alpha, f0=part.f, max_iter=200)
