@@ -25,10 +25,11 @@ for spec in sys.argv[1:]:
     if kern == "lin":
         import dataclasses
         w = dataclasses.replace(w, kernel=0)
+    extra_kw = {"cache_rows": -1} if kern == "nocache" else {}
     X, y = w.train(int(nrows) if nrows else None)
     Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
     kw = dict(max_iter=int(mi)) if mi and int(mi) > 0 else {}
-    for extra in ({},):
+    for extra in (extra_kw,):
         S.svm_train_dev(Xd, yd, w.C, w.kernel, w.gamma, w.tol, **kw, **extra)   # warm
         torch.cuda.synchronize()
         t0 = time.time()

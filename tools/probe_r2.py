@@ -143,3 +143,23 @@ if "keep" in what:
         os.environ.pop("SVMB200_L2_KEEP_MB")
         del Xd, yd
         torch.cuda.empty_cache()
+
+if "persist" in what:
+    # persisting-L2 carve-out x evict_last window (SVMB200_L2_PERSIST_MB, SVMB200_L2_KEEP_MB)
+    w = W.get("W5")
+    for n, its in ((125_000, 3000), (1_000_000, 1500)):
+        X, y = w.train(n)
+        Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+        for persist, keep in (("", "48"), ("79", "48"), ("79", "64"), ("79", "76"), ("79", "96"), ("40", "40")):
+            if persist:
+                os.environ["SVMB200_L2_PERSIST_MB"] = persist
+            else:
+                os.environ.pop("SVMB200_L2_PERSIST_MB", None)
+            os.environ["SVMB200_L2_KEEP_MB"] = keep
+            S.svm_train_dev(Xd, yd, w.C, w.kernel, w.gamma, w.tol, max_iter=200, cache_rows=-1)
+            r, t = timed(lambda: S.svm_train_dev(Xd, yd, w.C, w.kernel, w.gamma, w.tol, max_iter=its, cache_rows=-1))
+            print(json.dumps({"probe": "persist", "rows": n, "persist_mb": persist or "default", "keep_mb": int(keep),
+                              "us_per_iter": 1e6 * r["info"]["seconds_solve"] / r["info"]["iterations"]}), flush=True)
+        os.environ.pop("SVMB200_L2_KEEP_MB"); os.environ.pop("SVMB200_L2_PERSIST_MB", None)
+        del Xd, yd
+        torch.cuda.empty_cache()
