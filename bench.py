@@ -400,7 +400,9 @@ def run_ours(args):
         tl, th = min(m, rank * mt), min(m, (rank + 1) * mt)
         Xt_d = torch.from_numpy(Xt[tl:th]).to(dev).contiguous()
         del Xt
-        S.svm_predict_dev(Xsv, coef, b_last, w.kernel, w.gamma, Xt_d[:1024], stream=stream, mode=1)   # warm
+        # warm with the full shape: the workspace (packed operands, ~2 GB) then comes from the
+        # memory pool instead of a first-time mapping inside the timed launch
+        S.svm_predict_dev(Xsv, coef, b_last, w.kernel, w.gamma, Xt_d, stream=stream, mode=1)
         barrier()
         p0 = torch.cuda.Event(enable_timing=True); p1 = torch.cuda.Event(enable_timing=True)
         p0.record(stream)
@@ -411,7 +413,27 @@ def run_ours(args):
         nsv = int(coef.shape[0])
         flops = 2.0 * m * nsv * d
         tf32_peak = bf16 * 0.5            # nominal TF32 : BF16 dense ratio (1.1 : 2.25 PF), no TF32 measured peak
-        predict = {"rows": m, "n_sv": nsv, "seconds": tp_s, "mode": "tcgen05 kind::tf32 3xTF32 + fp64 epilogue",
+        # context: cuBLAS's own TF32 GEMM rate on this box (8192^3, the tensor pipe as a library drives it)
+        ga = torch.randn(8192, 8192, device=dev)
+        gb = torch.randn(8192, 8192, device=dev)
+        tf32_prev = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = True
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                ga @ gb
+            g0 = torch.cuda.Event(enable_timing=True); g1 = torch.cuda.Event(enable_timing=True)
+            g0.record(stream)
+            for _ in range(10):
+                ga @ gb
+            g1.record(stream)
+        stream.synchronize()
+        torch.backends.cuda.matmul.allow_tf32 = tf32_prev
+        cublas_tf32 = 10 * 2.0 * 8192 ** 3 / (g0.elapsed_time(g1) * 1e-3) / 1e12
+        del ga, gb
+        predict = {"rows": m, "n_sv": nsv, "seconds": tp_s,
+                   "mode": "tcgen05 kind::tf32 3xTF32, 128 x 256 accumulator tiles + fp64/fp32 split-exp epilogue",
+                   "cublas_tf32_tflops": cublas_tf32,
+                   "frac_of_cublas_tf32": 3 * flops / tp_s / 1e12 / cublas_tf32,
                    "roofline": {"bound": "tensor", "achieved": 3 * flops / tp_s / 1e12, "peak": tf32_peak,
                                 "unit": "TFLOP/s", "frac": 3 * flops / tp_s / 1e12 / tf32_peak,
                                 "algorithmic_tflops": flops / tp_s / 1e12,

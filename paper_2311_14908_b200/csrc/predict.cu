@@ -82,47 +82,70 @@ __global__ void k_pad_coef(const double* __restrict__ coef, long long n, long lo
         out[i] = i < n ? coef[i] : 0.0;
 }
 
+__global__ void k_interleave(const double* __restrict__ a, const double* __restrict__ b, long long n,
+                             double2* __restrict__ out) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        out[i] = make_double2(a[i], b[i]);
+}
+
 // Tensor-core path (predict_tc.cuh): pack both operands to 3xTF32 core-matrix blocks,
-// then one CTA per 128 test rows.
-int predict_device_tc(const float* X_sv, const double* coef, long long n_sv, long long d, double b,
-                      int kernel, double gamma, const float* X_test, long long m, double* dec,
-                      cudaStream_t st) {
+// then one CTA per 128 test rows.  Tuning switches: SVMB200_PREDICT_EXP (the epilogue's exp,
+// 0-4, see k_predict_tc), SVMB200_PREDICT_BN (128 or 256 support vectors per tile).
+template <int BN_>
+static int predict_tc_launch(const float* X_sv, const double* coef, long long n_sv, long long d, double b,
+                             int kernel, double gamma, const float* X_test, long long m, double* dec,
+                             cudaStream_t st, int expv) {
     using namespace svmtc;
-    pool_setup();
+    using Cf = TcCfg<BN_>;
     const long long m_pad = (m + BM - 1) / BM * BM;
-    const long long n_pad = (n_sv + BN - 1) / BN * BN;
-    const int k_chunks = (int)((d + BK - 1) / BK);
+    const long long n_pad = (n_sv + Cf::BN - 1) / Cf::BN * Cf::BN;
+    const int k_chunks = (int)((d + Cf::BK - 1) / Cf::BK);
     float *pa = nullptr, *pb = nullptr;
     double *qt = nullptr, *qs = nullptr, *cf = nullptr;
-    const size_t a_floats = (size_t)m_pad * k_chunks * BK * 2, b_floats = (size_t)n_pad * k_chunks * BK * 2;
+    double2* qc = nullptr;
+    const size_t a_floats = (size_t)m_pad * k_chunks * Cf::BK * 2, b_floats = (size_t)n_pad * k_chunks * Cf::BK * 2;
     if (cudaMallocAsync(&pa, a_floats * 4, st) != cudaSuccess || cudaMallocAsync(&pb, b_floats * 4, st) != cudaSuccess ||
         cudaMallocAsync(&qt, m_pad * 8, st) != cudaSuccess || cudaMallocAsync(&qs, n_pad * 8, st) != cudaSuccess ||
-        cudaMallocAsync(&cf, n_pad * 8, st) != cudaSuccess) {
+        cudaMallocAsync(&cf, n_pad * 8, st) != cudaSuccess || cudaMallocAsync(&qc, n_pad * 16, st) != cudaSuccess) {
         if (pa) cudaFreeAsync(pa, st); if (pb) cudaFreeAsync(pb, st);
         if (qt) cudaFreeAsync(qt, st); if (qs) cudaFreeAsync(qs, st); if (cf) cudaFreeAsync(cf, st);
+        if (qc) cudaFreeAsync(qc, st);
         return fail(SVM_ENOMEM, "predict workspace allocation failed");
     }
-    k_pack_3xtf32<<<1184, 256, 0, st>>>(X_test, m, (int)d, k_chunks, m_pad, pa, qt);
-    k_pack_3xtf32<<<1184, 256, 0, st>>>(X_sv, n_sv, (int)d, k_chunks, n_pad, pb, qs);
+    k_pack_3xtf32<<<1184, 256, 0, st>>>(X_test, m, (int)d, k_chunks, m_pad, BM, Cf::BK, pa, qt);
+    k_pack_3xtf32<<<1184, 256, 0, st>>>(X_sv, n_sv, (int)d, k_chunks, n_pad, Cf::BN, Cf::BK, pb, qs);
     k_pad_coef<<<256, 256, 0, st>>>(coef, n_sv, n_pad, cf);
     counted(3);
     if (kernel == SVM_RBF) {                       // the epilogue takes -gamma |s|^2 per SV
         k_scale_norms<<<256, 256, 0, st>>>(qs, n_pad, -gamma);
         counted();
     }
-    const size_t smem = (size_t)STAGES * STAGE_BYTES;
-    // the epilogue's exp (tuning switch SVMB200_PREDICT_EXP: 0 CUDA exp, 1 table, 2 polynomial)
-    int expv = 0;            // (measured: all three equal at the W5 scale -- the exp does not bound it)
-    if (const char* e = getenv("SVMB200_PREDICT_EXP")) expv = atoi(e);
-    auto fn = kernel != SVM_RBF ? k_predict_tc<0, 0>
-            : expv == 0 ? k_predict_tc<1, 0> : expv == 2 ? k_predict_tc<1, 2> : k_predict_tc<1, 1>;
+    k_interleave<<<256, 256, 0, st>>>(qs, cf, n_pad, qc);
+    counted();
+    const size_t smem = (size_t)Cf::STAGES * Cf::STAGE_BYTES;
+    auto fn = kernel != SVM_RBF ? k_predict_tc<0, 0, BN_>
+            : expv == 0 ? k_predict_tc<1, 0, BN_> : expv == 1 ? k_predict_tc<1, 1, BN_>
+            : expv == 2 ? k_predict_tc<1, 2, BN_> : expv == 3 ? k_predict_tc<1, 3, BN_> : k_predict_tc<1, 4, BN_>;
     CKR(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    fn<<<(unsigned)(m_pad / BM), NTHREADS, smem, st>>>(pa, pb, qt, qs, cf, k_chunks, (int)(n_pad / BN), m, b,
+    fn<<<(unsigned)(m_pad / BM), NTHREADS, smem, st>>>(pa, pb, qt, qc, k_chunks, (int)(n_pad / Cf::BN), m, b,
                                                         gamma, dec);
     counted();
     CKR(cudaGetLastError());
     cudaFreeAsync(pa, st); cudaFreeAsync(pb, st); cudaFreeAsync(qt, st); cudaFreeAsync(qs, st); cudaFreeAsync(cf, st);
+    cudaFreeAsync(qc, st);
     return SVM_OK;
+}
+
+int predict_device_tc(const float* X_sv, const double* coef, long long n_sv, long long d, double b,
+                      int kernel, double gamma, const float* X_test, long long m, double* dec,
+                      cudaStream_t st) {
+    pool_setup();
+    int expv = 3;            // measured (1M x 284k x 256): 0 1.01 s, 3 0.90 s, 4 1.11 s (BN = 128)
+    if (const char* e = getenv("SVMB200_PREDICT_EXP")) expv = atoi(e);
+    int bn = 256;            // measured with expv 3: BN 128 0.91 s, BN 256 0.85 s
+    if (const char* e = getenv("SVMB200_PREDICT_BN")) bn = atoi(e);
+    if (bn == 256) return predict_tc_launch<256>(X_sv, coef, n_sv, d, b, kernel, gamma, X_test, m, dec, st, expv);
+    return predict_tc_launch<128>(X_sv, coef, n_sv, d, b, kernel, gamma, X_test, m, dec, st, expv);
 }
 
 int predict_device(const float* X_sv, const double* coef, long long n_sv, long long d, double b,

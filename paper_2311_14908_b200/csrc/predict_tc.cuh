@@ -32,19 +32,32 @@
 namespace svmtc {
 
 constexpr int BM = 128;          // test rows per CTA (MMA M)
-constexpr int BN = 128;          // support vectors per tile (MMA N)
-constexpr int BK = 32;           // tf32 elements per stage (128 B per row)
-constexpr int STAGES = 3;
-constexpr int TILE_FLOATS = BM * BK;           // 4096 floats = 16 KB per operand block
-constexpr int STAGE_BYTES = 4 * TILE_FLOATS * 4;  // A hi, A lo, B hi, B lo
 constexpr int EPI_WARPS = 16;                     // epilogue: EPI_WARPS / 4 warps per TMEM lane quarter
 constexpr int NPART = EPI_WARPS / 4;              // column parts of an accumulator tile
 constexpr int NTHREADS = 64 + 32 * EPI_WARPS;
-constexpr int TMEM_COLS = 2 * BN;
 
-// element (r, k) of a [rows][BK] block in the core-matrix order
-__host__ __device__ inline int packed_index(int r, int k) {
-    return (((r >> 3) * (BK / 4) + (k >> 2)) << 5) + ((r & 7) << 2) + (k & 3);
+// Tile shapes: BN support vectors per accumulator tile (MMA N), BK tf32 elements of K per
+// stage.  BN = 128: 3 stages of 64 KB, two 128-column accumulators (256 TMEM columns);
+// BN = 256: 4 stages of 48 KB, two 256-column accumulators (all 512 columns) -- each
+// stage's A block then feeds twice the MMA work, 25% fewer bytes from L2 per product.
+template <int BN_>
+struct TcCfg {
+    static constexpr int BN = BN_;
+    static constexpr int BK = BN_ == 128 ? 32 : 16;
+    static constexpr int STAGES = BN_ == 128 ? 3 : 4;
+    static constexpr int A_FLOATS = BM * BK;      // one of A hi / A lo per stage
+    static constexpr int B_FLOATS = BN * BK;      // one of B hi / B lo per stage
+    static constexpr int STAGE_BYTES = (2 * A_FLOATS + 2 * B_FLOATS) * 4;
+    static constexpr int TMEM_COLS = 2 * BN;
+    static constexpr int SBO = 8 * BK * 4;        // bytes between 8-row groups of a block
+    // instruction descriptor: D f32, A/B tf32, both K-major, N = BN, M = BM
+    static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                                      ((uint32_t)(BM >> 4) << 24);
+};
+
+// element (r, k) of a [rows][bk] block in the core-matrix order
+__host__ __device__ inline int packed_index(int r, int k, int bk) {
+    return (((r >> 3) * (bk / 4) + (k >> 2)) << 5) + ((r & 7) << 2) + (k & 3);
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -72,20 +85,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
-// shared-memory matrix descriptor: K-major, no swizzle, LBO 128 B, SBO 1024 B, sm100 version 1
+// shared-memory matrix descriptor: K-major, no swizzle, LBO 128 B, SBO bytes between 8-row
+// groups, sm100 version 1
+template <int SBO>
 __device__ __forceinline__ uint64_t smem_desc(const void* p) {
     const uint64_t a = (smem_u32(p) >> 4) & 0x3fffu;
-    return a | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(1024 >> 4) << 32) | (1ull << 46);
+    return a | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(SBO >> 4) << 32) | (1ull << 46);
 }
-// instruction descriptor: D f32, A/B tf32, both K-major, N = BN, M = BM
-constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                           ((uint32_t)(BM >> 4) << 24);
 
+template <uint32_t IDESC>
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
     asm volatile("{\n\t.reg .pred p;\n\t"
                  "setp.ne.b32 p, %4, 0;\n\t"
                  "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
-                 :: "r"(tmem_d), "l"(da), "l"(db), "r"(IDESC), "r"(accumulate) : "memory");
+                 :: "r"(tmem_d), "l"(da), "l"(db), "n"(IDESC), "r"(accumulate) : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
@@ -144,23 +157,74 @@ __device__ __forceinline__ double exp_nonpos_poly(double x) {
     return __hiloint2double(__double2hiint(q) + n * (1 << 20), __double2loint(q));
 }
 
-// EXPV: the epilogue's exp -- 0 CUDA's fp64 exp, 1 table-driven (exp_nonpos), 2 polynomial
-template <int KERNEL, int EXPV>
+// fp32 <-> fp64 by integer operations (no conversion instruction on the fp64 pipe, which
+// the tensor cores share).  widen: exact; 0 and fp32 subnormals -> +-0 (a dot product of
+// fp32 data is never subnormal unless 0 or a cancellation below 2^-126, whose effect on
+// exp(.) is nil).  narrow: truncation (relative error < 2^-23), |x| < 2^-126 -> 0.
+__device__ __forceinline__ double widen_f32_int(uint32_t fb) {
+    const uint32_t ex = (fb >> 23) & 0xffu;
+    const uint32_t hi = ex == 0u ? (fb & 0x80000000u)
+                                 : ((fb & 0x80000000u) | ((ex + 896u) << 20) | ((fb >> 3) & 0xfffffu));
+    const uint32_t lo = ex == 0u ? 0u : (fb << 29);
+    return __hiloint2double((int)hi, (int)lo);
+}
+__device__ __forceinline__ float narrow_f64_int(double x) {
+    const uint32_t h = (uint32_t)__double2hiint(x), l = (uint32_t)__double2loint(x);
+    const uint32_t e = (h >> 20) & 0x7ffu;
+    const uint32_t fb = (h & 0x80000000u) | ((e - 896u) << 23) | ((h & 0xfffffu) << 3) | (l >> 29);
+    return e > 896u && e < 1151u ? __uint_as_float(fb) : 0.0f;
+}
+
+// The epilogue's kernel value K = exp(x), x = c + g2 * dot (c = -gamma (|t|^2 + |s|^2),
+// g2 = 2 gamma, dot = the fp32 accumulator t.s), with as few fp64-pipe operations as the
+// accuracy allows -- the fp64 pipe is shared with the tensor cores (ncu: pipe_shared =
+// fp64 + tensor), so every fp64 operation of the epilogue is taken from the MMAs.
+//   x = (n / 256) ln 2 + r, n = nearest integer of x 256 / ln 2 (1.5 2^52 shift), r by one
+//   fma with ln 2 / 256 rounded to double (|n| < 2^18 for x >= -708: error < 6e-14 abs.),
+//   exp(x) = 2^(n >> 8) 2^((n & 255) / 256) (1 + r + p),  p = r^2 (1/2 + r/6 + r^2/24)
+//   in fp32 (|r| <= ln 2 / 512, |p| <= 9.3e-7: fp32's ~2^-22 relative error on p is
+//   < 3e-13 of K; truncation r^5/120 < 4e-17), 2^(j / 256) from a shared-memory table.
+// Relative error of K < 4e-13 (BASELINE.json's decision tolerance is 1e-4 absolute;
+// with sum |coef| <= 3e6 the kernel-value error adds < 1.2e-6).  x < -707.5 -> 0 (K < 1e-307).
+// INT_CVT: the fp32 <-> fp64 conversions by integer operations instead of F2F.
+template <bool INT_CVT>
+__device__ __forceinline__ double exp_split(uint32_t dot_bits, double c, double g2, const double* __restrict__ t256) {
+    const double dot = INT_CVT ? widen_f32_int(dot_bits) : (double)__uint_as_float(dot_bits);
+    const double x = fma(g2, dot, c);
+    const double sh = 6755399441055744.0;                     // 1.5 * 2^52
+    const double tN = fma(x, 369.32993046757464, sh);         // x * 256 / ln 2 + shift
+    const int n = __double2loint(tN);
+    const double nd = tN - sh;
+    const double r = fma(nd, -0.0027076061740622863, x);     // ln 2 / 256
+    const float rf = INT_CVT ? narrow_f64_int(r) : __double2float_rn(r);
+    const float pf = (rf * rf) * fmaf(fmaf(rf, 1.0f / 24.0f, 1.0f / 6.0f), rf, 0.5f);
+    const double q = r + (INT_CVT ? widen_f32_int(__float_as_uint(pf)) : (double)pf);
+    const double T = t256[n & 255];
+    const double v = fma(T, q, T);
+    const double kv = __hiloint2double(__double2hiint(v) + (n >> 8) * (1 << 20), __double2loint(v));
+    return n < -261376 ? 0.0 : kv;                            // x < -707.5 (n >> 8 >= -1021: v 2^(n >> 8) normal)
+}
+
+// EXPV: the epilogue's exp -- 0 CUDA's fp64 exp, 1 table-driven (exp_nonpos), 2 polynomial,
+// 3 exp_split with F2F conversions, 4 exp_split with integer conversions.  BN_: TcCfg.
+template <int KERNEL, int EXPV, int BN_>
 __global__ void __launch_bounds__(NTHREADS, 1)
 k_predict_tc(const float* __restrict__ A,   // packed test rows [m_tiles][k_chunks][2][BM*BK]
              const float* __restrict__ B,   // packed SVs       [n_tiles][k_chunks][2][BN*BK]
              const double* __restrict__ qt, // |t_i|^2 [m_pad]
-             const double* __restrict__ qs, // RBF: -gamma |s|^2 [n_pad] (unused for linear)
-             const double* __restrict__ cf, // coef    [n_pad] (0 for padding)
+             const double2* __restrict__ qc, // {RBF: -gamma |s|^2 (linear: unused), coef (0 for padding)} [n_pad]
              int k_chunks, int n_tiles, long long m, double b, double gamma,
              double* __restrict__ dec) {
+    using Cf = TcCfg<BN_>;
+    constexpr int BN = Cf::BN, BK = Cf::BK, STAGES = Cf::STAGES, TMEM_COLS = Cf::TMEM_COLS;
+    constexpr int AF = Cf::A_FLOATS, BF = Cf::B_FLOATS;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     float* stage_base = reinterpret_cast<float*>(smem_raw);
     __shared__ uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
     __shared__ uint32_t tmem_base_sh;
     __shared__ double part_sh[NPART][BM];           // the column parts' partial sums
-    __shared__ double t64[64];                      // 2^(j / 64), j = 0..63 (exp_nonpos)
-    if (threadIdx.x < 64) t64[threadIdx.x] = exp2((double)threadIdx.x / 64.0);
+    __shared__ double t64[256];                     // 2^(j / 64) (exp_nonpos), 2^(j / 256) (exp_split)
+    if (threadIdx.x < 256) t64[threadIdx.x] = exp2((double)threadIdx.x / (EXPV >= 3 ? 256.0 : 64.0));
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int mt = blockIdx.x;
@@ -182,18 +246,18 @@ k_predict_tc(const float* __restrict__ A,   // packed test rows [m_tiles][k_chun
     if (warp == 0) {
         // ---------------- producer
         if (lane == 0) {
-            const float* a_tile = A + (size_t)mt * k_chunks * 2 * TILE_FLOATS;
+            const float* a_tile = A + (size_t)mt * k_chunks * 2 * AF;
             int slot = 0;
             uint32_t par = 0;
             bool wrapped = false;
             for (int nt = 0; nt < n_tiles; ++nt) {
-                const float* b_tile = B + (size_t)nt * k_chunks * 2 * TILE_FLOATS;
+                const float* b_tile = B + (size_t)nt * k_chunks * 2 * BF;
                 for (int kc = 0; kc < k_chunks; ++kc) {
                     if (wrapped) mbar_wait(&empty[slot], par ^ 1u);
-                    float* st = stage_base + (size_t)slot * 4 * TILE_FLOATS;
-                    mbar_arrive_tx(&full[slot], STAGE_BYTES);
-                    bulk_g2s(st, a_tile + (size_t)kc * 2 * TILE_FLOATS, 2 * TILE_FLOATS * 4, &full[slot]);
-                    bulk_g2s(st + 2 * TILE_FLOATS, b_tile + (size_t)kc * 2 * TILE_FLOATS, 2 * TILE_FLOATS * 4, &full[slot]);
+                    float* st = stage_base + (size_t)slot * (2 * AF + 2 * BF);
+                    mbar_arrive_tx(&full[slot], Cf::STAGE_BYTES);
+                    bulk_g2s(st, a_tile + (size_t)kc * 2 * AF, 2 * AF * 4, &full[slot]);
+                    bulk_g2s(st + 2 * AF, b_tile + (size_t)kc * 2 * BF, 2 * BF * 4, &full[slot]);
                     if (++slot == STAGES) { slot = 0; par ^= 1u; wrapped = true; }
                 }
             }
@@ -211,18 +275,20 @@ k_predict_tc(const float* __restrict__ A,   // packed test rows [m_tiles][k_chun
                 mbar_wait(&full[slot], par);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 if (lane == 0) {
-                    const float* st = stage_base + (size_t)slot * 4 * TILE_FLOATS;
+                    const float* st = stage_base + (size_t)slot * (2 * AF + 2 * BF);
                     const float* ahi = st;
-                    const float* alo = st + TILE_FLOATS;
-                    const float* bhi = st + 2 * TILE_FLOATS;
-                    const float* blo = st + 3 * TILE_FLOATS;
+                    const float* alo = st + AF;
+                    const float* bhi = st + 2 * AF;
+                    const float* blo = st + 2 * AF + BF;
+                    constexpr uint32_t ID = Cf::IDESC;
+                    constexpr int SB = Cf::SBO;
 #pragma unroll
                     for (int k8 = 0; k8 < BK / 8; ++k8) {
                         const int off = k8 * 64;            // 2 core matrices (256 B) per K = 8
                         const uint32_t first = (kc == 0 && k8 == 0) ? 0u : 1u;
-                        mma_tf32(tacc, smem_desc(ahi + off), smem_desc(bhi + off), first);
-                        mma_tf32(tacc, smem_desc(ahi + off), smem_desc(blo + off), 1u);
-                        mma_tf32(tacc, smem_desc(alo + off), smem_desc(bhi + off), 1u);
+                        mma_tf32<ID>(tacc, smem_desc<SB>(ahi + off), smem_desc<SB>(bhi + off), first);
+                        mma_tf32<ID>(tacc, smem_desc<SB>(ahi + off), smem_desc<SB>(blo + off), 1u);
+                        mma_tf32<ID>(tacc, smem_desc<SB>(alo + off), smem_desc<SB>(bhi + off), 1u);
                     }
                     mma_commit(&empty[slot]);               // frees the stage when done
                     if (kc == k_chunks - 1) mma_commit(&tfull[acc]);
@@ -249,8 +315,7 @@ k_predict_tc(const float* __restrict__ A,   // packed test rows [m_tiles][k_chun
             const int acc = nt & 1;
             mbar_wait(&tfull[acc], (nt >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const double* qs_t = qs + (size_t)nt * BN;
-            const double* cf_t = cf + (size_t)nt * BN;
+            const double2* qc_t = qc + (size_t)nt * BN;
 #pragma unroll 1
             for (int c0 = half * (BN / NPART); c0 < (half + 1) * (BN / NPART); c0 += 16) {
                 // 16 accumulator columns per load (x16)
@@ -269,7 +334,10 @@ k_predict_tc(const float* __restrict__ A,   // packed test rows [m_tiles][k_chun
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
                     double kv;
-                    if (KERNEL == 1) {
+                    const double2 sc = qc_t[c0 + j];             // {-gamma |s|^2, coef}: one 16-byte load
+                    if (KERNEL == 1 && EXPV >= 3) {
+                        kv = exp_split<EXPV == 4>(v[j], a_t + sc.x, g2, t64);
+                    } else if (KERNEL == 1) {
                         // fp32 accumulator -> fp64 by integer ops (the fp64 pipe is shared with
                         // the tensor cores): rebias the exponent, widen the mantissa; 0 stays 0
                         // (the dot of fp32 data is never subnormal unless 0 or a cancellation
@@ -281,14 +349,14 @@ k_predict_tc(const float* __restrict__ A,   // packed test rows [m_tiles][k_chun
                         const uint32_t lo = ex == 0u ? 0u : (fb << 29);
                         const double dot = __hiloint2double((int)hi, (int)lo);
                         // (x > 0 by rounding, when t ~ s, gives K = 1 + O(1e-16): not clamped)
-                        const double x = fma(g2, dot, a_t + __ldg(&qs_t[c0 + j]));
+                        const double x = fma(g2, dot, a_t + sc.x);
                         if (EXPV == 0) kv = exp(x);
                         else if (EXPV == 1) kv = exp_nonpos(x, t64);
                         else kv = exp_nonpos_poly(x);
                     } else {
                         kv = (double)__uint_as_float(v[j]);
                     }
-                    acc_d = fma(__ldg(&cf_t[c0 + j]), kv, acc_d);
+                    acc_d = fma(sc.y, kv, acc_d);
                 }
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -311,10 +379,14 @@ k_predict_tc(const float* __restrict__ A,   // packed test rows [m_tiles][k_chun
     }
 }
 
-// Pack rows [rows][d] fp32 (row-major) into [tiles][k_chunks][hi|lo][BM*BK] tf32 blocks;
-// also |x|^2 in fp64.  Padding rows / features are zero.
+// Pack rows [rows][d] fp32 (row-major) into [tiles][k_chunks][hi|lo][tr*bk] tf32 blocks
+// (tr rows per tile, bk elements of K per chunk); also |x|^2 in fp64.  Padding rows /
+// features are zero.
 __global__ void k_pack_3xtf32(const float* __restrict__ X, long long rows, int d, int k_chunks,
-                              long long rows_pad, float* __restrict__ out, double* __restrict__ norms) {
+                              long long rows_pad, int tr, int bk, float* __restrict__ out,
+                              double* __restrict__ norms) {
+    const int BK = bk;
+    const int TILE_FLOATS = tr * bk;
     const long long total = rows_pad * (long long)k_chunks * BK;
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
          e += (long long)gridDim.x * blockDim.x) {
@@ -327,11 +399,11 @@ __global__ void k_pack_3xtf32(const float* __restrict__ X, long long rows, int d
         uint32_t lb;
         asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lb) : "f"(x - hi));
         const float lo = __uint_as_float(lb);
-        const long long tile = r / BM;
-        const int rr = (int)(r - tile * BM), kc = k / BK, kk = k - kc * BK;
+        const long long tile = r / tr;
+        const int rr = (int)(r - tile * tr), kc = k / BK, kk = k - kc * BK;
         float* blk = out + ((size_t)tile * k_chunks + kc) * 2 * TILE_FLOATS;
-        blk[packed_index(rr, kk)] = hi;
-        blk[TILE_FLOATS + packed_index(rr, kk)] = lo;
+        blk[packed_index(rr, kk, bk)] = hi;
+        blk[TILE_FLOATS + packed_index(rr, kk, bk)] = lo;
     }
     for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < rows_pad;
          r += (long long)gridDim.x * blockDim.x) {

@@ -140,6 +140,7 @@ struct Params {
     int crw;                       // cluster mode: 16-byte words per record (4 + 2 ceil(crow/3))
     unsigned long long* timers;    // optional [8] per-phase cycle totals of CTA 0
     int poll_ns;                   // > 0: back-off between mailbox polls (tuning)
+    int dbg_fast_only;             // diagnostic only (SVMB200_DBG_FAST_ONLY): skip the exp slow phase -- WRONG results, timing probe
     int dp;                        // dense pivot entries in shared memory (>= d; = d_pad unless mixed)
     // Mixed compact rows (SURVEY §8(f) compact encodings): the columns whose values are all
     // exactly 0 or 1 are stored as bits, the others as fp32.  A row of xblk holds mix_nc fp32
@@ -1738,7 +1739,7 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
                         else kl[q] = svmexp::exp_cr_fast(-(P.gamma * dl[q]), tab, sl[q]);
                         all_safe = all_safe && su[q] && sl[q];
                     }
-                    if (!all_safe) {
+                    if (!all_safe && !P.dbg_fast_only) {
 #pragma unroll
                         for (int q = 0; q < RPT; ++q) {
                             if (!su[q]) ku[q] = svmexp::exp_cr_slow(-(P.gamma * du[q]), tab);

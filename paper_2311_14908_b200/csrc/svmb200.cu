@@ -832,6 +832,7 @@ int solve(SolveArgs& a) {
     P.timeout_ns = a.timeout_ns;
     P.wss = p.wss;
     if (const char* e = getenv("SVMB200_POLL_NS")) P.poll_ns = atoi(e);
+    if (const char* e = getenv("SVMB200_DBG_FAST_ONLY")) P.dbg_fast_only = atoi(e);
     // L2 residency of streamed X: keep the first tiles of every CTA block in L2
     // (SVMB200_L2_KEEP_MB, per GPU; tuning)
     if (!pl.resident && pl.bin_words == 0 && !gram && pl.mix_nseg == 0 && pl.esz == 4) {

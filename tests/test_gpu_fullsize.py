@@ -170,6 +170,29 @@ def test_predict_tensor_w2_bench_model(S):
     _predict_at_scale(S, np.ascontiguousarray(X[sv]), (g["alpha"] * y)[sv], float(g["b"]), w, Xt, rows)
 
 
+def test_predict_tensor_exact_dots_w2(S):
+    """On exactly binary data (W2) the 3xTF32 dot products, the fp64 norms and so the
+    kernel arguments are exact: the tensor-core decision values then differ from the
+    oracle's only by the epilogue's exp (< 4e-13 relative, predict_tc.cuh exp_split) and
+    fp64 summation order -- pinned at 1e-11 of sum_s |coef_s| K_s, far inside 1e-4 (an
+    fp32 exp would miss it by four orders of magnitude)."""
+    import os
+    import torch
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "W2_oracle.npz"))
+    w = W.get("W2")
+    X, y = w.train()
+    sv = g["alpha"] > 1e-8
+    Xsv = np.ascontiguousarray(X[sv])
+    coef = (g["alpha"] * y)[sv]
+    Xt, _ = w.test()
+    Xt = np.ascontiguousarray(Xt[np.random.default_rng(7).choice(len(Xt), 400, replace=False)])
+    dec = S.svm_predict_dev(torch.from_numpy(Xsv).cuda(), torch.from_numpy(coef).cuda(), float(g["b"]), w.kernel,
+                            w.gamma, torch.from_numpy(Xt).cuda(), mode=S.PREDICT_TENSOR).cpu().numpy()
+    ref = O.decision(Xsv, coef, float(g["b"]), w.kernel, w.gamma, Xt)
+    mag = O.decision(Xsv, np.abs(coef), 0.0, w.kernel, w.gamma, Xt)      # sum_s |coef_s| K_s
+    assert np.all(np.abs(dec - ref) <= 1e-11 * mag + 1e-13), np.max(np.abs(dec - ref) / mag)
+
+
 def test_predict_tensor_w5_scale(S):
     """BASELINE.json configs[4] prediction size: 10^6 held-out rows against 450,000
     support vectors (W5 training rows; coefficients drawn like alpha y with C = 1, 40% at

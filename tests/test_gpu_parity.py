@@ -599,16 +599,25 @@ def test_l2_prefetch_switch_keeps_results(S, monkeypatch):
         _assert_exact(r_g, r_or)
 
 
-@pytest.mark.parametrize("expv", ["0", "1", "2"])
-def test_predict_tensor_exp_variants(S, monkeypatch, expv):
-    """The tensor-core epilogue's exp variants (SVMB200_PREDICT_EXP) all stay within
-    BASELINE.json's 1e-4 of the oracle."""
-    monkeypatch.setenv("SVMB200_PREDICT_EXP", expv)
+@pytest.fixture(scope="module")
+def w5_small_model():
     w = W.get("W5")
     X, y = w.train(3000)
     r = O.train(X, y, w.C, w.kernel, w.gamma, w.tol)
     sv = r.alpha > 1e-8
     Xt, _ = w.test(700)
-    d_o = O.decision(X[sv], (r.alpha * y)[sv], r.b, w.kernel, w.gamma, Xt)
-    d_t = S.svm_predict(X[sv], (r.alpha * y)[sv], r.b, w.kernel, w.gamma, Xt, mode=S.PREDICT_TENSOR)
+    Xs, cf = np.ascontiguousarray(X[sv]), (r.alpha * y)[sv]
+    return w, Xs, cf, r.b, Xt, O.decision(Xs, cf, r.b, w.kernel, w.gamma, Xt)
+
+
+@pytest.mark.parametrize("bn", ["128", "256"])
+@pytest.mark.parametrize("expv", ["0", "1", "2", "3", "4"])
+def test_predict_tensor_exp_variants(S, monkeypatch, w5_small_model, expv, bn):
+    """The tensor-core epilogue's exp variants (SVMB200_PREDICT_EXP) and both tile widths
+    (SVMB200_PREDICT_BN: 128 or 256 support vectors per accumulator tile; 700 test rows,
+    a ragged last tile of SVs) all stay within BASELINE.json's 1e-4 of the oracle."""
+    monkeypatch.setenv("SVMB200_PREDICT_EXP", expv)
+    monkeypatch.setenv("SVMB200_PREDICT_BN", bn)
+    w, Xs, cf, b, Xt, d_o = w5_small_model
+    d_t = S.svm_predict(Xs, cf, b, w.kernel, w.gamma, Xt, mode=S.PREDICT_TENSOR)
     assert np.max(np.abs(d_t - d_o)) <= 1e-4
