@@ -140,6 +140,8 @@ struct Params {
     int crw;                       // cluster mode: 16-byte words per record (4 + 2 ceil(crow/3))
     unsigned long long* timers;    // optional [8] per-phase cycle totals of CTA 0
     int poll_ns;                   // > 0: back-off between mailbox polls (tuning)
+    unsigned long long* dbg_ts;    // diagnostic (SVMB200_SKEW_TS = N): per (iteration < N, CTA) {row-pass start, publish} globaltimer, smid
+    int dbg_ts_n;
     int dbg_fast_only;             // diagnostic only (SVMB200_DBG_FAST_ONLY): skip the exp slow phase -- WRONG results, timing probe
     int dp;                        // dense pivot entries in shared memory (>= d; = d_pad unless mixed)
     // Mixed compact rows (SURVEY §8(f) compact encodings): the columns whose values are all
@@ -1107,6 +1109,9 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
                         }
                     }
                 }
+                if (P.dbg_ts && lane == 0 && it < P.dbg_ts_n)
+                    P.dbg_ts[3 * ((long long)it * P.ctas_per_rank * P.world + (long long)rank * P.ctas_per_rank + cta) + 1] =
+                        (unsigned long long)globaltimer();
                 SVM_PHASE(timing, PH_S_PUBLISH);
                 constexpr int PB = 5;                            // records in flight per lane
                 unsigned int rounds = 0;
@@ -1349,6 +1354,13 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
             if (lane == 0) { sh.decision = ST_RUNNING; sh.u = iu; sh.l = il; sh.pass = gainA ? 1 : 0; }
             __syncwarp();
             named_arrive<NSYNC_>(BAR_A);
+            if (P.dbg_ts && lane == 0 && it < P.dbg_ts_n) {
+                unsigned smid;
+                asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+                unsigned long long* e = P.dbg_ts + 3 * ((long long)it * P.ctas_per_rank * P.world + (long long)rank * P.ctas_per_rank + cta);
+                e[0] = (unsigned long long)globaltimer();
+                e[2] = smid;
+            }
             if (lane < 3 && !m_cluster) {
                 unsigned int spins = 0;
                 while (!rec_ok(wa, sq)) {            // written with w0/w1: (almost) never taken

@@ -16,6 +16,7 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <algorithm>
 
 #include "../../include/svmb200.h"
 #include "smo_kernel.cuh"
@@ -948,6 +949,15 @@ int solve(SolveArgs& a) {
     } else if (a.trace_dev && a.dev_cap > 0) {
         P.trace = a.trace_dev; P.hist = a.hist_dev; P.trace_cap = a.dev_cap;
     }
+    unsigned long long* skew_ts = nullptr;
+    if (const char* e = getenv("SVMB200_SKEW_TS")) {
+        const int n_it = atoi(e);
+        const size_t bytes = (size_t)n_it * a.ctas_per_rank * world * 3 * 8;
+        if (n_it > 0 && (rc = dalloc((void**)&skew_ts, bytes)) == SVM_OK) {
+            CKR(cudaMemsetAsync(skew_ts, 0, bytes, st));
+            P.dbg_ts = skew_ts; P.dbg_ts_n = n_it;
+        } else if (n_it > 0) { release(); return rc; }
+    }
     if (want_timers) {
         unsigned long long* tm;
         if ((rc = dalloc((void**)&tm, PH_N * sizeof(unsigned long long)))) { release(); return rc; }
@@ -1029,6 +1039,56 @@ int solve(SolveArgs& a) {
         for (int r = a.rank_base; r < a.rank_base + a.nranks_here; ++r)
             CKR(cudaMemcpyAsync(a.f_out + (a.f_out_global ? a.row_off[r] : 0), P.f[r],
                                 (size_t)a.n_rows[r] * 8, a.f_out_kind, st));
+    }
+    if (skew_ts) {
+        // diagnostic: how far apart the CTAs start their row passes and publish their records
+        const int G = a.ctas_per_rank * world;
+        const long long n_it = hc.it < P.dbg_ts_n ? hc.it : P.dbg_ts_n;
+        std::vector<unsigned long long> h((size_t)P.dbg_ts_n * G * 3);
+        CKR(cudaMemcpyAsync(h.data(), skew_ts, h.size() * 8, cudaMemcpyDeviceToHost, st));
+        CKR(cudaStreamSynchronize(st));
+        std::vector<double> late(G, 0.0), pass(G, 0.0), slate(G, 0.0);
+        double spread_pub = 0, spread_start = 0;
+        long long used = 0;
+        for (long long it = 1; it < n_it; ++it) {           // (iteration 0 starts cold)
+            const unsigned long long* e = h.data() + (size_t)it * G * 3;
+            unsigned long long p0 = ~0ull, p1 = 0, s0 = ~0ull, s1 = 0;
+            bool ok = true;
+            for (int c = 0; c < G; ++c) {
+                if (!e[3 * c] || !e[3 * c + 1]) { ok = false; break; }
+                p0 = std::min(p0, e[3 * c + 1]); p1 = std::max(p1, e[3 * c + 1]);
+                s0 = std::min(s0, e[3 * c]); s1 = std::max(s1, e[3 * c]);
+            }
+            if (!ok) continue;
+            ++used;
+            spread_pub += (double)(p1 - p0); spread_start += (double)(s1 - s0);
+            for (int c = 0; c < G; ++c) {
+                late[c] += (double)(e[3 * c + 1] - p0);
+                slate[c] += (double)(e[3 * c] - s0);
+                pass[c] += (double)(e[3 * c + 1] - e[3 * c]);
+            }
+        }
+        if (used > 0) {
+            std::vector<int> ord(G);
+            for (int c = 0; c < G; ++c) { ord[c] = c; late[c] /= used; pass[c] /= used; slate[c] /= used; }
+            std::sort(ord.begin(), ord.end(), [&](int x, int y) { return late[x] > late[y]; });
+            std::vector<double> ps(pass);
+            std::sort(ps.begin(), ps.end());
+            fprintf(stderr, "[svmb200] skew over %lld iterations (ns): publish spread %.0f, row-pass start spread %.0f, "
+                    "row pass min/median/max %.0f/%.0f/%.0f; latest publishers (cta smid late start_late pass):",
+                    used, spread_pub / used, spread_start / used, ps[0], ps[G / 2], ps[G - 1]);
+            const unsigned long long* e0 = h.data() + (size_t)1 * G * 3;
+            for (int q = 0; q < std::min(G, 12); ++q) {
+                const int c = ord[q];
+                fprintf(stderr, " [%d %llu %.0f %.0f %.0f]", c, e0[3 * c + 2], late[c], slate[c], pass[c]);
+            }
+            fprintf(stderr, " earliest:");
+            for (int q = G - 1; q >= std::max(0, G - 4); --q) {
+                const int c = ord[q];
+                fprintf(stderr, " [%d %llu %.0f %.0f %.0f]", c, e0[3 * c + 2], late[c], slate[c], pass[c]);
+            }
+            fprintf(stderr, "\n");
+        }
     }
     if (P.timers) {
         unsigned long long tm[PH_N];
