@@ -125,7 +125,8 @@ static int predict_tc_launch(const float* X_sv, const double* coef, long long n_
     const size_t smem = (size_t)Cf::STAGES * Cf::STAGE_BYTES;
     auto fn = kernel != SVM_RBF ? k_predict_tc<0, 0, BN_>
             : expv == 0 ? k_predict_tc<1, 0, BN_> : expv == 1 ? k_predict_tc<1, 1, BN_>
-            : expv == 2 ? k_predict_tc<1, 2, BN_> : expv == 3 ? k_predict_tc<1, 3, BN_> : k_predict_tc<1, 4, BN_>;
+            : expv == 2 ? k_predict_tc<1, 2, BN_> : expv == 3 ? k_predict_tc<1, 3, BN_>
+            : expv == 4 ? k_predict_tc<1, 4, BN_> : k_predict_tc<1, 5, BN_>;
     CKR(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     fn<<<(unsigned)(m_pad / BM), NTHREADS, smem, st>>>(pa, pb, qt, qc, k_chunks, (int)(n_pad / Cf::BN), m, b,
                                                         gamma, dec);
@@ -140,7 +141,8 @@ int predict_device_tc(const float* X_sv, const double* coef, long long n_sv, lon
                       int kernel, double gamma, const float* X_test, long long m, double* dec,
                       cudaStream_t st) {
     pool_setup();
-    int expv = 3;            // measured (1M x 284k x 256): 0 1.01 s, 3 0.90 s, 4 1.11 s (BN = 128)
+    int expv = 5;            // measured (1M x 284k x 256): 0 1.01 s, 3 0.90 s, 4 1.11 s (BN = 128);
+                             // BN = 256: 3 0.850 s, 5 0.835 s
     if (const char* e = getenv("SVMB200_PREDICT_EXP")) expv = atoi(e);
     int bn = 256;            // measured with expv 3: BN 128 0.91 s, BN 256 0.85 s
     if (const char* e = getenv("SVMB200_PREDICT_BN")) bn = atoi(e);

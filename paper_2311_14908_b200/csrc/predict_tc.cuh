@@ -37,18 +37,22 @@ constexpr int NPART = EPI_WARPS / 4;              // column parts of an accumula
 constexpr int NTHREADS = 64 + 32 * EPI_WARPS;
 
 // Tile shapes: BN support vectors per accumulator tile (MMA N), BK tf32 elements of K per
-// stage.  BN = 128: 3 stages of 64 KB, two 128-column accumulators (256 TMEM columns);
-// BN = 256: 4 stages of 48 KB, two 256-column accumulators (all 512 columns) -- each
-// stage's A block then feeds twice the MMA work, 25% fewer bytes from L2 per product.
+// stage, NACC accumulators in TMEM (the MMAs of tile j + 1 .. j + NACC - 1 overlap the
+// epilogue of tile j).  BN = 128: 3 stages of 64 KB, 4 accumulators (512 TMEM columns);
+// BN = 256: 4 stages of 48 KB, 2 accumulators (all 512 columns) -- each stage's A block
+// then feeds twice the MMA work of BN = 128, 25% fewer bytes from L2 per product.  (BN is
+// a multiple of 64: the epilogue's 4 column parts load 16 columns at a time.)
 template <int BN_>
 struct TcCfg {
     static constexpr int BN = BN_;
     static constexpr int BK = BN_ == 128 ? 32 : 16;
     static constexpr int STAGES = BN_ == 128 ? 3 : 4;
+    static constexpr int NACC = 512 / BN_;
+    static_assert(BN_ % 64 == 0 && NACC * BN_ <= 512, "tile width");
     static constexpr int A_FLOATS = BM * BK;      // one of A hi / A lo per stage
     static constexpr int B_FLOATS = BN * BK;      // one of B hi / B lo per stage
     static constexpr int STAGE_BYTES = (2 * A_FLOATS + 2 * B_FLOATS) * 4;
-    static constexpr int TMEM_COLS = 2 * BN;
+    static constexpr int TMEM_COLS = 512;         // (a power of two >= NACC * BN)
     static constexpr int SBO = 8 * BK * 4;        // bytes between 8-row groups of a block
     // instruction descriptor: D f32, A/B tf32, both K-major, N = BN, M = BM
     static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
@@ -205,8 +209,45 @@ __device__ __forceinline__ double exp_split(uint32_t dot_bits, double c, double 
     return n < -261376 ? 0.0 : kv;                            // x < -707.5 (n >> 8 >= -1021: v 2^(n >> 8) normal)
 }
 
+// 16 accumulator columns of one test row into its running sum.  FAC (EXPV 5): the row's
+// factor exp(a_t), a_t = -gamma |t|^2, is left out of every kernel value and applied once
+// to the row's sum (one fp64 add fewer per (row, SV)); the caller takes it only when
+// a_t >= -600 for all rows of the warp, so exp(x - a_t) <= exp(600) stays finite.
+template <int KERNEL, int EXPV, bool FAC>
+__device__ __forceinline__ void epi16(const uint32_t (&v)[16], const double2* __restrict__ qc_c, double a_t,
+                                      double g2, const double* __restrict__ t64, double& acc_d) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        double kv;
+        const double2 sc = qc_c[j];             // {-gamma |s|^2, coef}: one 16-byte load
+        if (KERNEL == 1 && EXPV >= 3) {
+            kv = exp_split<EXPV == 4>(v[j], FAC ? sc.x : a_t + sc.x, g2, t64);
+        } else if (KERNEL == 1) {
+            // fp32 accumulator -> fp64 by integer ops (the fp64 pipe is shared with
+            // the tensor cores): rebias the exponent, widen the mantissa; 0 stays 0
+            // (the dot of fp32 data is never subnormal unless 0 or a cancellation
+            // below 2^-126, whose exp(.) contribution is 1 either way)
+            const uint32_t fb = v[j];
+            const uint32_t ex = (fb >> 23) & 0xffu;
+            const uint32_t hi = ex == 0u ? (fb & 0x80000000u)
+                                         : ((fb & 0x80000000u) | ((ex + 896u) << 20) | ((fb >> 3) & 0xfffffu));
+            const uint32_t lo = ex == 0u ? 0u : (fb << 29);
+            const double dot = __hiloint2double((int)hi, (int)lo);
+            // (x > 0 by rounding, when t ~ s, gives K = 1 + O(1e-16): not clamped)
+            const double x = fma(g2, dot, a_t + sc.x);
+            if (EXPV == 0) kv = exp(x);
+            else if (EXPV == 1) kv = exp_nonpos(x, t64);
+            else kv = exp_nonpos_poly(x);
+        } else {
+            kv = (double)__uint_as_float(v[j]);
+        }
+        acc_d = fma(sc.y, kv, acc_d);
+    }
+}
+
 // EXPV: the epilogue's exp -- 0 CUDA's fp64 exp, 1 table-driven (exp_nonpos), 2 polynomial,
-// 3 exp_split with F2F conversions, 4 exp_split with integer conversions.  BN_: TcCfg.
+// 3 exp_split with F2F conversions, 4 exp_split with integer conversions, 5 exp_split with
+// the row factor exp(-gamma |t|^2) applied once per row (epi16 FAC).  BN_: TcCfg.
 template <int KERNEL, int EXPV, int BN_>
 __global__ void __launch_bounds__(NTHREADS, 1)
 k_predict_tc(const float* __restrict__ A,   // packed test rows [m_tiles][k_chunks][2][BM*BK]
@@ -216,11 +257,11 @@ k_predict_tc(const float* __restrict__ A,   // packed test rows [m_tiles][k_chun
              int k_chunks, int n_tiles, long long m, double b, double gamma,
              double* __restrict__ dec) {
     using Cf = TcCfg<BN_>;
-    constexpr int BN = Cf::BN, BK = Cf::BK, STAGES = Cf::STAGES, TMEM_COLS = Cf::TMEM_COLS;
+    constexpr int BN = Cf::BN, BK = Cf::BK, STAGES = Cf::STAGES, TMEM_COLS = Cf::TMEM_COLS, NACC = Cf::NACC;
     constexpr int AF = Cf::A_FLOATS, BF = Cf::B_FLOATS;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     float* stage_base = reinterpret_cast<float*>(smem_raw);
-    __shared__ uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
+    __shared__ uint64_t full[STAGES], empty[STAGES], tfull[NACC], tempty[NACC];
     __shared__ uint32_t tmem_base_sh;
     __shared__ double part_sh[NPART][BM];           // the column parts' partial sums
     __shared__ double t64[256];                     // 2^(j / 64) (exp_nonpos), 2^(j / 256) (exp_split)
@@ -230,7 +271,7 @@ k_predict_tc(const float* __restrict__ A,   // packed test rows [m_tiles][k_chun
     const int mt = blockIdx.x;
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], EPI_WARPS); }
+        for (int a = 0; a < NACC; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], EPI_WARPS); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -267,9 +308,9 @@ k_predict_tc(const float* __restrict__ A,   // packed test rows [m_tiles][k_chun
         int slot = 0;
         uint32_t par = 0;
         for (int nt = 0; nt < n_tiles; ++nt) {
-            const int acc = nt & 1;
+            const int acc = nt % NACC;
             const uint32_t tacc = tmem + acc * BN;
-            if (nt >= 2) mbar_wait(&tempty[acc], ((nt >> 1) - 1) & 1);
+            if (nt >= NACC) mbar_wait(&tempty[acc], ((nt / NACC) - 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             for (int kc = 0; kc < k_chunks; ++kc) {
                 mbar_wait(&full[slot], par);
@@ -310,10 +351,11 @@ k_predict_tc(const float* __restrict__ A,   // packed test rows [m_tiles][k_chun
         const double q_t = qt[(long long)mt * BM + row];
         const double a_t = -gamma * q_t;
         const double g2 = 2.0 * gamma;
+        const bool fac = KERNEL == 1 && EXPV == 5 && __all_sync(0xffffffffu, a_t >= -600.0);
         double acc_d = 0.0;
         for (int nt = 0; nt < n_tiles; ++nt) {
-            const int acc = nt & 1;
-            mbar_wait(&tfull[acc], (nt >> 1) & 1);
+            const int acc = nt % NACC;
+            mbar_wait(&tfull[acc], (nt / NACC) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const double2* qc_t = qc + (size_t)nt * BN;
 #pragma unroll 1
@@ -331,33 +373,8 @@ k_predict_tc(const float* __restrict__ A,   // packed test rows [m_tiles][k_chun
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 // fully unrolled: v[j] must index registers (a partial unroll put v in local
                 // memory -- STL/LDL per element)
-#pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    double kv;
-                    const double2 sc = qc_t[c0 + j];             // {-gamma |s|^2, coef}: one 16-byte load
-                    if (KERNEL == 1 && EXPV >= 3) {
-                        kv = exp_split<EXPV == 4>(v[j], a_t + sc.x, g2, t64);
-                    } else if (KERNEL == 1) {
-                        // fp32 accumulator -> fp64 by integer ops (the fp64 pipe is shared with
-                        // the tensor cores): rebias the exponent, widen the mantissa; 0 stays 0
-                        // (the dot of fp32 data is never subnormal unless 0 or a cancellation
-                        // below 2^-126, whose exp(.) contribution is 1 either way)
-                        const uint32_t fb = v[j];
-                        const uint32_t ex = (fb >> 23) & 0xffu;
-                        const uint32_t hi = ex == 0u ? (fb & 0x80000000u)
-                                                     : ((fb & 0x80000000u) | ((ex + 896u) << 20) | ((fb >> 3) & 0xfffffu));
-                        const uint32_t lo = ex == 0u ? 0u : (fb << 29);
-                        const double dot = __hiloint2double((int)hi, (int)lo);
-                        // (x > 0 by rounding, when t ~ s, gives K = 1 + O(1e-16): not clamped)
-                        const double x = fma(g2, dot, a_t + sc.x);
-                        if (EXPV == 0) kv = exp(x);
-                        else if (EXPV == 1) kv = exp_nonpos(x, t64);
-                        else kv = exp_nonpos_poly(x);
-                    } else {
-                        kv = (double)__uint_as_float(v[j]);
-                    }
-                    acc_d = fma(sc.y, kv, acc_d);
-                }
+                if (fac) epi16<KERNEL, EXPV, true>(v, qc_t + c0, a_t, g2, t64, acc_d);
+                else epi16<KERNEL, EXPV, false>(v, qc_t + c0, a_t, g2, t64, acc_d);
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
@@ -369,7 +386,7 @@ k_predict_tc(const float* __restrict__ A,   // packed test rows [m_tiles][k_chun
         if (half == 0 && gi < m) {
             double sum = acc_d;
             for (int p = 1; p < NPART; ++p) sum += part_sh[p][row];
-            dec[gi] = sum + b;
+            dec[gi] = (fac ? sum * exp(a_t) : sum) + b;
         }
     }
     __syncthreads();

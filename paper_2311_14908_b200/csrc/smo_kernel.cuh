@@ -49,7 +49,7 @@ constexpr int NTHREADS = NT + 64;  // + scalar warp + producer warp
 constexpr int NSYNC = NT + 32;     // participants of the named barriers
 constexpr int MAX_STAGES = 16;
 constexpr int MIX_MAXSEG = 8;      // mixed rows: at most this many runs of continuous / binary columns
-enum { BAR_A = 1, BAR_B = 2, BAR_C = 3, BAR_D = 4 };
+enum { BAR_A = 1, BAR_B = 2, BAR_C = 3, BAR_D = 4, BAR_E = 5 };
 
 enum { ST_RUNNING = 0, ST_CONVERGED = 1, ST_MAXITER = 2, ST_LIMIT = 3, ST_TIMEOUT = -8 };
 enum { FL_POS = 1, FL_UP = 2, FL_LOW = 4 };
@@ -142,7 +142,9 @@ struct Params {
     int poll_ns;                   // > 0: back-off between mailbox polls (tuning)
     unsigned long long* dbg_ts;    // diagnostic (SVMB200_SKEW_TS = N): per (iteration < N, CTA) {row-pass start, publish} globaltimer, smid
     int dbg_ts_n;
-    int dbg_fast_only;             // diagnostic only (SVMB200_DBG_FAST_ONLY): skip the exp slow phase -- WRONG results, timing probe
+    int dbg_fast_only;
+    int xch_dup;                   // >= 1, test hook (one process): every record also stored in xch_dup - 1 more
+                                   // slots, so one GPU polls as many records as xch_dup GPUs would             // diagnostic only (SVMB200_DBG_FAST_ONLY): skip the exp slow phase -- WRONG results, timing probe
     int dp;                        // dense pivot entries in shared memory (>= d; = d_pad unless mixed)
     // Mixed compact rows (SURVEY §8(f) compact encodings): the columns whose values are all
     // exactly 0 or 1 are stored as bits, the others as fp32.  A row of xblk holds mix_nc fp32
@@ -322,6 +324,8 @@ struct Shared {
     double red_a[2][16];           // ... and their alpha when alpha lives in HBM (read by the
                                    // consumer warps, off the scalar warp's critical path)
     int red_i[2][16];
+    double wp_f[2][16];            // wide poll: per consumer warp best (f, global row, record)
+    int wp_i[2][16], wp_g[2][16];
     int c_hit, c_su, c_sl;         // row cache: both rows cached / their slots
     int c_fill_u, c_fill_l;        // row cache: the slot this iteration fills (miss), else -1
     int lru_head, lru_tail;        // row cache: most / least recently used slot
@@ -478,6 +482,54 @@ __device__ __forceinline__ bool poll_records(const uint4* w0, const uint4* w1, i
                 if (il != INT_MAX && better_low(fl, il, b.fl, b.il)) { b.fl = fl; b.il = il; b.gl = g; }
             }
         tmo = __any_sync(0xffffffffu, tmo);
+    }
+    return tmo;
+}
+
+// The wide poll (g_total > 160 records, i.e. several GPUs): every consumer thread polls
+// records first, first + stride, ... (up to MAXR loads in flight), re-reading the ones not
+// yet written by exchange sq, and keeps the best up / low candidate it saw with its record.
+// The consumers are idle during the exchange; one warp polling 1,184 records (8 GPUs x 148
+// CTAs) would need 8 sequential rounds of loads.  Returns true on timeout (this thread).
+template <int MAXR>
+__device__ __forceinline__ bool poll_slice(const uint4* w0, const uint4* w1, int g_total, uint32_t sq,
+                                           int sys, long long timeout_ns, int first, int stride, Sel& b) {
+    b.fu = __longlong_as_double(0x7ff0000000000000ll); b.fl = -b.fu;
+    b.iu = INT_MAX; b.il = INT_MAX; b.gu = 0; b.gl = 0;
+    bool tmo = false;
+    long long t0 = 0;
+    unsigned int spins = 0;
+    for (int g0 = first; g0 < g_total && !tmo; g0 += MAXR * stride) {
+        uint4 v[MAXR][2];
+        unsigned pend = 0;
+#pragma unroll
+        for (int q = 0; q < MAXR; ++q) if (g0 + q * stride < g_total) pend |= 1u << q;
+        const unsigned mine = pend;
+        while (pend) {
+#pragma unroll
+            for (int q = 0; q < MAXR; ++q)
+                if (pend & (1u << q)) {
+                    v[q][0] = rec_load(w0 + g0 + q * stride, sys);
+                    v[q][1] = rec_load(w1 + g0 + q * stride, sys);
+                }
+#pragma unroll
+            for (int q = 0; q < MAXR; ++q)
+                if ((pend & (1u << q)) && rec_ok(v[q][0], sq) && rec_ok(v[q][1], sq)) pend &= ~(1u << q);
+            if (pend && (++spins & 255u) == 0) {
+                const long long now = globaltimer();
+                if (t0 == 0) t0 = now;
+                else if (now - t0 > timeout_ns) { tmo = true; break; }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < MAXR; ++q)
+            if (mine & (1u << q)) {
+                const int g = g0 + q * stride;
+                const int iu = rec_idx(v[q][0]), il = rec_idx(v[q][1]);
+                const double fu = rec_f64(v[q][0]), fl = rec_f64(v[q][1]);
+                if (iu != INT_MAX && better_up(fu, iu, b.fu, b.iu)) { b.fu = fu; b.iu = iu; b.gu = g; }
+                if (il != INT_MAX && better_low(fl, il, b.fl, b.il)) { b.fl = fl; b.il = il; b.gl = g; }
+            }
     }
     return tmo;
 }
@@ -690,7 +742,9 @@ __device__ __forceinline__ void dict_rows(int kc, const unsigned char* stb, int 
 // BINCL: the kernel specialised for binary rows resident in a thread-block cluster (the
 // latency-bound small-problem path): the other modes compile out, so the per-iteration code
 // is short (instruction-cache resident).
-template <int KERNEL, int RPT, bool A_SMEM, bool BINCL, int NTC = NT, bool WSS2 = false>
+// WIDE: the consumer warps poll the exchange records (several GPUs: > 320 records; a
+// separate instantiation, since its registers slow the single-GPU kernels)
+template <int KERNEL, int RPT, bool A_SMEM, bool BINCL, int NTC = NT, bool WSS2 = false, bool WIDE = false>
 __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
     // NTC consumer threads (8 or 16 warps), then the scalar and the producer warp
     constexpr int NT_ = NTC, NWC_ = NTC / 32, SCALAR_ = NWC_, PRODUCER_ = NWC_ + 1;
@@ -920,6 +974,36 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
         if (!is_scalar) {
             // consumers: the scalar warp runs the exchange, the selection, the stopping test,
             // the row-cache directory and the pivot gather, then releases barrier A
+            if constexpr (WIDE) {
+                // wide poll: the consumers poll the records (the scalar warp publishes this
+                // CTA's record meanwhile), each warp hands its best up / low candidate over
+                const int g_total = xworld * P.ctas_per_rank * P.xch_dup;
+                const int par = (int)(seq & 1);
+                Sel b;
+                const bool to = poll_slice<4>(mbox_words(my_mb, par, 0, g_total), mbox_words(my_mb, par, 1, g_total),
+                                              g_total, (uint32_t)seq & 0xffffu, P.sys_scope, P.timeout_ns, t, NTC, b);
+                unsigned long long kwu, kwl;
+                unsigned iwu, iwl;
+                argmin_redux(0xffffffffu, b.iu == INT_MAX ? ~0ull : fkey(b.fu), b.iu == INT_MAX ? 0xffffffffu : (unsigned)b.iu,
+                             kwu, iwu);
+                argmin_redux(0xffffffffu, b.il == INT_MAX ? ~0ull : ~fkey(b.fl), b.il == INT_MAX ? 0xffffffffu : (unsigned)b.il,
+                             kwl, iwl);
+                const unsigned mu = __ballot_sync(0xffffffffu, b.iu != INT_MAX && (unsigned)b.iu == iwu);
+                const unsigned ml = __ballot_sync(0xffffffffu, b.il != INT_MAX && (unsigned)b.il == iwl);
+                const int gu = __shfl_sync(0xffffffffu, b.gu, mu ? __ffs(mu) - 1 : 0);
+                const int gl = __shfl_sync(0xffffffffu, b.gl, ml ? __ffs(ml) - 1 : 0);
+                const bool any_to = __any_sync(0xffffffffu, to);
+                if (lane == 0) {
+                    sh.wp_i[0][warp] = iwu == 0xffffffffu ? INT_MAX : (int)iwu;
+                    sh.wp_f[0][warp] = iwu == 0xffffffffu ? INF : fkey_inv(kwu);
+                    sh.wp_g[0][warp] = gu;
+                    sh.wp_i[1][warp] = iwl == 0xffffffffu ? INT_MAX : (int)iwl;
+                    sh.wp_f[1][warp] = iwl == 0xffffffffu ? -INF : fkey_inv(~kwl);
+                    sh.wp_g[1][warp] = gl;
+                    if (any_to) sh.timeout = 1;
+                }
+                named_sync<NSYNC_>(BAR_E);
+            }
             named_sync<NSYNC_>(BAR_A);
             SVM_PHASE(timing, PH_C_EXCH);
             const int dec = sh.decision;
@@ -932,7 +1016,7 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
             // No fences or counters: a record word whose sequence number and checksum match
             // is complete.  Measured against counter- and tree-based exchanges in
             // tools/xch2_bench.cu.
-            const int g_total = xworld * P.ctas_per_rank;
+            const int g_total = xworld * P.ctas_per_rank * P.xch_dup;
             const int par = (int)(seq & 1);
             const uint32_t sq = (uint32_t)seq & 0xffffu;
             double fu, fl;
@@ -1086,9 +1170,19 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
                 }
                 Sel best;
                 const int gcta = (rank - xbase) * P.ctas_per_rank + cta;
-                if (lane < 4 * xworld)
-                    rec_store(mbox_words(P.mbox[xbase + (lane >> 2)], par, lane & 3, g_total) + gcta,
-                              rec_word(c, lane & 3, sq), P.sys_scope);
+                if (P.xch_dup == 1) {
+                    if (lane < 4 * xworld)
+                        rec_store(mbox_words(P.mbox[xbase + (lane >> 2)], par, lane & 3, g_total) + gcta,
+                                  rec_word(c, lane & 3, sq), P.sys_scope);
+                } else {
+                    // (test hook) copy k of the record in slot gcta + k * xworld * ctas_per_rank
+                    for (int e = lane; e < 4 * xworld * P.xch_dup; e += 32) {
+                        const int rr = (e >> 2) % xworld, k = (e >> 2) / xworld;
+                        rec_store(mbox_words(P.mbox[xbase + rr], par, e & 3, g_total) + gcta +
+                                      k * xworld * P.ctas_per_rank,
+                                  rec_word(c, e & 3, sq), P.sys_scope);
+                    }
+                }
                 // warm L2 with this CTA's candidate rows: the two winners' rows are gathered
                 // from the row-major replica right after the selection (the critical path)
                 if (m_mixed && P.xcomp && m_cache == 0) {
@@ -1115,9 +1209,22 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
                 SVM_PHASE(timing, PH_S_PUBLISH);
                 constexpr int PB = 5;                            // records in flight per lane
                 unsigned int rounds = 0;
-                tmo = poll_records<PB>(mbox_words(my_mb, par, 0, g_total), mbox_words(my_mb, par, 1, g_total),
-                                       g_total, sq, P.sys_scope, P.timeout_ns, lane, best, rounds) ||
-                      sh.timeout != 0;
+                if constexpr (WIDE) {
+                    // the consumer warps polled: lane w takes warp w's candidates
+                    named_sync<NSYNC_>(BAR_E);
+                    const bool has = lane < NWC_;
+                    best.iu = has ? sh.wp_i[0][lane] : INT_MAX;
+                    best.fu = has ? sh.wp_f[0][lane] : INF;
+                    best.gu = has ? sh.wp_g[0][lane] : 0;
+                    best.il = has ? sh.wp_i[1][lane] : INT_MAX;
+                    best.fl = has ? sh.wp_f[1][lane] : -INF;
+                    best.gl = has ? sh.wp_g[1][lane] : 0;
+                    tmo = sh.timeout != 0;
+                } else {
+                    tmo = poll_records<PB>(mbox_words(my_mb, par, 0, g_total), mbox_words(my_mb, par, 1, g_total),
+                                           g_total, sq, P.sys_scope, P.timeout_ns, lane, best, rounds) ||
+                          sh.timeout != 0;
+                }
                 if (timing) ph_acc[PH_C_PIVOT] += rounds;     // (timers only) poll rounds of lane 0
                 SVM_PHASE(timing, PH_S_POLL);
                 // the warp's winners (lexicographic (f, index) minimum / maximum through three

@@ -504,29 +504,36 @@ int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl, bool bina
 
 typedef void (*KernelFn)(const Params);
 
+template <int K, bool W>
+KernelFn pick_rpt_w(int rpt, bool a_smem, int ntc) {
+    if (ntc == 512) {
+        if (a_smem) return rpt == 2 ? smo_persistent<K, 2, true, false, 512, false, W> : smo_persistent<K, 1, true, false, 512, false, W>;
+        return rpt == 2 ? smo_persistent<K, 2, false, false, 512, false, W> : smo_persistent<K, 1, false, false, 512, false, W>;
+    }
+    if (a_smem) return rpt == 4 ? smo_persistent<K, 4, true, false, NT, false, W> : rpt == 2 ? smo_persistent<K, 2, true, false, NT, false, W> : smo_persistent<K, 1, true, false, NT, false, W>;
+    return rpt == 4 ? smo_persistent<K, 4, false, false, NT, false, W> : rpt == 2 ? smo_persistent<K, 2, false, false, NT, false, W> : smo_persistent<K, 1, false, false, NT, false, W>;
+}
+
+// wide: the consumer-warp record poll (WIDE instantiations; not for wss 2)
 template <int K>
-KernelFn pick_rpt(int rpt, bool a_smem, int ntc, bool wss2 = false) {
+KernelFn pick_rpt(int rpt, bool a_smem, int ntc, bool wss2 = false, bool wide = false) {
     if (wss2) {                                            // second-order selection: 256 consumers
         if (a_smem) return rpt == 4 ? smo_persistent<K, 4, true, false, NT, true> : rpt == 2 ? smo_persistent<K, 2, true, false, NT, true> : smo_persistent<K, 1, true, false, NT, true>;
         return rpt == 4 ? smo_persistent<K, 4, false, false, NT, true> : rpt == 2 ? smo_persistent<K, 2, false, false, NT, true> : smo_persistent<K, 1, false, false, NT, true>;
     }
-    if (ntc == 512) {
-        if (a_smem) return rpt == 2 ? smo_persistent<K, 2, true, false, 512> : smo_persistent<K, 1, true, false, 512>;
-        return rpt == 2 ? smo_persistent<K, 2, false, false, 512> : smo_persistent<K, 1, false, false, 512>;
-    }
-    if (a_smem) return rpt == 4 ? smo_persistent<K, 4, true, false> : rpt == 2 ? smo_persistent<K, 2, true, false> : smo_persistent<K, 1, true, false>;
-    return rpt == 4 ? smo_persistent<K, 4, false, false> : rpt == 2 ? smo_persistent<K, 2, false, false> : smo_persistent<K, 1, false, false>;
+    return wide ? pick_rpt_w<K, true>(rpt, a_smem, ntc) : pick_rpt_w<K, false>(rpt, a_smem, ntc);
 }
 
 KernelFn pick_bincl(int kernel) { return kernel == SVM_RBF ? smo_bincl<1> : smo_bincl<0>; }
 
 // bincl: binary rows resident in a cluster (the specialised kernel; rpt is 1 there)
-KernelFn pick_kernel(int kernel, int rpt, bool a_smem, bool bincl = false, int ntc = NT, bool wss2 = false) {
+KernelFn pick_kernel(int kernel, int rpt, bool a_smem, bool bincl = false, int ntc = NT, bool wss2 = false,
+                     bool wide = false) {
     if (bincl && getenv("SVMB200_NO_SPECIALISE") == nullptr) {
         if (kernel == SVM_RBF) return a_smem ? smo_persistent<1, 1, true, true> : smo_persistent<1, 1, false, true>;
         return a_smem ? smo_persistent<0, 1, true, true> : smo_persistent<0, 1, false, true>;
     }
-    return kernel == SVM_RBF ? pick_rpt<1>(rpt, a_smem, ntc, wss2) : pick_rpt<0>(rpt, a_smem, ntc, wss2);
+    return kernel == SVM_RBF ? pick_rpt<1>(rpt, a_smem, ntc, wss2, wide) : pick_rpt<0>(rpt, a_smem, ntc, wss2, wide);
 }
 
 int device_limits(int* n_sm, int* max_smem) {
@@ -762,23 +769,38 @@ int solve(SolveArgs& a) {
         if (a.p.cluster > 0 && pl.cluster == 0)
             return fail(SVM_EINVAL, "cluster mode needs every rank's rows resident in the cluster's shared memory");
     }
+    // (test hook SVMB200_XCH_DUP = k, one process: every record also lands in k - 1 more slots,
+    // so one GPU polls as many records as k GPUs would)
+    int xch_dup = 1;
+    if (const char* e = getenv("SVMB200_XCH_DUP")) xch_dup = std::max(1, std::min(16, atoi(e)));
+    if (!a.mbox_local_alloc) xch_dup = 1;
+    // the record poll: one warp (<= 320 records: one GPU, or two) or every consumer warp (more
+    // GPUs; measured with SVMB200_XCH_DUP = 8, 1,184 records: a 125k-row W5 shard 42.5 -> 38.1
+    // us/iteration, W4 31.8 -> 25.4; at 148 records one warp is faster).  SVMB200_WIDE_POLL =
+    // 1 / 0 forces it on / off (not with wss 2 or the cluster exchange).
+    const long long n_records = (long long)(a.independent ? 1 : a.world) * a.ctas_per_rank * xch_dup;
+    bool wide = n_records > 320;
+    if (const char* e = getenv("SVMB200_WIDE_POLL")) wide = atoi(e) != 0;
+    wide = wide && p.wss != 2 && pl.cluster == 0 && !pl.bincl;
     KernelFn fn = pl.bincl ? pick_bincl(p.kernel)
                            : pick_kernel(p.kernel, pl.rpt, pl.alpha_smem, pl.cluster > 0 && pl.bin_words > 0, pl.ntc,
-                                         p.wss == 2);
+                                         p.wss == 2, wide);
     const int nthreads = pl.bincl ? NTB : pl.ntc + 64;
     {
         const char* mode = gram ? "gram" : pl.bin_words ? "binary-resident"
                          : pl.mix_nseg ? (pl.resident ? "mixed-resident" : pl.cache_slots ? "mixed+row-cache" : "mixed-streamed")
                          : pl.esz == 1 ? (pl.resident ? "dict-resident" : pl.cache_slots ? "dict+row-cache" : "dict-streamed")
                          : pl.resident ? "float-resident" : pl.cache_slots ? "streamed+row-cache" : "streamed";
-        char buf[320];
+        char buf[400];
         snprintf(buf, sizeof buf,
                  "{\"kernel\": \"%s<%d%s>\", \"ctas_per_rank\": %d, \"ranks\": %d, \"cluster\": %d, "
-                 "\"mode\": \"%s\", \"threads\": %d, \"smem\": %zu, \"rows_per_cta\": %d, \"cache_slots\": %d}",
+                 "\"mode\": \"%s\", \"threads\": %d, \"smem\": %zu, \"rows_per_cta\": %d, \"cache_slots\": %d, "
+                 "\"poll\": \"%s\"}",
                  pl.bincl ? "smo_bincl" : "smo_persistent", p.kernel,
                  pl.bincl ? "" : (std::string(",") + std::to_string(pl.rpt) + (pl.alpha_smem ? ",1" : ",0") +
                                   ((pl.cluster > 0 && pl.bin_words > 0) ? ",1" : ",0")).c_str(),
-                 a.ctas_per_rank, a.nranks_here, pl.cluster, mode, nthreads, pl.smem, pl.state_cap, pl.cache_slots);
+                 a.ctas_per_rank, a.nranks_here, pl.cluster, mode, nthreads, pl.smem, pl.state_cap, pl.cache_slots,
+                 pl.cluster > 0 || pl.bincl ? "cluster" : wide ? "wide" : "warp");
         g_plan = buf;
     }
     CKR(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
@@ -791,7 +813,7 @@ int solve(SolveArgs& a) {
 
     cudaStream_t st = a.stream;
     const int world = a.world;
-    const size_t mbox_bytes = svmk::mbox_bytes(a.ctas_per_rank, world);
+    const size_t mbox_bytes = svmk::mbox_bytes(a.ctas_per_rank * xch_dup, world);
 
     // ---- per-rank device state (a1)
     std::vector<void*> owned;
@@ -834,6 +856,7 @@ int solve(SolveArgs& a) {
     P.wss = p.wss;
     if (const char* e = getenv("SVMB200_POLL_NS")) P.poll_ns = atoi(e);
     if (const char* e = getenv("SVMB200_DBG_FAST_ONLY")) P.dbg_fast_only = atoi(e);
+    P.xch_dup = xch_dup;
     // L2 residency of streamed X: keep the first tiles of every CTA block in L2
     // (SVMB200_L2_KEEP_MB, per GPU; tuning)
     if (!pl.resident && pl.bin_words == 0 && !gram && pl.mix_nseg == 0 && pl.esz == 4) {

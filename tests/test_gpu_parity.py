@@ -611,7 +611,7 @@ def w5_small_model():
 
 
 @pytest.mark.parametrize("bn", ["128", "256"])
-@pytest.mark.parametrize("expv", ["0", "1", "2", "3", "4"])
+@pytest.mark.parametrize("expv", ["0", "1", "2", "3", "4", "5"])
 def test_predict_tensor_exp_variants(S, monkeypatch, w5_small_model, expv, bn):
     """The tensor-core epilogue's exp variants (SVMB200_PREDICT_EXP) and both tile widths
     (SVMB200_PREDICT_BN: 128 or 256 support vectors per accumulator tile; 700 test rows,
@@ -621,3 +621,34 @@ def test_predict_tensor_exp_variants(S, monkeypatch, w5_small_model, expv, bn):
     w, Xs, cf, b, Xt, d_o = w5_small_model
     d_t = S.svm_predict(Xs, cf, b, w.kernel, w.gamma, Xt, mode=S.PREDICT_TENSOR)
     assert np.max(np.abs(d_t - d_o)) <= 1e-4
+
+
+def test_predict_tensor_row_factor_fallback(S, monkeypatch, w5_small_model):
+    """Epilogue variant 5 takes exp(-gamma |t|^2) out of every kernel value only for warps
+    whose rows all have gamma |t|^2 <= 600 (so exp(x + gamma |t|^2) stays finite).  Test
+    rows shifted far from the origin (gamma |t|^2 ~ 10^3; the kernel values are unchanged)
+    take the fallback, which is variant 3's arithmetic: bit-identical results; unshifted
+    rows take the factored form and agree with variant 3 to rounding."""
+    w, Xs, cf, b, Xt, _ = w5_small_model
+    shift = np.float32(np.sqrt(1000.0 / (w.gamma * Xs.shape[1])))
+    res = {}
+    for v in ("3", "5"):
+        monkeypatch.setenv("SVMB200_PREDICT_EXP", v)
+        res[v] = (S.svm_predict(Xs + shift, cf, b, w.kernel, w.gamma, Xt + shift, mode=S.PREDICT_TENSOR),
+                  S.svm_predict(Xs, cf, b, w.kernel, w.gamma, Xt, mode=S.PREDICT_TENSOR))
+    assert np.array_equal(res["3"][0], res["5"][0])
+    assert np.max(np.abs(res["3"][1] - res["5"][1])) <= 1e-10
+
+
+@pytest.mark.parametrize("name,n,vr,ctas", [("W5", 2500, 1, 0), ("W5", 2500, 4, 0), ("W4", 6000, 1, 0),
+                                             ("W3", 1500, 2, 0), ("W5", 2500, 3, 17)])
+def test_wide_poll_parity(S, monkeypatch, name, n, vr, ctas):
+    """The wide record poll (every consumer thread polls a slice of the records; the
+    automatic choice above 160 records, i.e. several GPUs) forced on one GPU: the same
+    trajectory, alpha, f and b as the oracle, with virtual ranks and ragged CTA counts."""
+    monkeypatch.setenv("SVMB200_WIDE_POLL", "1")
+    w = W.get(name)
+    X, y = w.train(n)
+    r_g, r_or = _run_pair(S, w, X, y, virtual_ranks=vr, ctas=ctas, cluster=-1)
+    assert S.last_plan()["cluster"] == 0
+    _assert_exact(r_g, r_or)

@@ -1,0 +1,14 @@
+# wide poll as its own instantiation: single-GPU timings back to baseline?  8x-record timings; tests
+OUT=gpurun_out/r3l
+mkdir -p $OUT
+for rep in 1 2; do
+  echo "== default" >> $OUT/xch.txt
+  SVMB200_PHASE_TIMERS=0 timeout 300 python tools/phase_probe.py W4:20000 W5@125000:5000 W5:1500 W3:0 >> $OUT/xch.txt 2>&1
+  for dup in 4 8; do
+  for wp in 0 1; do
+    echo "== dup=$dup wide_poll=$wp" >> $OUT/xch.txt
+    SVMB200_XCH_DUP=$dup SVMB200_WIDE_POLL=$wp SVMB200_PHASE_TIMERS=0 timeout 300 python tools/phase_probe.py W5@125000:5000 W4:10000 >> $OUT/xch.txt 2>&1
+  done
+  done
+done
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_boundary.py -q -x > $OUT/pytest.log 2>&1; echo rc=$? >> $OUT/pytest.log
