@@ -331,6 +331,11 @@ struct Shared {
     int lru_head, lru_tail;        // row cache: most / least recently used slot
     int kul_cnt;                   // compacted terms of K(x_u, x_l) (cache mode)
     int timeout;
+    // phase timers (diagnostic): consumer thread 0 uses row 0, the scalar warp's lane 0 row 1
+    // (in shared memory, not registers: 14 accumulators live across the whole solve loop
+    // cost the row pass registers even when timing is off)
+    unsigned long long ph_acc[2][PH_N];
+    long long ph_t[2];
     unsigned long long bars[2 * MAX_STAGES];
     double exp_tab[svmexp::EXP_TABLE_DOUBLES];
 };
@@ -425,8 +430,8 @@ __device__ __forceinline__ uint4 rec_load(const uint4* p, int sys) {
         if (on) {                                                            \
             (void)*(volatile int*)&sh.decision;                              \
             const long long c_ = clock64();                                  \
-            ph_acc[ph] += (unsigned long long)(c_ - ph_t);                   \
-            ph_t = c_;                                                       \
+            sh.ph_acc[ph_row][ph] += (unsigned long long)(c_ - sh.ph_t[ph_row]); \
+            sh.ph_t[ph_row] = c_;                                            \
         }                                                                    \
     } while (0)
 
@@ -752,9 +757,11 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
     static_assert(NWC_ <= 16, "at most 16 consumer warps");
     // mode switches: compile-time constants in the BINCL specialisation
     const bool m_cluster = BINCL || P.cluster != 0;
-    const bool m_isbin = BINCL || P.bin_words > 0;
+    // (the 16-warp instantiations never hold binary-resident rows or a row cache: the plan
+    // takes 8 warps for those, and compiling them out spares the row pass registers)
+    const bool m_isbin = BINCL || (NTC != 512 && P.bin_words > 0);
     const double* const m_gram = BINCL ? nullptr : P.gram;
-    const int m_cache = BINCL ? 0 : P.cache_slots;
+    const int m_cache = (BINCL || NTC == 512) ? 0 : P.cache_slots;
     const bool m_resident = BINCL || P.resident != 0;
     constexpr bool m_wss2 = WSS2 && !BINCL;                 // second-order working set (NEXT-2):
                                                             // its own instantiations, so the
@@ -921,10 +928,13 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
         return;
     }
 
-    unsigned long long ph_acc[PH_N] = {};
-    long long ph_t = clock64();
     const bool is_scalar = (warp == SCALAR_);
     const bool timing = P.timers != nullptr && blockIdx.x == 0 && (t == 0 || (is_scalar && lane == 0));
+    const int ph_row = is_scalar ? 1 : 0;
+    if (timing) {
+        for (int k = 0; k < PH_N; ++k) sh.ph_acc[ph_row][k] = 0;
+        sh.ph_t[ph_row] = clock64();
+    }
     int final_state = ST_RUNNING;
     Ctl* ctl = P.ctl[rank];
     Mailbox* my_mb = P.mbox[rank];
@@ -1225,7 +1235,7 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
                                            g_total, sq, P.sys_scope, P.timeout_ns, lane, best, rounds) ||
                           sh.timeout != 0;
                 }
-                if (timing) ph_acc[PH_C_PIVOT] += rounds;     // (timers only) poll rounds of lane 0
+                if (timing) sh.ph_acc[ph_row][PH_C_PIVOT] += rounds;     // (timers only) poll rounds of lane 0
                 SVM_PHASE(timing, PH_S_POLL);
                 // the warp's winners (lexicographic (f, index) minimum / maximum through three
                 // redux.sync on the order-preserving key, R22) and the records they came from
@@ -1952,7 +1962,7 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
         }
     }
     if (timing)
-        for (int k = 0; k < PH_N; ++k) atomicAdd(&P.timers[k], ph_acc[k]);
+        for (int k = 0; k < PH_N; ++k) atomicAdd(&P.timers[k], sh.ph_acc[ph_row][k]);
     named_sync<NSYNC_>(BAR_D);
     // ---- write the CTA's state back (consumers) and the rank control (scalar warp)
     if (warp < NWC_) {

@@ -417,6 +417,7 @@ int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl, bool bina
         if (v == 256 || (v == 512 && cl_words == 0)) pl.ntc = v;
     }
     if (t_plan_wss2) pl.ntc = NT;
+    if (pl.bin_words > 0 || cache_slots > 0) pl.ntc = NT;   // (not compiled into the 16-warp kernels)
     pl.rpt = pl.state_cap <= pl.ntc ? 1 : (pl.state_cap <= 2 * pl.ntc ? 2 : 4);
     if (const char* e = getenv("SVMB200_RPT")) {          // tuning override: 1, 2 or 4
         const int r = atoi(e);

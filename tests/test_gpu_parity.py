@@ -644,11 +644,28 @@ def test_predict_tensor_row_factor_fallback(S, monkeypatch, w5_small_model):
                                              ("W3", 1500, 2, 0), ("W5", 2500, 3, 17)])
 def test_wide_poll_parity(S, monkeypatch, name, n, vr, ctas):
     """The wide record poll (every consumer thread polls a slice of the records; the
-    automatic choice above 160 records, i.e. several GPUs) forced on one GPU: the same
+    automatic choice above 320 records, i.e. three or more GPUs) forced on one GPU: the same
     trajectory, alpha, f and b as the oracle, with virtual ranks and ragged CTA counts."""
     monkeypatch.setenv("SVMB200_WIDE_POLL", "1")
     w = W.get(name)
     X, y = w.train(n)
     r_g, r_or = _run_pair(S, w, X, y, virtual_ranks=vr, ctas=ctas, cluster=-1)
-    assert S.last_plan()["cluster"] == 0
+    assert S.last_plan()["cluster"] == 0 and S.last_plan()["poll"] == "wide"
+    _assert_exact(r_g, r_or)
+
+
+@pytest.mark.parametrize("name,n", [("W5", 2500), ("W4", 6000)])
+def test_record_duplication_hook(S, monkeypatch, name, n):
+    """SVMB200_XCH_DUP = 8 stores every record in 8 slots (one GPU then polls the 1,184
+    records of an 8-GPU exchange, a timing aid): the wide poll is chosen automatically and
+    the result still equals the oracle bit for bit; with the wide poll forced off, too."""
+    monkeypatch.setenv("SVMB200_XCH_DUP", "8")
+    w = W.get(name)
+    X, y = w.train(n)
+    r_g, r_or = _run_pair(S, w, X, y, cluster=-1)
+    assert S.last_plan()["poll"] == "wide"
+    _assert_exact(r_g, r_or)
+    monkeypatch.setenv("SVMB200_WIDE_POLL", "0")
+    r_g, r_or = _run_pair(S, w, X, y, cluster=-1)
+    assert S.last_plan()["poll"] == "warp"
     _assert_exact(r_g, r_or)
