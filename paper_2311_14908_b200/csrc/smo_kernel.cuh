@@ -749,19 +749,22 @@ __device__ __forceinline__ void dict_rows(int kc, const unsigned char* stb, int 
 // is short (instruction-cache resident).
 // WIDE: the consumer warps poll the exchange records (several GPUs: > 320 records; a
 // separate instantiation, since its registers slow the single-GPU kernels)
-template <int KERNEL, int RPT, bool A_SMEM, bool BINCL, int NTC = NT, bool WSS2 = false, bool WIDE = false>
+// MIX: mixed compact rows only (no cluster exchange, Gram, row cache, dictionary or dense rows
+// compiled in): the 16-warp W4 kernel, whose row pass is register-bound
+template <int KERNEL, int RPT, bool A_SMEM, bool BINCL, int NTC = NT, bool WSS2 = false, bool WIDE = false,
+          bool MIX = false>
 __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
     // NTC consumer threads (8 or 16 warps), then the scalar and the producer warp
     constexpr int NT_ = NTC, NWC_ = NTC / 32, SCALAR_ = NWC_, PRODUCER_ = NWC_ + 1;
     constexpr int NTHREADS_ = NTC + 64, NSYNC_ = NTC + 32;
     static_assert(NWC_ <= 16, "at most 16 consumer warps");
     // mode switches: compile-time constants in the BINCL specialisation
-    const bool m_cluster = BINCL || P.cluster != 0;
+    const bool m_cluster = BINCL || (!MIX && P.cluster != 0);
     // (the 16-warp instantiations never hold binary-resident rows or a row cache: the plan
     // takes 8 warps for those, and compiling them out spares the row pass registers)
-    const bool m_isbin = BINCL || (NTC != 512 && P.bin_words > 0);
-    const double* const m_gram = BINCL ? nullptr : P.gram;
-    const int m_cache = (BINCL || NTC == 512) ? 0 : P.cache_slots;
+    const bool m_isbin = BINCL || (!MIX && NTC == NT && P.bin_words > 0);
+    const double* const m_gram = (BINCL || MIX) ? nullptr : P.gram;
+    const int m_cache = (BINCL || NTC != NT || MIX) ? 0 : P.cache_slots;
     const bool m_resident = BINCL || P.resident != 0;
     constexpr bool m_wss2 = WSS2 && !BINCL;                 // second-order working set (NEXT-2):
                                                             // its own instantiations, so the
@@ -773,13 +776,13 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
     double2* piv = reinterpret_cast<double2*>(smem_raw + off); off += (size_t)P.dp * 16;
     // mixed rows: the pivots in the compact form (continuous pairs, then the bit words of
     // x_up and of x_low)
-    const bool m_mixed = !BINCL && P.mix_nseg > 0;
+    const bool m_mixed = MIX || (!BINCL && P.mix_nseg > 0);
     double2* pivm = reinterpret_cast<double2*>(smem_raw + off);
     if (m_mixed) off += (size_t)P.mix_nc * 16;
     uint32_t* pbits = reinterpret_cast<uint32_t*>(smem_raw + off);
     if (m_mixed) off += (((size_t)2 * P.mix_nbw * 4) + 15) & ~size_t(15);
     // dictionary-coded rows: the values of the codes (fp64) and the element size of xblk
-    const bool m_dict = !BINCL && P.dict_n > 0;
+    const bool m_dict = !BINCL && !MIX && P.dict_n > 0;
     const int esz = m_dict ? 1 : 4;
     double* dict_s = reinterpret_cast<double*>(smem_raw + off);
     if (m_dict) off += 256 * 8;
@@ -1149,9 +1152,9 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
                     const int wjl = lane < NWC_ ? sh.red_i[1][lane] : INT_MAX;
                     unsigned long long kwu, kwl;
                     unsigned iwu, iwl;
-                    argmin_redux(0xffffffffu, wju == INT_MAX ? ~0ull : fkey(sh.red_f[0][lane & (NWC_ - 1)]),
+                    argmin_redux(0xffffffffu, wju == INT_MAX ? ~0ull : fkey(sh.red_f[0][min(lane, NWC_ - 1)]),
                                  wju == INT_MAX ? 0xffffffffu : (unsigned)wju, kwu, iwu);
-                    argmin_redux(0xffffffffu, wjl == INT_MAX ? ~0ull : ~fkey(sh.red_f[1][lane & (NWC_ - 1)]),
+                    argmin_redux(0xffffffffu, wjl == INT_MAX ? ~0ull : ~fkey(sh.red_f[1][min(lane, NWC_ - 1)]),
                                  wjl == INT_MAX ? 0xffffffffu : (unsigned)wjl, kwl, iwl);
                     ju = iwu == 0xffffffffu ? INT_MAX : (int)iwu;
                     jl = iwl == 0xffffffffu ? INT_MAX : (int)iwl;

@@ -415,6 +415,9 @@ int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl, bool bina
     if (const char* e = getenv("SVMB200_NT")) {                  // tuning override: 256 or 512
         const int v = atoi(e);
         if (v == 256 || (v == 512 && cl_words == 0)) pl.ntc = v;
+        // (448: 14 consumer warps + 2 = 16 warps, 4 per SM sub-partition -> 128 registers per
+        // thread instead of 96; mixed rows only, tuning)
+        if (v == 448 && cl_words == 0 && pl.mix_nseg > 0) pl.ntc = v;
     }
     if (t_plan_wss2) pl.ntc = NT;
     if (pl.bin_words > 0 || cache_slots > 0) pl.ntc = NT;   // (not compiled into the 16-warp kernels)
@@ -423,7 +426,7 @@ int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl, bool bina
         const int r = atoi(e);
         if (r == 1 || r == 2 || r == 4) pl.rpt = r;
     }
-    if (pl.ntc == 512 && pl.rpt == 4) pl.rpt = 2;          // register budget of 576 threads
+    if (pl.ntc > NT && pl.rpt == 4) pl.rpt = 2;           // register budget of 576 threads
     pl.rt = pl.ntc * pl.rpt;
     // Stage size: the largest kc (features per stage) whose zero padding of d stays small and
     // for which two stages fit next to the state -- fewer, larger bulk copies amortise the
@@ -506,7 +509,15 @@ int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl, bool bina
 typedef void (*KernelFn)(const Params);
 
 template <int K, bool W>
-KernelFn pick_rpt_w(int rpt, bool a_smem, int ntc) {
+KernelFn pick_rpt_w(int rpt, bool a_smem, int ntc, bool mix = false) {
+    if (ntc == 448 && mix) {
+        if (a_smem) return rpt == 2 ? smo_persistent<K, 2, true, false, 448, false, W, true> : smo_persistent<K, 1, true, false, 448, false, W, true>;
+        return rpt == 2 ? smo_persistent<K, 2, false, false, 448, false, W, true> : smo_persistent<K, 1, false, false, 448, false, W, true>;
+    }
+    if (ntc == 512 && mix) {
+        if (a_smem) return rpt == 2 ? smo_persistent<K, 2, true, false, 512, false, W, true> : smo_persistent<K, 1, true, false, 512, false, W, true>;
+        return rpt == 2 ? smo_persistent<K, 2, false, false, 512, false, W, true> : smo_persistent<K, 1, false, false, 512, false, W, true>;
+    }
     if (ntc == 512) {
         if (a_smem) return rpt == 2 ? smo_persistent<K, 2, true, false, 512, false, W> : smo_persistent<K, 1, true, false, 512, false, W>;
         return rpt == 2 ? smo_persistent<K, 2, false, false, 512, false, W> : smo_persistent<K, 1, false, false, 512, false, W>;
@@ -517,24 +528,24 @@ KernelFn pick_rpt_w(int rpt, bool a_smem, int ntc) {
 
 // wide: the consumer-warp record poll (WIDE instantiations; not for wss 2)
 template <int K>
-KernelFn pick_rpt(int rpt, bool a_smem, int ntc, bool wss2 = false, bool wide = false) {
+KernelFn pick_rpt(int rpt, bool a_smem, int ntc, bool wss2 = false, bool wide = false, bool mix = false) {
     if (wss2) {                                            // second-order selection: 256 consumers
         if (a_smem) return rpt == 4 ? smo_persistent<K, 4, true, false, NT, true> : rpt == 2 ? smo_persistent<K, 2, true, false, NT, true> : smo_persistent<K, 1, true, false, NT, true>;
         return rpt == 4 ? smo_persistent<K, 4, false, false, NT, true> : rpt == 2 ? smo_persistent<K, 2, false, false, NT, true> : smo_persistent<K, 1, false, false, NT, true>;
     }
-    return wide ? pick_rpt_w<K, true>(rpt, a_smem, ntc) : pick_rpt_w<K, false>(rpt, a_smem, ntc);
+    return wide ? pick_rpt_w<K, true>(rpt, a_smem, ntc, mix) : pick_rpt_w<K, false>(rpt, a_smem, ntc, mix);
 }
 
 KernelFn pick_bincl(int kernel) { return kernel == SVM_RBF ? smo_bincl<1> : smo_bincl<0>; }
 
 // bincl: binary rows resident in a cluster (the specialised kernel; rpt is 1 there)
 KernelFn pick_kernel(int kernel, int rpt, bool a_smem, bool bincl = false, int ntc = NT, bool wss2 = false,
-                     bool wide = false) {
+                     bool wide = false, bool mix = false) {
     if (bincl && getenv("SVMB200_NO_SPECIALISE") == nullptr) {
         if (kernel == SVM_RBF) return a_smem ? smo_persistent<1, 1, true, true> : smo_persistent<1, 1, false, true>;
         return a_smem ? smo_persistent<0, 1, true, true> : smo_persistent<0, 1, false, true>;
     }
-    return kernel == SVM_RBF ? pick_rpt<1>(rpt, a_smem, ntc, wss2, wide) : pick_rpt<0>(rpt, a_smem, ntc, wss2, wide);
+    return kernel == SVM_RBF ? pick_rpt<1>(rpt, a_smem, ntc, wss2, wide, mix) : pick_rpt<0>(rpt, a_smem, ntc, wss2, wide, mix);
 }
 
 int device_limits(int* n_sm, int* max_smem) {
@@ -783,9 +794,14 @@ int solve(SolveArgs& a) {
     bool wide = n_records > 320;
     if (const char* e = getenv("SVMB200_WIDE_POLL")) wide = atoi(e) != 0;
     wide = wide && p.wss != 2 && pl.cluster == 0 && !pl.bincl;
+    // the mixed-rows-only 16-warp instantiation (W4): no other mode compiled in
+    const bool mix_only = pl.ntc > NT && pl.mix_nseg > 0 && pl.cluster == 0 && !pl.bincl && gram == nullptr &&
+                          pl.cache_slots == 0 && pl.bin_words == 0 && p.wss != 2 && pl.esz == 4 &&
+                          getenv("SVMB200_NO_SPECIALISE") == nullptr;
+    if (pl.ntc == 448 && !mix_only) return fail(SVM_EINVAL, "SVMB200_NT=448 is for the mixed-rows kernel only");
     KernelFn fn = pl.bincl ? pick_bincl(p.kernel)
                            : pick_kernel(p.kernel, pl.rpt, pl.alpha_smem, pl.cluster > 0 && pl.bin_words > 0, pl.ntc,
-                                         p.wss == 2, wide);
+                                         p.wss == 2, wide, mix_only);
     const int nthreads = pl.bincl ? NTB : pl.ntc + 64;
     {
         const char* mode = gram ? "gram" : pl.bin_words ? "binary-resident"
@@ -799,7 +815,7 @@ int solve(SolveArgs& a) {
                  "\"poll\": \"%s\"}",
                  pl.bincl ? "smo_bincl" : "smo_persistent", p.kernel,
                  pl.bincl ? "" : (std::string(",") + std::to_string(pl.rpt) + (pl.alpha_smem ? ",1" : ",0") +
-                                  ((pl.cluster > 0 && pl.bin_words > 0) ? ",1" : ",0")).c_str(),
+                                  ((pl.cluster > 0 && pl.bin_words > 0) ? ",1" : ",0") + (mix_only ? ",mix" : "")).c_str(),
                  a.ctas_per_rank, a.nranks_here, pl.cluster, mode, nthreads, pl.smem, pl.state_cap, pl.cache_slots,
                  pl.cluster > 0 || pl.bincl ? "cluster" : wide ? "wide" : "warp");
         g_plan = buf;

@@ -669,3 +669,21 @@ def test_record_duplication_hook(S, monkeypatch, name, n):
     r_g, r_or = _run_pair(S, w, X, y, cluster=-1)
     assert S.last_plan()["poll"] == "warp"
     _assert_exact(r_g, r_or)
+
+
+@pytest.mark.parametrize("nt", ["448", "512"])
+def test_mixed_rows_only_kernel(S, monkeypatch, nt):
+    """The mixed-rows-only 16-warp instantiations (MIX; 512 consumer threads, or 448 so the
+    16 warps get 128 registers each) equal the oracle on mixed compact rows, RBF and linear,
+    with ragged tiles; SVMB200_NO_SPECIALISE gives the general kernel the same result."""
+    monkeypatch.setenv("SVMB200_NT", nt)
+    for name, n, kern in (("W4", 5000, None), ("W4", 3333, O.LINEAR)):
+        w = W.get(name)
+        if kern is not None:
+            import dataclasses
+            w = dataclasses.replace(w, kernel=kern)
+        X, y = w.train(n)
+        r_g, r_or = _run_pair(S, w, X, y, cluster=-1, cache_rows=-1)
+        _assert_exact(r_g, r_or)
+        plan = S.last_plan()
+        assert plan["threads"] == int(nt) + 64 and plan["kernel"].endswith(",mix>"), plan
