@@ -749,22 +749,23 @@ __device__ __forceinline__ void dict_rows(int kc, const unsigned char* stb, int 
 // is short (instruction-cache resident).
 // WIDE: the consumer warps poll the exchange records (several GPUs: > 320 records; a
 // separate instantiation, since its registers slow the single-GPU kernels)
-// MIX: mixed compact rows only (no cluster exchange, Gram, row cache, dictionary or dense rows
-// compiled in): the 16-warp W4 kernel, whose row pass is register-bound
+// SPEC: 0 every mode; 1 mixed compact rows only, 2 dense streamed fp32 rows only (no cluster
+// exchange, Gram, row cache, binary, dictionary or other row format compiled in) -- the W4
+// and W5 kernels, whose row passes pay for the registers of modes they never take
 template <int KERNEL, int RPT, bool A_SMEM, bool BINCL, int NTC = NT, bool WSS2 = false, bool WIDE = false,
-          bool MIX = false>
+          int SPEC = 0>
 __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
     // NTC consumer threads (8 or 16 warps), then the scalar and the producer warp
     constexpr int NT_ = NTC, NWC_ = NTC / 32, SCALAR_ = NWC_, PRODUCER_ = NWC_ + 1;
     constexpr int NTHREADS_ = NTC + 64, NSYNC_ = NTC + 32;
     static_assert(NWC_ <= 16, "at most 16 consumer warps");
     // mode switches: compile-time constants in the BINCL specialisation
-    const bool m_cluster = BINCL || (!MIX && P.cluster != 0);
+    const bool m_cluster = BINCL || (SPEC == 0 && P.cluster != 0);
     // (the 16-warp instantiations never hold binary-resident rows or a row cache: the plan
     // takes 8 warps for those, and compiling them out spares the row pass registers)
-    const bool m_isbin = BINCL || (!MIX && NTC == NT && P.bin_words > 0);
-    const double* const m_gram = (BINCL || MIX) ? nullptr : P.gram;
-    const int m_cache = (BINCL || NTC != NT || MIX) ? 0 : P.cache_slots;
+    const bool m_isbin = BINCL || (SPEC == 0 && NTC == NT && P.bin_words > 0);
+    const double* const m_gram = (BINCL || SPEC != 0) ? nullptr : P.gram;
+    const int m_cache = (BINCL || NTC != NT || SPEC != 0) ? 0 : P.cache_slots;
     const bool m_resident = BINCL || P.resident != 0;
     constexpr bool m_wss2 = WSS2 && !BINCL;                 // second-order working set (NEXT-2):
                                                             // its own instantiations, so the
@@ -776,13 +777,13 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
     double2* piv = reinterpret_cast<double2*>(smem_raw + off); off += (size_t)P.dp * 16;
     // mixed rows: the pivots in the compact form (continuous pairs, then the bit words of
     // x_up and of x_low)
-    const bool m_mixed = MIX || (!BINCL && P.mix_nseg > 0);
+    const bool m_mixed = SPEC == 1 || (SPEC == 0 && !BINCL && P.mix_nseg > 0);
     double2* pivm = reinterpret_cast<double2*>(smem_raw + off);
     if (m_mixed) off += (size_t)P.mix_nc * 16;
     uint32_t* pbits = reinterpret_cast<uint32_t*>(smem_raw + off);
     if (m_mixed) off += (((size_t)2 * P.mix_nbw * 4) + 15) & ~size_t(15);
     // dictionary-coded rows: the values of the codes (fp64) and the element size of xblk
-    const bool m_dict = !BINCL && !MIX && P.dict_n > 0;
+    const bool m_dict = !BINCL && SPEC == 0 && P.dict_n > 0;
     const int esz = m_dict ? 1 : 4;
     double* dict_s = reinterpret_cast<double*>(smem_raw + off);
     if (m_dict) off += 256 * 8;

@@ -687,3 +687,18 @@ def test_mixed_rows_only_kernel(S, monkeypatch, nt):
         _assert_exact(r_g, r_or)
         plan = S.last_plan()
         assert plan["threads"] == int(nt) + 64 and plan["kernel"].endswith(",mix>"), plan
+
+
+@pytest.mark.parametrize("spec", ["1", None])
+def test_dense_only_kernel(S, monkeypatch, spec):
+    """The dense-streamed-only 8-warp instantiation (SPEC 2, W5's kernel) and, with
+    SVMB200_NO_SPECIALISE, the general one both equal the oracle on streamed fp32 rows
+    (RBF, and linear with virtual ranks)."""
+    if spec:
+        monkeypatch.setenv("SVMB200_NO_SPECIALISE", spec)
+    import dataclasses
+    for w, n, vr in ((W.get("W5"), 2600, 1), (dataclasses.replace(W.get("W5"), kernel=O.LINEAR), 1800, 2)):
+        X, y = w.train(n)
+        r_g, r_or = _run_pair(S, w, X, y, cluster=-1, cache_rows=-1, virtual_ranks=vr)
+        _assert_exact(r_g, r_or)
+        assert S.last_plan()["kernel"].endswith(",dense>") == (spec is None), S.last_plan()
