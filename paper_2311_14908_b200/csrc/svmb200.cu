@@ -510,8 +510,10 @@ typedef void (*KernelFn)(const Params);
 
 template <int K, bool W>
 KernelFn pick_rpt_w(int rpt, bool a_smem, int ntc, bool mix = false, bool dense = false) {
-    if (ntc == NT && dense && !a_smem && rpt >= 2)
+    if (ntc == NT && dense && rpt >= 2) {
+        if (a_smem) return rpt == 4 ? smo_persistent<K, 4, true, false, NT, false, W, 2> : smo_persistent<K, 2, true, false, NT, false, W, 2>;
         return rpt == 4 ? smo_persistent<K, 4, false, false, NT, false, W, 2> : smo_persistent<K, 2, false, false, NT, false, W, 2>;
+    }
     if (ntc == 448 && mix) {
         if (a_smem) return rpt == 2 ? smo_persistent<K, 2, true, false, 448, false, W, 1> : smo_persistent<K, 1, true, false, 448, false, W, 1>;
         return rpt == 2 ? smo_persistent<K, 2, false, false, 448, false, W, 1> : smo_persistent<K, 1, false, false, 448, false, W, 1>;
@@ -806,7 +808,7 @@ int solve(SolveArgs& a) {
     // the dense-streamed-only 8-warp instantiation (W5 and its shards)
     const bool dense_only = pl.ntc == NT && pl.mix_nseg == 0 && pl.esz == 4 && pl.cluster == 0 && !pl.bincl &&
                             gram == nullptr && pl.cache_slots == 0 && pl.bin_words == 0 && p.wss != 2 &&
-                            !pl.alpha_smem && pl.rpt >= 2 && getenv("SVMB200_NO_SPECIALISE") == nullptr;
+                            pl.rpt >= 2 && getenv("SVMB200_NO_SPECIALISE") == nullptr;
     KernelFn fn = pl.bincl ? pick_bincl(p.kernel)
                            : pick_kernel(p.kernel, pl.rpt, pl.alpha_smem, pl.cluster > 0 && pl.bin_words > 0, pl.ntc,
                                          p.wss == 2, wide, mix_only, dense_only);

@@ -697,8 +697,11 @@ def test_dense_only_kernel(S, monkeypatch, spec):
     if spec:
         monkeypatch.setenv("SVMB200_NO_SPECIALISE", spec)
     import dataclasses
-    for w, n, vr in ((W.get("W5"), 2600, 1), (dataclasses.replace(W.get("W5"), kernel=O.LINEAR), 1800, 2)):
+    # (few CTAs, so each holds >= 2 rows per consumer thread: the instantiations with
+    # RPT 2 and 4; alpha in shared memory (<= 2048 rows per CTA) and in HBM)
+    for w, n, vr, ctas in ((W.get("W5"), 2600, 1, 4), (W.get("W5"), 5000, 1, 2),
+                           (dataclasses.replace(W.get("W5"), kernel=O.LINEAR), 1800, 2, 4)):
         X, y = w.train(n)
-        r_g, r_or = _run_pair(S, w, X, y, cluster=-1, cache_rows=-1, virtual_ranks=vr)
+        r_g, r_or = _run_pair(S, w, X, y, cluster=-1, cache_rows=-1, virtual_ranks=vr, ctas=ctas)
         _assert_exact(r_g, r_or)
         assert S.last_plan()["kernel"].endswith(",dense>") == (spec is None), S.last_plan()
