@@ -750,8 +750,9 @@ __device__ __forceinline__ void dict_rows(int kc, const unsigned char* stb, int 
 // WIDE: the consumer warps poll the exchange records (several GPUs: > 320 records; a
 // separate instantiation, since its registers slow the single-GPU kernels)
 // SPEC: 0 every mode; 1 mixed compact rows only, 2 dense streamed fp32 rows only (no cluster
-// exchange, Gram, row cache, binary, dictionary or other row format compiled in) -- the W4
-// and W5 kernels, whose row passes pay for the registers of modes they never take
+// exchange, Gram, row cache, binary, dictionary or other row format compiled in), 3
+// dictionary rows with or without the row cache -- the W4, W5 and W3 kernels, whose row
+// passes pay for the registers of modes they never take
 template <int KERNEL, int RPT, bool A_SMEM, bool BINCL, int NTC = NT, bool WSS2 = false, bool WIDE = false,
           int SPEC = 0>
 __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
@@ -765,7 +766,7 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
     // takes 8 warps for those, and compiling them out spares the row pass registers)
     const bool m_isbin = BINCL || (SPEC == 0 && NTC == NT && P.bin_words > 0);
     const double* const m_gram = (BINCL || SPEC != 0) ? nullptr : P.gram;
-    const int m_cache = (BINCL || NTC != NT || SPEC != 0) ? 0 : P.cache_slots;
+    const int m_cache = (BINCL || NTC != NT || SPEC == 1 || SPEC == 2) ? 0 : P.cache_slots;
     const bool m_resident = BINCL || P.resident != 0;
     constexpr bool m_wss2 = WSS2 && !BINCL;                 // second-order working set (NEXT-2):
                                                             // its own instantiations, so the
@@ -783,7 +784,7 @@ __global__ void __launch_bounds__(NTC + 64, 1) smo_persistent(const Params P) {
     uint32_t* pbits = reinterpret_cast<uint32_t*>(smem_raw + off);
     if (m_mixed) off += (((size_t)2 * P.mix_nbw * 4) + 15) & ~size_t(15);
     // dictionary-coded rows: the values of the codes (fp64) and the element size of xblk
-    const bool m_dict = !BINCL && SPEC == 0 && P.dict_n > 0;
+    const bool m_dict = SPEC == 3 || (!BINCL && SPEC == 0 && P.dict_n > 0);
     const int esz = m_dict ? 1 : 4;
     double* dict_s = reinterpret_cast<double*>(smem_raw + off);
     if (m_dict) off += 256 * 8;

@@ -509,7 +509,11 @@ int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl, bool bina
 typedef void (*KernelFn)(const Params);
 
 template <int K, bool W>
-KernelFn pick_rpt_w(int rpt, bool a_smem, int ntc, bool mix = false, bool dense = false) {
+KernelFn pick_rpt_w(int rpt, bool a_smem, int ntc, bool mix = false, bool dense = false, bool dict = false) {
+    if (ntc == NT && dict && !W && rpt >= 2) {
+        if (a_smem) return rpt == 4 ? smo_persistent<K, 4, true, false, NT, false, false, 3> : smo_persistent<K, 2, true, false, NT, false, false, 3>;
+        return rpt == 4 ? smo_persistent<K, 4, false, false, NT, false, false, 3> : smo_persistent<K, 2, false, false, NT, false, false, 3>;
+    }
     if (ntc == NT && dense && rpt >= 2) {
         if (a_smem) return rpt == 4 ? smo_persistent<K, 4, true, false, NT, false, W, 2> : smo_persistent<K, 2, true, false, NT, false, W, 2>;
         return rpt == 4 ? smo_persistent<K, 4, false, false, NT, false, W, 2> : smo_persistent<K, 2, false, false, NT, false, W, 2>;
@@ -533,25 +537,25 @@ KernelFn pick_rpt_w(int rpt, bool a_smem, int ntc, bool mix = false, bool dense 
 // wide: the consumer-warp record poll (WIDE instantiations; not for wss 2)
 template <int K>
 KernelFn pick_rpt(int rpt, bool a_smem, int ntc, bool wss2 = false, bool wide = false, bool mix = false,
-                  bool dense = false) {
+                  bool dense = false, bool dict = false) {
     if (wss2) {                                            // second-order selection: 256 consumers
         if (a_smem) return rpt == 4 ? smo_persistent<K, 4, true, false, NT, true> : rpt == 2 ? smo_persistent<K, 2, true, false, NT, true> : smo_persistent<K, 1, true, false, NT, true>;
         return rpt == 4 ? smo_persistent<K, 4, false, false, NT, true> : rpt == 2 ? smo_persistent<K, 2, false, false, NT, true> : smo_persistent<K, 1, false, false, NT, true>;
     }
-    return wide ? pick_rpt_w<K, true>(rpt, a_smem, ntc, mix, dense) : pick_rpt_w<K, false>(rpt, a_smem, ntc, mix, dense);
+    return wide ? pick_rpt_w<K, true>(rpt, a_smem, ntc, mix, dense) : pick_rpt_w<K, false>(rpt, a_smem, ntc, mix, dense, dict);
 }
 
 KernelFn pick_bincl(int kernel) { return kernel == SVM_RBF ? smo_bincl<1> : smo_bincl<0>; }
 
 // bincl: binary rows resident in a cluster (the specialised kernel; rpt is 1 there)
 KernelFn pick_kernel(int kernel, int rpt, bool a_smem, bool bincl = false, int ntc = NT, bool wss2 = false,
-                     bool wide = false, bool mix = false, bool dense = false) {
+                     bool wide = false, bool mix = false, bool dense = false, bool dict = false) {
     if (bincl && getenv("SVMB200_NO_SPECIALISE") == nullptr) {
         if (kernel == SVM_RBF) return a_smem ? smo_persistent<1, 1, true, true> : smo_persistent<1, 1, false, true>;
         return a_smem ? smo_persistent<0, 1, true, true> : smo_persistent<0, 1, false, true>;
     }
-    return kernel == SVM_RBF ? pick_rpt<1>(rpt, a_smem, ntc, wss2, wide, mix, dense)
-                             : pick_rpt<0>(rpt, a_smem, ntc, wss2, wide, mix, dense);
+    return kernel == SVM_RBF ? pick_rpt<1>(rpt, a_smem, ntc, wss2, wide, mix, dense, dict)
+                             : pick_rpt<0>(rpt, a_smem, ntc, wss2, wide, mix, dense, dict);
 }
 
 int device_limits(int* n_sm, int* max_smem) {
@@ -809,9 +813,13 @@ int solve(SolveArgs& a) {
     const bool dense_only = pl.ntc == NT && pl.mix_nseg == 0 && pl.esz == 4 && pl.cluster == 0 && !pl.bincl &&
                             gram == nullptr && pl.cache_slots == 0 && pl.bin_words == 0 && p.wss != 2 &&
                             pl.rpt >= 2 && getenv("SVMB200_NO_SPECIALISE") == nullptr;
+    // the dictionary-rows-only 8-warp instantiation (W3; with or without the row cache)
+    const bool dict_only = pl.ntc == NT && pl.esz == 1 && pl.mix_nseg == 0 && pl.cluster == 0 && !pl.bincl &&
+                           gram == nullptr && pl.bin_words == 0 && p.wss != 2 && !wide && pl.rpt >= 2 &&
+                           getenv("SVMB200_NO_SPECIALISE") == nullptr;
     KernelFn fn = pl.bincl ? pick_bincl(p.kernel)
                            : pick_kernel(p.kernel, pl.rpt, pl.alpha_smem, pl.cluster > 0 && pl.bin_words > 0, pl.ntc,
-                                         p.wss == 2, wide, mix_only, dense_only);
+                                         p.wss == 2, wide, mix_only, dense_only, dict_only);
     const int nthreads = pl.bincl ? NTB : pl.ntc + 64;
     {
         const char* mode = gram ? "gram" : pl.bin_words ? "binary-resident"
@@ -825,7 +833,7 @@ int solve(SolveArgs& a) {
                  "\"poll\": \"%s\"}",
                  pl.bincl ? "smo_bincl" : "smo_persistent", p.kernel,
                  pl.bincl ? "" : (std::string(",") + std::to_string(pl.rpt) + (pl.alpha_smem ? ",1" : ",0") +
-                                  ((pl.cluster > 0 && pl.bin_words > 0) ? ",1" : ",0") + (mix_only ? ",mix" : dense_only ? ",dense" : "")).c_str(),
+                                  ((pl.cluster > 0 && pl.bin_words > 0) ? ",1" : ",0") + (mix_only ? ",mix" : dense_only ? ",dense" : dict_only ? ",dict" : "")).c_str(),
                  a.ctas_per_rank, a.nranks_here, pl.cluster, mode, nthreads, pl.smem, pl.state_cap, pl.cache_slots,
                  pl.cluster > 0 || pl.bincl ? "cluster" : wide ? "wide" : "warp");
         g_plan = buf;

@@ -705,3 +705,19 @@ def test_dense_only_kernel(S, monkeypatch, spec):
         r_g, r_or = _run_pair(S, w, X, y, cluster=-1, cache_rows=-1, virtual_ranks=vr, ctas=ctas)
         _assert_exact(r_g, r_or)
         assert S.last_plan()["kernel"].endswith(",dense>") == (spec is None), S.last_plan()
+
+
+@pytest.mark.parametrize("cache", [-1, 0])
+def test_dict_only_kernel(S, monkeypatch, cache):
+    """The dictionary-rows-only 8-warp instantiation (SPEC 3, W3's kernel), with and
+    without the row cache, equals the oracle (W3 subset, few CTAs so each thread holds
+    >= 2 rows); the general kernel (SVMB200_NO_SPECIALISE) gives the same result."""
+    w = W.get("W3")
+    X, y = w.train(2000)
+    r_g, r_or = _run_pair(S, w, X, y, cluster=-1, cache_rows=cache, ctas=3)
+    _assert_exact(r_g, r_or)
+    assert S.last_plan()["kernel"].endswith(",dict>"), S.last_plan()
+    monkeypatch.setenv("SVMB200_NO_SPECIALISE", "1")
+    r_g2 = S.svm_train_ex(X, y, w.C, w.kernel, w.gamma, w.tol, cluster=-1, cache_rows=cache, ctas=3)
+    assert not S.last_plan()["kernel"].endswith(",dict>")
+    assert np.array_equal(r_g2["alpha"], r_g["alpha"]) and r_g2["b"] == r_g["b"]
