@@ -4,8 +4,8 @@
 //   RBF:    K = exp(-gamma (|t|^2 + |s|^2 - 2 t.s)),  linear: K = t.s
 //
 // The contraction T * SV^T (m x n_sv x d) is a dense GEMM that is never materialised:
-// each CTA owns 128 test rows, streams the support vectors in tiles of 128, and the
-// epilogue turns every 128 x 128 accumulator tile into kernel values and reduces it
+// each CTA owns 128 test rows, streams the support vectors in tiles of BN (256), and the
+// epilogue turns every 128 x BN accumulator tile into kernel values and reduces it
 // over the support vectors on the fly.
 //
 //   * operands in "3xTF32": x = hi + lo with hi = x rounded to tf32 and lo = tf32(x - hi);
@@ -13,16 +13,18 @@
 //     accumulator), ~2^-21 relative per product instead of tf32's 2^-11
 //   * operands are pre-packed once into the K-major, no-swizzle core-matrix layout of
 //     tcgen05 shared-memory descriptors (8 rows x 16 bytes per core matrix, LBO = 128 B
-//     between K-adjacent core matrices, SBO = 1024 B between 8-row groups), so every
-//     stage is four contiguous cp.async.bulk copies (A hi/lo, B hi/lo; 16 KB each)
+//     between K-adjacent core matrices, SBO = 8 BK x 4 B between 8-row groups), so every
+//     stage is two contiguous cp.async.bulk copies (A hi|lo, B hi|lo; 48 KB with BN = 256)
 //   * warp roles: warp 0 producer (bulk copies, mbarrier ring), warp 1 MMA issuer (one
-//     thread; TMEM allocation), warps 2-5 epilogue (tcgen05.ld 32x32b, one test row per
-//     thread); two 128-column TMEM accumulators so the epilogue of tile j overlaps the
-//     MMAs of tile j + 1
-//   * epilogue in fp64: D = |t|^2 + |s|^2 - 2 (t.s) from exact fp64 norms, K = exp(-gamma D)
-//     (a table-driven fp64 exp good to a few ulp, exp_nonpos), dec accumulated with fp64
-//     fma -- fp32 there would cost up to 1e-3 on Adult-like data (C = 100, 15 distinct
-//     kernel values, correlated rounding).
+//     thread; TMEM allocation), warps 2-17 epilogue (tcgen05.ld 32x32b, one test row per
+//     thread, 4 warps per TMEM lane quarter); TcCfg: 128 x 256 accumulator tiles, two in
+//     TMEM, so the epilogue of tile j overlaps the MMAs of tile j + 1
+//   * epilogue: x = -gamma (|t|^2 + |s|^2 - 2 t.s) from exact fp64 norms, K = exp(x) with
+//     only what needs fp64 in fp64 (exp_split: fp64 range reduction and final fma, the small
+//     correction polynomial in fp32; relative error < 4e-13), dec accumulated with fp64 fma --
+//     an fp32 exp or sum would cost up to 1e-3 on Adult-like data (C = 100, 15 distinct
+//     kernel values, correlated rounding).  The fp64 pipe is shared with the tensor pipe, so
+//     every fp64 operation of the epilogue is taken from the MMAs.
 // Not bit-exact (tensor cores); parity vs the oracle is BASELINE.json's 1e-4 absolute.
 #pragma once
 
