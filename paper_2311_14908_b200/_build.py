@@ -1,6 +1,7 @@
 """Build libsvmb200.so in-tree with nvcc for sm_100a (no torch extension machinery).
 
-  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo --fmad=false -shared ...
+  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo --fmad=false -c ... (one process
+  per source, in parallel), then nvcc -shared ...
 
 --fmad=false keeps every product and sum the source writes as a separate rounding;
 the kernels request fused multiply-adds explicitly with fma() where the arithmetic
@@ -17,8 +18,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libsvmb200.so")
-SOURCES = ["svmb200.cu", "predict.cu", "comm.cu", "gram.cu", "gd.cu", "finalize.cu", "shrink.cu"]
-HEADERS = ["smo_kernel.cuh", "smo_bincl.cuh", "svm_exp.cuh", "exp_table.inc", "svm_internal.h", "predict_tc.cuh"]
+# (the solver's instantiations are spread over the four smo_*.cu units; every unit compiles
+# in its own nvcc process, in parallel, then one link)
+SOURCES = ["smo_gen_rbf.cu", "smo_gen_lin.cu", "smo_spec_rbf.cu", "smo_spec_lin.cu", "svmb200.cu", "predict.cu",
+           "comm.cu", "gram.cu", "gd.cu", "finalize.cu", "shrink.cu"]
+HEADERS = ["smo_kernel.cuh", "smo_pick.cuh", "smo_bincl.cuh", "svm_exp.cuh", "exp_table.inc", "svm_internal.h",
+           "predict_tc.cuh"]
 
 
 def _nccl_paths():
@@ -48,16 +53,27 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
+    import tempfile
+    from concurrent.futures import ThreadPoolExecutor
     inc, lib = _nccl_paths()
     srcs = [os.path.join(CSRC, f) for f in SOURCES if os.path.exists(os.path.join(CSRC, f))]
-    cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
-           "--fmad=false", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-Xptxas", "-v" if verbose else "-O3",
-           "-I", inc, "-I", os.path.join(ROOT, "include"),
-           "-o", LIB + ".tmp"] + srcs + [
-           "-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + lib, "-lcudart"]
-    cmd = [c for c in cmd if c]
-    subprocess.check_call(cmd)
+    common = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
+              "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
+              "-Xptxas", "-v" if verbose else "-O3",
+              "-I", inc, "-I", os.path.join(ROOT, "include")]
+    with tempfile.TemporaryDirectory(prefix="svmb200_build_") as tmp:
+        objs = [os.path.join(tmp, os.path.basename(f) + ".o") for f in srcs]
+
+        def compile_one(k):
+            subprocess.check_call(common + ["-c", srcs[k], "-o", objs[k]])
+
+        workers = max(1, min(len(srcs), os.cpu_count() or 1))
+        with ThreadPoolExecutor(max_workers=workers) as ex:
+            list(ex.map(compile_one, range(len(srcs))))       # re-raises the first failure
+        link = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
+                "-o", LIB + ".tmp"] + objs + [
+               "-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + lib, "-lcudart"]
+        subprocess.check_call(link)
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

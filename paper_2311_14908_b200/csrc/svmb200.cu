@@ -508,54 +508,31 @@ int make_plan(long long n_r_max, int d, int G, int max_smem, Plan& pl, bool bina
 
 typedef void (*KernelFn)(const Params);
 
-template <int K, bool W>
-KernelFn pick_rpt_w(int rpt, bool a_smem, int ntc, bool mix = false, bool dense = false, bool dict = false) {
-    if (ntc == NT && dict && !W && rpt >= 2) {
-        if (a_smem) return rpt == 4 ? smo_persistent<K, 4, true, false, NT, false, false, 3> : smo_persistent<K, 2, true, false, NT, false, false, 3>;
-        return rpt == 4 ? smo_persistent<K, 4, false, false, NT, false, false, 3> : smo_persistent<K, 2, false, false, NT, false, false, 3>;
-    }
-    if (ntc == NT && dense && rpt >= 2) {
-        if (a_smem) return rpt == 4 ? smo_persistent<K, 4, true, false, NT, false, W, 2> : smo_persistent<K, 2, true, false, NT, false, W, 2>;
-        return rpt == 4 ? smo_persistent<K, 4, false, false, NT, false, W, 2> : smo_persistent<K, 2, false, false, NT, false, W, 2>;
-    }
-    if (ntc == 448 && mix) {
-        if (a_smem) return rpt == 2 ? smo_persistent<K, 2, true, false, 448, false, W, 1> : smo_persistent<K, 1, true, false, 448, false, W, 1>;
-        return rpt == 2 ? smo_persistent<K, 2, false, false, 448, false, W, 1> : smo_persistent<K, 1, false, false, 448, false, W, 1>;
-    }
-    if (ntc == 512 && mix) {
-        if (a_smem) return rpt == 2 ? smo_persistent<K, 2, true, false, 512, false, W, 1> : smo_persistent<K, 1, true, false, 512, false, W, 1>;
-        return rpt == 2 ? smo_persistent<K, 2, false, false, 512, false, W, 1> : smo_persistent<K, 1, false, false, 512, false, W, 1>;
-    }
-    if (ntc == 512) {
-        if (a_smem) return rpt == 2 ? smo_persistent<K, 2, true, false, 512, false, W> : smo_persistent<K, 1, true, false, 512, false, W>;
-        return rpt == 2 ? smo_persistent<K, 2, false, false, 512, false, W> : smo_persistent<K, 1, false, false, 512, false, W>;
-    }
-    if (a_smem) return rpt == 4 ? smo_persistent<K, 4, true, false, NT, false, W> : rpt == 2 ? smo_persistent<K, 2, true, false, NT, false, W> : smo_persistent<K, 1, true, false, NT, false, W>;
-    return rpt == 4 ? smo_persistent<K, 4, false, false, NT, false, W> : rpt == 2 ? smo_persistent<K, 2, false, false, NT, false, W> : smo_persistent<K, 1, false, false, NT, false, W>;
-}
-
-// wide: the consumer-warp record poll (WIDE instantiations; not for wss 2)
-template <int K>
-KernelFn pick_rpt(int rpt, bool a_smem, int ntc, bool wss2 = false, bool wide = false, bool mix = false,
-                  bool dense = false, bool dict = false) {
-    if (wss2) {                                            // second-order selection: 256 consumers
-        if (a_smem) return rpt == 4 ? smo_persistent<K, 4, true, false, NT, true> : rpt == 2 ? smo_persistent<K, 2, true, false, NT, true> : smo_persistent<K, 1, true, false, NT, true>;
-        return rpt == 4 ? smo_persistent<K, 4, false, false, NT, true> : rpt == 2 ? smo_persistent<K, 2, false, false, NT, true> : smo_persistent<K, 1, false, false, NT, true>;
-    }
-    return wide ? pick_rpt_w<K, true>(rpt, a_smem, ntc, mix, dense) : pick_rpt_w<K, false>(rpt, a_smem, ntc, mix, dense, dict);
-}
+// The solver's instantiations live in four translation units compiled in parallel
+// (smo_pick.cuh; smo_{gen,spec}_{rbf,lin}.cu): the general ones (every mode, the second-order
+// rule, the wide poll) and the specialised ones (mixed-, dense- or dictionary-rows only;
+// binary rows in a cluster).
+KernelFn pick_general_rbf(int rpt, bool a_smem, int ntc, bool wss2, bool wide);
+KernelFn pick_general_lin(int rpt, bool a_smem, int ntc, bool wss2, bool wide);
+KernelFn pick_spec_rbf(int rpt, bool a_smem, int ntc, bool wide, bool mix, bool dense, bool dict);
+KernelFn pick_spec_lin(int rpt, bool a_smem, int ntc, bool wide, bool mix, bool dense, bool dict);
+KernelFn pick_bincl_spec_rbf(bool a_smem);
+KernelFn pick_bincl_spec_lin(bool a_smem);
 
 KernelFn pick_bincl(int kernel) { return kernel == SVM_RBF ? smo_bincl<1> : smo_bincl<0>; }
 
 // bincl: binary rows resident in a cluster (the specialised kernel; rpt is 1 there)
 KernelFn pick_kernel(int kernel, int rpt, bool a_smem, bool bincl = false, int ntc = NT, bool wss2 = false,
                      bool wide = false, bool mix = false, bool dense = false, bool dict = false) {
-    if (bincl && getenv("SVMB200_NO_SPECIALISE") == nullptr) {
-        if (kernel == SVM_RBF) return a_smem ? smo_persistent<1, 1, true, true> : smo_persistent<1, 1, false, true>;
-        return a_smem ? smo_persistent<0, 1, true, true> : smo_persistent<0, 1, false, true>;
+    const bool rbf = kernel == SVM_RBF;
+    if (bincl && getenv("SVMB200_NO_SPECIALISE") == nullptr)
+        return rbf ? pick_bincl_spec_rbf(a_smem) : pick_bincl_spec_lin(a_smem);
+    if (!wss2 && (mix || dense || dict)) {
+        KernelFn f = rbf ? pick_spec_rbf(rpt, a_smem, ntc, wide, mix, dense, dict)
+                         : pick_spec_lin(rpt, a_smem, ntc, wide, mix, dense, dict);
+        if (f) return f;
     }
-    return kernel == SVM_RBF ? pick_rpt<1>(rpt, a_smem, ntc, wss2, wide, mix, dense, dict)
-                             : pick_rpt<0>(rpt, a_smem, ntc, wss2, wide, mix, dense, dict);
+    return rbf ? pick_general_rbf(rpt, a_smem, ntc, wss2, wide) : pick_general_lin(rpt, a_smem, ntc, wss2, wide);
 }
 
 int device_limits(int* n_sm, int* max_smem) {
